@@ -1,0 +1,180 @@
+/*
+ * hssmf_b200.h — C-ABI of the B200-native numeric factorization and solve of
+ * the HSS-compressed multifrontal sparse LU (arXiv 1502.07405 reference,
+ * /root/reference/proj). Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * Drop-in boundary: every entry point below replaces one reference interface,
+ * cited as file:line under proj/include/hssmf (or proj/src). The C++ wrappers
+ * in include/hssmf_b200/hssmf.hpp rebuild the reference's value types and
+ * exception classes on top of these calls.
+ *
+ * Conventions
+ *  - matrices are square CSR with sorted, duplicate-free rows, int32 indices
+ *    (SparseMatrix<T>, sparse_matrix.hpp:14-47);
+ *  - dense blocks are column-major with an explicit leading dimension
+ *    (DenseMatrix<T>, dense_matrix.hpp:17-35);
+ *  - every call returns an hssmf_code; failing calls fill *st (may be NULL).
+ */
+#ifndef HSSMF_B200_H
+#define HSSMF_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes; the C++ wrapper maps them to the reference's exception types
+ * (errors.hpp:10-54): SHAPE -> IoError, NOT_FACTORED -> SolverError,
+ * SINGULAR -> SingularMatrixError(front, column), RANK -> HssRankExceeded */
+typedef enum {
+  HSSMF_OK = 0,
+  HSSMF_ERR_SHAPE = 1,
+  HSSMF_ERR_NOT_FACTORED = 2,
+  HSSMF_ERR_SINGULAR = 3,
+  HSSMF_ERR_CUDA = 4,
+  HSSMF_ERR_NCCL = 5,
+  HSSMF_ERR_RANK = 6,
+  HSSMF_ERR_OTHER = 7
+} hssmf_code;
+
+typedef struct {
+  int code;
+  int front;   /* failing front (postorder id) or -1 */
+  int column;  /* zero-pivot column within that front's F11 or -1 */
+  char msg[512];
+} hssmf_status;
+
+/* SolverOptions, numeric subset (solver_options.hpp:28-45). eps is the
+ * relative ID tolerance; the absolute floor is derived per sampling round as
+ * eps * max(|S_r|, |S_c|) exactly like hss_compress.hpp:335-338. */
+typedef struct {
+  int ls;        /* switch level: fronts with level < ls may use HSS */
+  double eps;    /* relative compression tolerance */
+  int leaf;      /* HSS leaf size */
+  int d0, dd, p; /* initial sample columns, increment, oversampling */
+  int min_hss;   /* minimum front dimension for HSS */
+  int max_rank;  /* rank guard, 0 -> min(n/2, 5000) */
+  int mode;      /* 0 auto, 1 mf (pure multifrontal), 2 mf-hss */
+} hssmf_options;
+
+typedef struct hssmf_csr hssmf_csr;
+typedef struct hssmf_tree hssmf_tree;
+typedef struct hssmf_factors hssmf_factors;
+typedef struct hssmf_hss hssmf_hss;
+
+/* ---- host analysis (integer outputs bit-exact with the reference) ---- */
+
+/* generate_grid_problem (grid_problems.hpp:65-117); kind 0 p2d 1 p3d 2 c2d 3 c3d;
+ * dims/ndims receive the GridGeometry (grid_problems.hpp:34-41) */
+int hssmf_csr_grid(int kind, int k, double nu, hssmf_csr** out, int* dims, int* ndims,
+                   hssmf_status* st);
+/* BASELINE config 4: h^2-scaled -lap(u) + beta.grad(u), beta = scale*(1,.5,.25)/h,
+ * upwind coefficients by the reference rule detail::upwind (grid_problems.hpp:57-61) */
+int hssmf_csr_convdiff3d(int k, double scale, hssmf_csr** out, hssmf_status* st);
+/* SparseMatrix(n, ptr, ind, val) (sparse_matrix.hpp:18-22) */
+int hssmf_csr_create(int n, const int* ptr, const int* ind, const double* val,
+                     hssmf_csr** out, hssmf_status* st);
+/* SparseMatrix::permuted (sparse_matrix.hpp:95-102), perm[old] = new */
+int hssmf_csr_permuted(const hssmf_csr* a, const int* perm, hssmf_csr** out, hssmf_status* st);
+void hssmf_csr_info(const hssmf_csr* a, int* n, long long* nnz);
+void hssmf_csr_get(const hssmf_csr* a, int* ptr, int* ind, double* val);
+/* y = A x (SparseMatrix::matvec N, sparse_matrix.hpp:70-86), deterministic row order */
+void hssmf_csr_matvec(const hssmf_csr* a, const double* x, double* y);
+void hssmf_csr_free(hssmf_csr* a);
+
+/* nested_dissection_geometric (ordering.cpp:213-222) followed by
+ * EliminationTree::from_separators (elimination_tree.cpp:10-26); perm[old]=new */
+int hssmf_nd_geometric(const int* dims, int ndims, int leaf, int* perm, hssmf_tree** out,
+                       hssmf_status* st);
+/* EliminationTree with explicit nodes (upd sets optional: upd_ptr may be NULL) */
+int hssmf_tree_create(int n, int nnodes, const int* sep_begin, const int* sep_end,
+                      const int* child0, const int* child1, const int* parent,
+                      const int* upd_ptr, const int* upd_ind, hssmf_tree** out,
+                      hssmf_status* st);
+/* symbolic_factorization(A, t) (elimination_tree.hpp:67-73) */
+int hssmf_symbolic(const hssmf_csr* a, hssmf_tree* t, hssmf_status* st);
+void hssmf_tree_info(const hssmf_tree* t, int* n, int* nnodes, long long* upd_total);
+void hssmf_tree_get(const hssmf_tree* t, int* sep_begin, int* sep_end, int* child0,
+                    int* child1, int* parent, int* level, int* upd_ptr, int* upd_ind);
+void hssmf_tree_free(hssmf_tree* t);
+/* front_cluster_tree (multifrontal.hpp:318-326) via ClusterTree::balanced/join
+ * (cluster_tree.hpp:38-61); returns the node count, arrays may be NULL */
+int hssmf_front_cluster_tree(int ns, int nu, int leaf, int* begin, int* end, int* child0,
+                             int* child1, int* parent);
+
+/* ---- numeric factorization / solve on a B200 ---- */
+
+/* analysis upload + static schedule + numeric factorization:
+ * mf_factor(a, t, opts) (multifrontal.hpp:473-503). a must carry the tree's
+ * ordering. device: CUDA ordinal. */
+int hssmf_factor(int device, const hssmf_csr* a, const hssmf_tree* t, const hssmf_options* o,
+                 hssmf_factors** out, hssmf_status* st);
+/* numeric re-factorization with new values on the same pattern; val is host
+ * (on_device = 0) or device memory, nnz entries in the CSR order of a */
+int hssmf_refactor(hssmf_factors* f, const double* val, int on_device, hssmf_status* st);
+/* mf_solve(m, b) (multifrontal.hpp:612-622): b is n x nrhs column-major with
+ * leading dimension ldb, in the tree ordering, solved in place; host or device */
+int hssmf_solve(hssmf_factors* f, double* b, int ldb, int nrhs, int on_device,
+                hssmf_status* st);
+/* MfFactors::{front_stats, hss_fronts, fallbacks, max_front_rank, factor_nnz()}
+ * (multifrontal.hpp:454-468); type 0 dense 1 hss 2 hss_dense */
+void hssmf_factor_summary(const hssmf_factors* f, int* nnodes, int* hss_fronts,
+                          int* fallbacks, int* max_rank, long long* factor_nnz);
+void hssmf_front_stats(const hssmf_factors* f, int* level, int* dim, int* sep, int* rank,
+                       long long* flops, int* type);
+/* per HSS-tree node u/v ranks of one front (hss_matrix.hpp:210-216) and the
+ * adaptive sampling stats (HssCompressStats, hss_compress.hpp:34-37);
+ * returns the node count (0 for a dense front); arrays may be NULL */
+int hssmf_front_hss(const hssmf_factors* f, int front, int* u_rank, int* v_rank, int* rounds,
+                    int* d_final);
+/* device time of the last factor / solve (CUDA events on the engine stream) */
+void hssmf_timing(const hssmf_factors* f, double* factor_ms, double* solve_ms);
+/* per-kernel-class profile (events around each launch when enabled) */
+void hssmf_set_profile(hssmf_factors* f, int on);
+int hssmf_kernel_stats(const hssmf_factors* f, int max, char* names /* max*32 */,
+                       int* launches, double* ms, double* flops, double* bytes);
+void hssmf_reset_kernel_stats(hssmf_factors* f);
+long long hssmf_device_bytes(const hssmf_factors* f);
+void hssmf_factors_free(hssmf_factors* f);
+
+/* ---- standalone dense HSS (BASELINE config 2) ---- */
+/* hss_compress(A, ClusterTree::balanced(n, leaf), HssOptions) + ulv_factor
+ * (hss_compress.hpp:373-383, hss_ulv.hpp:284-319); a is n x n, lda >= n */
+int hssmf_hss_dense(int device, const double* a, int lda, int n, int leaf, double eps, int d0,
+                    int dd, int p, int max_rank, int on_device, hssmf_hss** out,
+                    hssmf_status* st);
+int hssmf_hss_info(const hssmf_hss* h, int* u_rank, int* v_rank, int* rounds, int* d_final,
+                   double* compress_ms, double* ulv_ms);
+/* UlvFactors::solve (hss_ulv.hpp:150-176) */
+int hssmf_hss_solve(hssmf_hss* h, double* b, int ldb, int nrhs, int on_device,
+                    hssmf_status* st);
+void hssmf_hss_free(hssmf_hss* h);
+
+/* ---- kernel-level entry points used by the parity tests ---- */
+/* SeededRowSampler values R(l, c), c in [c0, c1) for global rows grow[l]
+ * (random_sampler.hpp:19-68) computed by the device generator; out is
+ * nrows x (c1-c0) column-major, host memory */
+int hssmf_dev_random_rows(int device, int nrows, const long long* grow, int c0, int c1,
+                          double* out, hssmf_status* st);
+/* C = alpha op(A) op(B) + beta C on the device DMMA GEMM, host buffers */
+int hssmf_dev_gemm(int device, char ta, char tb, int m, int n, int k, double alpha,
+                   const double* a, int lda, const double* b, int ldb, double beta, double* c,
+                   int ldc, hssmf_status* st);
+/* interpolative_decomposition (rrqr.hpp:175-194) on the device CPQR: y is m x n;
+ * perm (n), rank, certified, coeffs (rank x (n-rank), ld rank) */
+int hssmf_dev_id(int device, const double* y, int m, int n, double eps, int max_rank,
+                 double abs_tol, int* perm, int* rank, int* certified, double* coeffs,
+                 hssmf_status* st);
+/* lu_partial_pivot (lu.hpp:80-85) on the device panel kernels; a is m x n (m>=n) */
+int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st);
+
+/* measurement: average device time (ms) of `iters` m x n x k DGEMMs (NN) on
+ * the DMMA kernel, device-resident operands; used for the FP64 roofline */
+int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st);
+
+const char* hssmf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,531 @@
+"""Python mirror of the reference's public interface for the hot path.
+
+Same names, argument meaning and error behaviour as proj/include/hssmf
+(SparseMatrix, generate_grid_problem, nested_dissection_geometric,
+EliminationTree, symbolic_factorization, SolverOptions, HssOptions,
+mf_factor, mf_solve, mf_solve_new, hss_compress, ulv_factor), implemented on
+top of the C-ABI (include/hssmf_b200.h). Host analysis is native C++; all
+numerics run in sm_100a kernels. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+GRID_KINDS = {"p2d": 0, "p3d": 1, "c2d": 2, "c3d": 3}
+FRONT_TYPES = {0: "dense", 1: "hss", 2: "hss_dense"}
+
+
+# ---- exceptions (errors.hpp:10-54) -----------------------------------------
+class SolverError(RuntimeError):
+    pass
+
+
+class IoError(SolverError):
+    pass
+
+
+class SingularMatrixError(SolverError):
+    def __init__(self, msg, column):
+        super().__init__(msg)
+        self._column = column
+
+    def column(self):
+        return self._column
+
+
+class HssRankExceeded(SolverError):
+    pass
+
+
+class CudaError(SolverError):
+    pass
+
+
+def _check(rc, st: N.Status):
+    if rc == 0:
+        return
+    msg = st.msg.decode(errors="replace")
+    if rc == 1:
+        raise IoError(msg)
+    if rc == 2:
+        raise SolverError(msg)
+    if rc == 3:
+        raise SingularMatrixError(msg, st.column)
+    if rc == 4:
+        raise CudaError(msg)
+    if rc == 6:
+        raise HssRankExceeded(msg)
+    raise SolverError(msg)
+
+
+def _call(fname, *args):
+    st = N.Status()
+    rc = getattr(N.lib(), fname)(*args, C.byref(st))
+    _check(rc, st)
+
+
+# ---- sparse matrix (sparse_matrix.hpp) --------------------------------------
+class SparseMatrix:
+    """square CSR with sorted, duplicate-free rows (owns a native handle)"""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        n, nnz = C.c_int(), C.c_longlong()
+        N.lib().hssmf_csr_info(self._h, C.byref(n), C.byref(nnz))
+        self.n = n.value
+        self._nnz = nnz.value
+        self._arrays = None
+
+    @classmethod
+    def from_csr(cls, n, ptr, ind, val):
+        h = C.c_void_p()
+        _call("hssmf_csr_create", int(n), np.ascontiguousarray(ptr, np.int32),
+              np.ascontiguousarray(ind, np.int32), np.ascontiguousarray(val, np.float64),
+              C.byref(h))
+        return cls(h)
+
+    def size(self):
+        return self.n
+
+    def nnz(self):
+        return self._nnz
+
+    def arrays(self):
+        if self._arrays is None:
+            ptr = np.zeros(self.n + 1, np.int32)
+            ind = np.zeros(self._nnz, np.int32)
+            val = np.zeros(self._nnz, np.float64)
+            N.lib().hssmf_csr_get(self._h, ptr, ind, val)
+            self._arrays = (ptr, ind, val)
+        return self._arrays
+
+    def permuted(self, perm):
+        h = C.c_void_p()
+        _call("hssmf_csr_permuted", self._h, np.ascontiguousarray(perm, np.int32), C.byref(h))
+        return SparseMatrix(h)
+
+    def matvec(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(self.n, np.float64)
+        N.lib().hssmf_csr_matvec(self._h, x, y)
+        return y
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().hssmf_csr_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+@dataclass
+class GridGeometry:
+    dims: tuple = (1, 1, 1)
+    ndims: int = 0
+
+
+@dataclass
+class GridProblem:
+    A: SparseMatrix
+    geom: GridGeometry
+    kind: str
+    k: int
+    nu: float
+
+
+def generate_grid_problem(kind: str, k: int, nu: float = 1e-4) -> GridProblem:
+    """grid_problems.hpp:65-117"""
+    h = C.c_void_p()
+    dims = np.zeros(3, np.int32)
+    nd = C.c_int()
+    _call("hssmf_csr_grid", GRID_KINDS[kind], int(k), float(nu), C.byref(h), dims,
+          C.byref(nd))
+    return GridProblem(SparseMatrix(h), GridGeometry(tuple(int(d) for d in dims), nd.value),
+                       kind, k, nu)
+
+
+def generate_convdiff3d(k: int, scale: float = 0.1) -> GridProblem:
+    """BASELINE config 4 operator (constant beta, upwind); not a reference generator"""
+    h = C.c_void_p()
+    _call("hssmf_csr_convdiff3d", int(k), float(scale), C.byref(h))
+    return GridProblem(SparseMatrix(h), GridGeometry((k, k, k), 3), "cd3d", k, scale)
+
+
+# ---- elimination tree (elimination_tree.hpp) --------------------------------
+class EliminationTree:
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self.refresh()
+
+    def refresh(self):
+        n, nn, tot = C.c_int(), C.c_int(), C.c_longlong()
+        N.lib().hssmf_tree_info(self._h, C.byref(n), C.byref(nn), C.byref(tot))
+        self.n = n.value
+        z = lambda k: np.zeros(k, np.int32)  # noqa: E731
+        nn = nn.value
+        self.sep_begin, self.sep_end, self.child0, self.child1 = z(nn), z(nn), z(nn), z(nn)
+        self.parent, self.level, self.upd_ptr, self.upd_ind = z(nn), z(nn), z(nn + 1), \
+            z(tot.value)
+        N.lib().hssmf_tree_get(self._h, self.sep_begin, self.sep_end, self.child0,
+                               self.child1, self.parent, self.level, self.upd_ptr,
+                               self.upd_ind)
+
+    @classmethod
+    def from_arrays(cls, n, sep_begin, sep_end, child0, child1, parent, upd=None):
+        a = lambda x: np.ascontiguousarray(x, np.int32)  # noqa: E731
+        h = C.c_void_p()
+        if upd is not None:
+            up = np.zeros(len(sep_begin) + 1, np.int32)
+            for i, u in enumerate(upd):
+                up[i + 1] = up[i] + len(u)
+            ui = a(np.concatenate([np.asarray(u, np.int32) for u in upd]) if len(upd) else [])
+            upp, uip = up.ctypes.data_as(C.c_void_p), ui.ctypes.data_as(C.c_void_p)
+            keep = (up, ui)
+        else:
+            upp = uip = None
+            keep = None
+        _call("hssmf_tree_create", int(n), len(sep_begin), a(sep_begin), a(sep_end),
+              a(child0), a(child1), a(parent), upp, uip, C.byref(h))
+        del keep
+        return cls(h)
+
+    def size(self):
+        return len(self.sep_begin)
+
+    def root_id(self):
+        return self.size() - 1
+
+    def upd(self, i):
+        return self.upd_ind[self.upd_ptr[i]:self.upd_ptr[i + 1]]
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().hssmf_tree_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def nested_dissection_geometric(geom: GridGeometry, leaf: int):
+    """ordering.cpp:213-222 + EliminationTree::from_separators; returns
+    (tree without upd sets, perm with perm[old] = new)"""
+    n = int(np.prod(geom.dims))
+    perm = np.zeros(n, np.int32)
+    h = C.c_void_p()
+    _call("hssmf_nd_geometric", np.ascontiguousarray(geom.dims, np.int32), geom.ndims,
+          int(leaf), perm, C.byref(h))
+    return EliminationTree(h), perm
+
+
+def symbolic_factorization(a: SparseMatrix, t: EliminationTree):
+    """elimination_tree.hpp:67-73"""
+    _call("hssmf_symbolic", a._h, t._h)
+    t.refresh()
+
+
+def front_cluster_tree(ns, nu, leaf):
+    L = N.lib()
+    nn = L.hssmf_front_cluster_tree(ns, nu, leaf, None, None, None, None, None)
+    arr = [np.zeros(nn, np.int32) for _ in range(5)]
+    L.hssmf_front_cluster_tree(ns, nu, leaf, *[x.ctypes.data_as(C.c_void_p) for x in arr])
+    return arr
+
+
+@dataclass
+class OrderedProblem:
+    a: SparseMatrix
+    t: EliminationTree
+    perm: np.ndarray
+    geom: GridGeometry
+
+
+def ordered_problem(g: GridProblem, nd_leaf: int) -> OrderedProblem:
+    """the canonical pipeline of tests/support/problems.hpp:20-30"""
+    t, perm = nested_dissection_geometric(g.geom, nd_leaf)
+    a = g.A.permuted(perm)
+    symbolic_factorization(a, t)
+    return OrderedProblem(a, t, perm, g.geom)
+
+
+def ordered_grid(kind: str, k: int, nd_leaf: int, nu: float = 1e-4) -> OrderedProblem:
+    return ordered_problem(generate_grid_problem(kind, k, nu), nd_leaf)
+
+
+# ---- options (solver_options.hpp:28-59, hss_compress.hpp:26-32) ------------
+@dataclass
+class SolverOptions:
+    nd_leaf: int = 32
+    ls: int = 0
+    eps: float = 1e-8
+    leaf: int = 128
+    d0: int = 128
+    dd: int = 128
+    p: int = 10
+    min_hss: int = 512
+    max_rank: int = 0
+    mode: str = "auto"  # auto | mf | mf-hss
+
+    def validate(self):
+        if self.eps < 0 or self.eps >= 1:
+            raise IoError("eps must be in [0,1)")
+        if self.ls < 0:
+            raise IoError("ls must be >= 0")
+        if self.leaf < 16:
+            raise IoError("leaf size b must be >= 16")
+        if self.d0 < 1 or self.dd < 1 or self.p < 0 or self.p >= self.d0:
+            raise IoError("need d0 >= 1, dd >= 1, 0 <= p < d0")
+        if self.nd_leaf < 1:
+            raise IoError("dissection leaf must be >= 1")
+
+    def native(self) -> N.Options:
+        mode = {"auto": 0, "mf": 1, "mf-hss": 2}[self.mode]
+        return N.Options(self.ls, self.eps, self.leaf, self.d0, self.dd, self.p, self.min_hss,
+                         self.max_rank, mode)
+
+
+@dataclass
+class HssOptions:
+    eps: float = 1e-8
+    d0: int = 128
+    dd: int = 128
+    p: int = 10
+    max_rank: int = 5000
+
+
+@dataclass
+class FrontStat:
+    id: int
+    level: int
+    dim: int
+    sep: int
+    rank: int
+    flops: int
+    type: str
+
+
+# ---- factorization (multifrontal.hpp:454-631) --------------------------------
+class MfFactors:
+    def __init__(self, handle, n):
+        self._h = handle
+        self.n = n
+        L = N.lib()
+        nn, hf, fb, mr, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_longlong()
+        L.hssmf_factor_summary(self._h, C.byref(nn), C.byref(hf), C.byref(fb), C.byref(mr),
+                               C.byref(nz))
+        self.hss_fronts, self.fallbacks, self.max_front_rank = hf.value, fb.value, mr.value
+        self._factor_nnz = nz.value
+        nn = nn.value
+        z = lambda: np.zeros(nn, np.int32)  # noqa: E731
+        self.level, self.dim, self.sep, self.rank, self.type = z(), z(), z(), z(), z()
+        self.flops = np.zeros(nn, np.int64)
+        L.hssmf_front_stats(self._h, self.level, self.dim, self.sep, self.rank, self.flops,
+                            self.type)
+        self.factored = True
+
+    @property
+    def front_stats(self):
+        return [FrontStat(i, int(self.level[i]), int(self.dim[i]), int(self.sep[i]),
+                          int(self.rank[i]), int(self.flops[i]), FRONT_TYPES[int(self.type[i])])
+                for i in range(len(self.level))]
+
+    def factor_nnz(self):
+        return self._factor_nnz
+
+    def front_hss(self, front):
+        L = N.lib()
+        nn = L.hssmf_front_hss(self._h, front, None, None, None, None)
+        if nn == 0:
+            return None
+        u = np.zeros(nn, np.int32)
+        v = np.zeros(nn, np.int32)
+        r, d = C.c_int(), C.c_int()
+        L.hssmf_front_hss(self._h, front, u.ctypes.data_as(C.c_void_p),
+                          v.ctypes.data_as(C.c_void_p), C.byref(r), C.byref(d))
+        return u, v, r.value, d.value
+
+    def timing(self):
+        f, s = C.c_double(), C.c_double()
+        N.lib().hssmf_timing(self._h, C.byref(f), C.byref(s))
+        return f.value, s.value
+
+    def set_profile(self, on=True):
+        N.lib().hssmf_set_profile(self._h, 1 if on else 0)
+
+    def kernel_stats(self):
+        k = 32
+        names = C.create_string_buffer(32 * k)
+        la = np.zeros(k, np.int32)
+        ms, fl, by = np.zeros(k), np.zeros(k), np.zeros(k)
+        n = N.lib().hssmf_kernel_stats(self._h, k, names, la, ms, fl, by)
+        out = []
+        for i in range(n):
+            nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
+            out.append(dict(name=nm, launches=int(la[i]), ms=float(ms[i]), flops=float(fl[i]),
+                            bytes=float(by[i])))
+        return out
+
+    def reset_kernel_stats(self):
+        N.lib().hssmf_reset_kernel_stats(self._h)
+
+    def device_bytes(self):
+        return N.lib().hssmf_device_bytes(self._h)
+
+    def refactor(self, val=None, device_ptr=None):
+        if device_ptr is not None:
+            _call("hssmf_refactor", self._h, C.c_void_p(device_ptr), 1)
+        elif val is not None:
+            v = np.ascontiguousarray(val, np.float64)
+            _call("hssmf_refactor", self._h, v.ctypes.data_as(C.c_void_p), 0)
+        else:
+            _call("hssmf_refactor", self._h, None, 0)
+
+    def solve_device(self, ptr, ldb, nrhs):
+        _call("hssmf_solve", self._h, C.c_void_p(ptr), int(ldb), int(nrhs), 1)
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().hssmf_factors_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def mf_factor(a: SparseMatrix, t: EliminationTree, opts: SolverOptions, device: int = 0):
+    """multifrontal.hpp:473-503: raises IoError on size mismatch and
+    SingularMatrixError('front <i>...', column) on an exact zero pivot"""
+    if a.size() != t.n:
+        raise IoError("mf factor: matrix and tree sizes differ")
+    h = C.c_void_p()
+    o = opts.native()
+    _call("hssmf_factor", int(device), a._h, t._h, C.byref(o), C.byref(h))
+    return MfFactors(h, a.size())
+
+
+def mf_solve(m: MfFactors, b: np.ndarray):
+    """multifrontal.hpp:612-622: solves in place (b is n x nrhs, column-major)"""
+    if m is None or not getattr(m, "factored", False) or not m._h:
+        raise SolverError("mf solve: not factored")
+    if b.ndim == 1:
+        b2 = b.reshape(-1, 1)
+    else:
+        b2 = b
+    if b2.shape[0] != m.n:
+        raise IoError("mf solve: rhs rows mismatch")
+    if not (b2.flags.f_contiguous and b2.dtype == np.float64):
+        raise IoError("mf solve: b must be a Fortran-ordered float64 array")
+    _call("hssmf_solve", m._h, b2.ctypes.data_as(C.c_void_p), m.n, b2.shape[1], 0)
+    return b
+
+
+def mf_solve_new(m: MfFactors, b: np.ndarray) -> np.ndarray:
+    x = np.array(b, dtype=np.float64, order="F", copy=True)
+    mf_solve(m, x)
+    return x
+
+
+# ---- standalone dense HSS (hss_compress.hpp:373-383, hss_ulv.hpp) ----------
+class HssFactors:
+    """hss_compress(A, ClusterTree::balanced(n, leaf), opts) + ulv_factor"""
+
+    def __init__(self, a: np.ndarray, leaf: int, opts: HssOptions, device: int = 0,
+                 device_ptr=None, n=None):
+        h = C.c_void_p()
+        if device_ptr is not None:
+            self.n = int(n)
+            _call("hssmf_hss_dense", int(device), C.c_void_p(device_ptr), self.n, self.n,
+                  int(leaf), opts.eps, opts.d0, opts.dd, opts.p, opts.max_rank, 1, C.byref(h))
+        else:
+            A = np.asfortranarray(a, dtype=np.float64)
+            if A.shape[0] != A.shape[1]:
+                raise IoError("hss compress: matrix and cluster tree sizes disagree")
+            self.n = A.shape[0]
+            _call("hssmf_hss_dense", int(device), A.ctypes.data_as(C.c_void_p), self.n,
+                  self.n, int(leaf), opts.eps, opts.d0, opts.dd, opts.p, opts.max_rank, 0,
+                  C.byref(h))
+        self._h = h
+        L = N.lib()
+        r, d, tc, tu = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+        nn = L.hssmf_hss_info(self._h, None, None, C.byref(r), C.byref(d), C.byref(tc),
+                              C.byref(tu))
+        self.u_rank = np.zeros(nn, np.int32)
+        self.v_rank = np.zeros(nn, np.int32)
+        L.hssmf_hss_info(self._h, self.u_rank.ctypes.data_as(C.c_void_p),
+                         self.v_rank.ctypes.data_as(C.c_void_p), C.byref(r), C.byref(d),
+                         C.byref(tc), C.byref(tu))
+        self.rounds, self.d_final = r.value, d.value
+        self.compress_ms, self.ulv_ms = tc.value, tu.value
+
+    def hss_rank(self):
+        return int(max(self.u_rank[:-1].max(initial=0), self.v_rank[:-1].max(initial=0)))
+
+    def solve(self, b):
+        x = np.array(b, dtype=np.float64, order="F", copy=True)
+        x2 = x.reshape(-1, 1) if x.ndim == 1 else x
+        if x2.shape[0] != self.n:
+            raise IoError("ulv solve: rhs rows mismatch")
+        _call("hssmf_hss_solve", self._h, x2.ctypes.data_as(C.c_void_p), self.n, x2.shape[1],
+              0)
+        return x
+
+    def solve_device(self, ptr, ldb, nrhs):
+        _call("hssmf_hss_solve", self._h, C.c_void_p(ptr), int(ldb), int(nrhs), 1)
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().hssmf_hss_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def hss_compress(a: np.ndarray, leaf: int, opts: HssOptions, device: int = 0) -> HssFactors:
+    return HssFactors(a, leaf, opts, device)
+
+
+# ---- kernel-level parity hooks -------------------------------------------------
+def dev_random_rows(grow, c0, c1, device=0):
+    g = np.ascontiguousarray(grow, np.int64)
+    out = np.zeros((len(g), c1 - c0), np.float64, order="F")
+    _call("hssmf_dev_random_rows", device, len(g), g, c0, c1, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def dev_gemm(ta, tb, alpha, a, b, beta, c, device=0):
+    A = np.asfortranarray(a, np.float64)
+    B = np.asfortranarray(b, np.float64)
+    Cm = np.array(c, np.float64, order="F", copy=True)
+    m, n = Cm.shape
+    k = A.shape[1] if ta == "N" else A.shape[0]
+    _call("hssmf_dev_gemm", device, ta.encode(), tb.encode(), m, n, k, alpha,
+          A.ctypes.data_as(C.c_void_p), A.shape[0], B.ctypes.data_as(C.c_void_p), B.shape[0],
+          beta, Cm.ctypes.data_as(C.c_void_p), m)
+    return Cm
+
+
+def dev_interpolative_decomposition(y, eps, max_rank=-1, abs_tol=0.0, device=0):
+    Y = np.asfortranarray(y, np.float64)
+    m, n = Y.shape
+    perm = np.zeros(n, np.int32)
+    rank, cert = C.c_int(), C.c_int()
+    X = np.zeros(max(1, min(m, n) * n), np.float64)
+    _call("hssmf_dev_id", device, Y.ctypes.data_as(C.c_void_p), m, n, eps, max_rank, abs_tol,
+          perm, C.byref(rank), C.byref(cert), X.ctypes.data_as(C.c_void_p))
+    k = rank.value
+    return perm, k, bool(cert.value), X[: k * (n - k)].reshape((k, n - k), order="F")
+
+
+def dev_lu(a, device=0):
+    A = np.array(a, np.float64, order="F", copy=True)
+    m, n = A.shape
+    piv = np.zeros(n, np.int32)
+    _call("hssmf_dev_lu", device, A.ctypes.data_as(C.c_void_p), m, n, piv)
+    return A, piv

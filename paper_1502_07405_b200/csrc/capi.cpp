@@ -1,0 +1,379 @@
+// extern "C" boundary (include/hssmf_b200.h) over the host analysis and the
+// device engine. Exceptions never cross the ABI: they become hssmf_codes.
+#include "../../include/hssmf_b200.h"
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "engine.hpp"
+#include "hss_dense.hpp"
+#include "host/analysis.hpp"
+#include "kernels_test.hpp"
+
+using namespace hssmf_b200;
+
+struct hssmf_csr { Csr a; };
+struct hssmf_tree { Etree t; };
+struct hssmf_factors { std::unique_ptr<Engine> e; };
+struct hssmf_hss { std::unique_ptr<DenseHss> h; };
+
+namespace {
+  int fail(hssmf_status* st, int code, const std::string& msg, int front = -1, int col = -1) {
+    if (st) {
+      st->code = code;
+      st->front = front;
+      st->column = col;
+      std::snprintf(st->msg, sizeof(st->msg), "%s", msg.c_str());
+    }
+    return code;
+  }
+  int ok(hssmf_status* st) {
+    if (st) {
+      st->code = HSSMF_OK;
+      st->front = st->column = -1;
+      st->msg[0] = 0;
+    }
+    return HSSMF_OK;
+  }
+  template<typename F> int guard(hssmf_status* st, F&& f) {
+    try {
+      f();
+      return ok(st);
+    } catch (const SolverFailure& e) {
+      return fail(st, e.code, e.what(), e.front, e.column);
+    } catch (const CudaError& e) {
+      return fail(st, HSSMF_ERR_CUDA, e.what());
+    } catch (const std::exception& e) {
+      return fail(st, HSSMF_ERR_OTHER, e.what());
+    }
+  }
+  Options to_opts(const hssmf_options* o) {
+    Options r;
+    if (!o) return r;
+    r.ls = o->ls;
+    r.eps = o->eps;
+    r.leaf = o->leaf;
+    r.d0 = o->d0;
+    r.dd = o->dd;
+    r.p = o->p;
+    r.min_hss = o->min_hss;
+    r.max_rank = o->max_rank;
+    r.mode = o->mode;
+    return r;
+  }
+}  // namespace
+
+extern "C" {
+
+const char* hssmf_version(void) { return "hssmf_b200 0.1 (sm_100a)"; }
+
+int hssmf_csr_grid(int kind, int k, double nu, hssmf_csr** out, int* dims, int* ndims,
+                   hssmf_status* st) {
+  return guard(st, [&] {
+    auto* c = new hssmf_csr;
+    Geometry g;
+    c->a = grid_problem(kind, k, nu, g);
+    if (dims) for (int i = 0; i < 3; i++) dims[i] = g.dims[i];
+    if (ndims) *ndims = g.ndims;
+    *out = c;
+  });
+}
+
+int hssmf_csr_convdiff3d(int k, double scale, hssmf_csr** out, hssmf_status* st) {
+  return guard(st, [&] {
+    auto* c = new hssmf_csr;
+    Geometry g;
+    c->a = convdiff3d_const(k, scale, g);
+    *out = c;
+  });
+}
+
+int hssmf_csr_create(int n, const int* ptr, const int* ind, const double* val,
+                     hssmf_csr** out, hssmf_status* st) {
+  return guard(st, [&] {
+    if (n < 0) throw SolverFailure(1, -1, -1, "csr: negative size");
+    auto* c = new hssmf_csr;
+    c->a.n = n;
+    c->a.ptr.assign(ptr, ptr + n + 1);
+    c->a.ind.assign(ind, ind + ptr[n]);
+    c->a.val.assign(val, val + ptr[n]);
+    *out = c;
+  });
+}
+
+int hssmf_csr_permuted(const hssmf_csr* a, const int* perm, hssmf_csr** out,
+                       hssmf_status* st) {
+  return guard(st, [&] {
+    auto* c = new hssmf_csr;
+    c->a = a->a.permuted(std::vector<int>(perm, perm + a->a.n));
+    *out = c;
+  });
+}
+
+void hssmf_csr_info(const hssmf_csr* a, int* n, long long* nnz) {
+  *n = a->a.n;
+  *nnz = a->a.nnz();
+}
+
+void hssmf_csr_get(const hssmf_csr* a, int* ptr, int* ind, double* val) {
+  std::memcpy(ptr, a->a.ptr.data(), (a->a.n + 1) * sizeof(int));
+  std::memcpy(ind, a->a.ind.data(), a->a.ind.size() * sizeof(int));
+  std::memcpy(val, a->a.val.data(), a->a.val.size() * sizeof(double));
+}
+
+void hssmf_csr_matvec(const hssmf_csr* a, const double* x, double* y) {
+  const auto& A = a->a;
+  for (int i = 0; i < A.n; i++) {
+    double s = 0;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; k++) s += A.val[k] * x[A.ind[k]];
+    y[i] = s;
+  }
+}
+
+void hssmf_csr_free(hssmf_csr* a) { delete a; }
+
+int hssmf_nd_geometric(const int* dims, int ndims, int leaf, int* perm, hssmf_tree** out,
+                       hssmf_status* st) {
+  return guard(st, [&] {
+    Geometry g;
+    g.dims = {dims[0], dims[1], dims[2]};
+    g.ndims = ndims;
+    std::vector<int> p;
+    auto* t = new hssmf_tree;
+    t->t = nested_dissection_geometric(g, leaf, p);
+    std::memcpy(perm, p.data(), p.size() * sizeof(int));
+    *out = t;
+  });
+}
+
+int hssmf_tree_create(int n, int nnodes, const int* sep_begin, const int* sep_end,
+                      const int* child0, const int* child1, const int* parent,
+                      const int* upd_ptr, const int* upd_ind, hssmf_tree** out,
+                      hssmf_status* st) {
+  return guard(st, [&] {
+    auto* t = new hssmf_tree;
+    t->t.n = n;
+    t->t.nodes.resize(nnodes);
+    for (int i = 0; i < nnodes; i++) {
+      auto& f = t->t.nodes[i];
+      f.sep_begin = sep_begin[i];
+      f.sep_end = sep_end[i];
+      f.child0 = child0[i];
+      f.child1 = child1[i];
+      f.parent = parent[i];
+      if (upd_ptr) f.upd.assign(upd_ind + upd_ptr[i], upd_ind + upd_ptr[i + 1]);
+    }
+    t->t.compute_levels();
+    *out = t;
+  });
+}
+
+int hssmf_symbolic(const hssmf_csr* a, hssmf_tree* t, hssmf_status* st) {
+  return guard(st, [&] {
+    if (a->a.n != t->t.n) throw SolverFailure(1, -1, -1, "symbolic: size mismatch");
+    symbolic_factorization(a->a, t->t);
+    t->t.compute_levels();
+  });
+}
+
+void hssmf_tree_info(const hssmf_tree* t, int* n, int* nnodes, long long* upd_total) {
+  *n = t->t.n;
+  *nnodes = (int)t->t.nodes.size();
+  long long s = 0;
+  for (const auto& f : t->t.nodes) s += f.nu();
+  *upd_total = s;
+}
+
+void hssmf_tree_get(const hssmf_tree* t, int* sep_begin, int* sep_end, int* child0,
+                    int* child1, int* parent, int* level, int* upd_ptr, int* upd_ind) {
+  long long off = 0;
+  for (size_t i = 0; i < t->t.nodes.size(); i++) {
+    const auto& f = t->t.nodes[i];
+    sep_begin[i] = f.sep_begin;
+    sep_end[i] = f.sep_end;
+    child0[i] = f.child0;
+    child1[i] = f.child1;
+    parent[i] = f.parent;
+    level[i] = f.level;
+    upd_ptr[i] = (int)off;
+    for (int g : f.upd) upd_ind[off++] = g;
+  }
+  upd_ptr[t->t.nodes.size()] = (int)off;
+}
+
+void hssmf_tree_free(hssmf_tree* t) { delete t; }
+
+int hssmf_front_cluster_tree(int ns, int nu, int leaf, int* begin, int* end, int* child0,
+                             int* child1, int* parent) {
+  auto c = front_cluster_tree(ns, nu, leaf);
+  if (begin)
+    for (size_t i = 0; i < c.nodes.size(); i++) {
+      begin[i] = c.nodes[i].begin;
+      end[i] = c.nodes[i].end;
+      child0[i] = c.nodes[i].child0;
+      child1[i] = c.nodes[i].child1;
+      parent[i] = c.nodes[i].parent;
+    }
+  return (int)c.nodes.size();
+}
+
+int hssmf_factor(int device, const hssmf_csr* a, const hssmf_tree* t, const hssmf_options* o,
+                 hssmf_factors** out, hssmf_status* st) {
+  *out = nullptr;
+  auto f = std::make_unique<hssmf_factors>();
+  const int rc = guard(st, [&] {
+    f->e = std::make_unique<Engine>(device);
+    f->e->analyze(a->a, t->t, to_opts(o));
+    f->e->factor();
+  });
+  if (rc == HSSMF_OK) *out = f.release();
+  return rc;
+}
+
+int hssmf_refactor(hssmf_factors* f, const double* val, int on_device, hssmf_status* st) {
+  return guard(st, [&] {
+    if (val) f->e->set_values(val, on_device != 0);
+    f->e->factor();
+  });
+}
+
+int hssmf_solve(hssmf_factors* f, double* b, int ldb, int nrhs, int on_device,
+                hssmf_status* st) {
+  return guard(st, [&] {
+    if (!f || !f->e || !f->e->factored())
+      throw SolverFailure(2, -1, -1, "mf solve: not factored");
+    if (ldb < f->e->n()) throw SolverFailure(1, -1, -1, "mf solve: rhs rows mismatch");
+    f->e->solve(b, ldb, nrhs, on_device != 0);
+  });
+}
+
+void hssmf_factor_summary(const hssmf_factors* f, int* nnodes, int* hss_fronts,
+                          int* fallbacks, int* max_rank, long long* factor_nnz) {
+  *nnodes = (int)f->e->stats().size();
+  *hss_fronts = f->e->hss_fronts();
+  *fallbacks = f->e->fallbacks();
+  *max_rank = f->e->max_front_rank();
+  *factor_nnz = f->e->factor_nnz();
+}
+
+void hssmf_front_stats(const hssmf_factors* f, int* level, int* dim, int* sep, int* rank,
+                       long long* flops, int* type) {
+  const auto& s = f->e->stats();
+  for (size_t i = 0; i < s.size(); i++) {
+    level[i] = s[i].level;
+    dim[i] = s[i].dim;
+    sep[i] = s[i].sep;
+    rank[i] = s[i].rank;
+    flops[i] = s[i].flops;
+    type[i] = s[i].type;
+  }
+}
+
+int hssmf_front_hss(const hssmf_factors* f, int front, int* u_rank, int* v_rank, int* rounds,
+                    int* d_final) {
+  std::vector<int> u, v;
+  int r = 0, d = 0;
+  if (!f->e->front_hss(front, u, v, r, d)) return 0;
+  if (u_rank)
+    for (size_t i = 0; i < u.size(); i++) {
+      u_rank[i] = u[i];
+      v_rank[i] = v[i];
+    }
+  if (rounds) *rounds = r;
+  if (d_final) *d_final = d;
+  return (int)u.size();
+}
+
+void hssmf_timing(const hssmf_factors* f, double* factor_ms, double* solve_ms) {
+  *factor_ms = f->e->factor_ms();
+  *solve_ms = f->e->solve_ms();
+}
+
+void hssmf_set_profile(hssmf_factors* f, int on) { f->e->set_profile(on != 0); }
+
+int hssmf_kernel_stats(const hssmf_factors* f, int max, char* names, int* launches, double* ms,
+                       double* flops, double* bytes) {
+  auto ks = f->e->kernel_stats();
+  const int n = (int)ks.size() < max ? (int)ks.size() : max;
+  for (int i = 0; i < n; i++) {
+    std::snprintf(names + 32 * i, 32, "%s", ks[i].name.c_str());
+    launches[i] = ks[i].launches;
+    ms[i] = ks[i].ms;
+    flops[i] = ks[i].flops;
+    bytes[i] = ks[i].bytes;
+  }
+  return n;
+}
+
+void hssmf_reset_kernel_stats(hssmf_factors* f) { f->e->reset_kernel_stats(); }
+long long hssmf_device_bytes(const hssmf_factors* f) { return (long long)f->e->device_bytes(); }
+void hssmf_factors_free(hssmf_factors* f) { delete f; }
+
+int hssmf_hss_dense(int device, const double* a, int lda, int n, int leaf, double eps, int d0,
+                    int dd, int p, int max_rank, int on_device, hssmf_hss** out,
+                    hssmf_status* st) {
+  *out = nullptr;
+  auto h = std::make_unique<hssmf_hss>();
+  const int rc = guard(st, [&] {
+    h->h = std::make_unique<DenseHss>(device);
+    h->h->run(a, lda, n, leaf, eps, d0, dd, p, max_rank, on_device != 0);
+  });
+  if (rc == HSSMF_OK) *out = h.release();
+  return rc;
+}
+
+int hssmf_hss_info(const hssmf_hss* h, int* u_rank, int* v_rank, int* rounds, int* d_final,
+                   double* compress_ms, double* ulv_ms) {
+  std::vector<int> u, v;
+  h->h->ranks(u, v);
+  if (u_rank)
+    for (size_t i = 0; i < u.size(); i++) {
+      u_rank[i] = u[i];
+      v_rank[i] = v[i];
+    }
+  if (rounds) *rounds = h->h->rounds();
+  if (d_final) *d_final = h->h->d_final();
+  if (compress_ms) *compress_ms = h->h->compress_ms();
+  if (ulv_ms) *ulv_ms = h->h->ulv_ms();
+  return (int)u.size();
+}
+
+int hssmf_hss_solve(hssmf_hss* h, double* b, int ldb, int nrhs, int on_device,
+                    hssmf_status* st) {
+  return guard(st, [&] { h->h->solve(b, ldb, nrhs, on_device != 0); });
+}
+
+void hssmf_hss_free(hssmf_hss* h) { delete h; }
+
+int hssmf_dev_random_rows(int device, int nrows, const long long* grow, int c0, int c1,
+                          double* out, hssmf_status* st) {
+  return guard(st, [&] { test_random_rows(device, nrows, grow, c0, c1, out); });
+}
+
+int hssmf_dev_gemm(int device, char ta, char tb, int m, int n, int k, double alpha,
+                   const double* a, int lda, const double* b, int ldb, double beta, double* c,
+                   int ldc, hssmf_status* st) {
+  return guard(st, [&] { test_gemm(device, ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc); });
+}
+
+int hssmf_dev_id(int device, const double* y, int m, int n, double eps, int max_rank,
+                 double abs_tol, int* perm, int* rank, int* certified, double* coeffs,
+                 hssmf_status* st) {
+  return guard(st, [&] {
+    test_id(device, y, m, n, eps, max_rank, abs_tol, perm, rank, certified, coeffs);
+  });
+}
+
+int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st) {
+  return guard(st, [&] { *ms = bench_gemm(device, m, n, k, iters); });
+}
+
+int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st) {
+  return guard(st, [&] { test_lu(device, a, m, n, piv); });
+}
+
+}  // extern "C"

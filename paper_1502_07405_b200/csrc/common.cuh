@@ -1,0 +1,66 @@
+// Shared device helpers for the sm_100a kernels of the HSS-multifrontal path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace hssmf_b200 {
+
+  struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+  };
+
+#define HSSMF_CUDA(call)                                                              \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw ::hssmf_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                                    " at " __FILE__ ":" + std::to_string(__LINE__));  \
+  } while (0)
+
+#define HSSMF_LAUNCH_CHECK() HSSMF_CUDA(cudaGetLastError())
+
+  inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+  // ---- device-side ----------------------------------------------------------
+#ifdef __CUDACC__
+  // one FP64 tensor-core MMA: D(8x8) += A(8x4) * B(4x8).
+  // lane layout (PTX m8n8k4 .f64): a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+  // c[v] = C[lane>>2][2*(lane&3)+v]
+  __device__ __forceinline__ void dmma8x8x4(double (&c)[2], double a, double b) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+  }
+
+  __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+  }
+  __device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  template<int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+  }
+
+  // block-wide argmax of |v| with the lowest index winning ties
+  // (partial pivoting rule, reference lu.hpp:22-26). blockDim multiple of 32.
+  __device__ __forceinline__ void warp_argmax(double& v, int& i) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_down_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_down_sync(0xffffffffu, i, o);
+      if (v2 > v || (v2 == v && i2 < i)) {
+        v = v2;
+        i = i2;
+      }
+    }
+  }
+#endif
+
+}  // namespace hssmf_b200

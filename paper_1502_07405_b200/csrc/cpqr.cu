@@ -1,0 +1,247 @@
+#include "cpqr.cuh"
+
+#include <algorithm>
+#include <vector>
+
+namespace hssmf_b200 {
+
+  namespace {
+    constexpr int CT = 256, NW = CT / 32;
+
+    __device__ __forceinline__ double warp_sum(double v) {
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      return v;
+    }
+
+    // dynamic smem: nrm2[n], last[n] (double), v[m] (double), perm[n] (int)
+    __global__ void __launch_bounds__(CT)
+    cpqr_kernel(const CpqrTask* __restrict__ tasks, double eps, double abs_tol) {
+      extern __shared__ double sm[];
+      const CpqrTask T = tasks[blockIdx.x];
+      const int m = T.m, n = T.n, ld = T.ldy;
+      double* Y = T.Y;
+      double* nrm2 = sm;
+      double* last = nrm2 + n;
+      double* v = last + n;
+      int* perm = reinterpret_cast<int*>(v + m);
+      __shared__ double rv[NW];
+      __shared__ int ri[NW];
+      __shared__ int s_p, s_stop, s_cert;
+      __shared__ double s_tk, s_r11;
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      const int kmax_dim = min(m, n);
+      const int kmax = T.max_rank < 0 ? kmax_dim : min(kmax_dim, T.max_rank);
+
+      if (m == 0 || n == 0) {
+        for (int j = tid; j < n; j += CT) T.perm[j] = j;
+        if (tid == 0) { T.out[0] = 0; T.out[1] = 1; }
+        return;
+      }
+      // exact squared column norms (rrqr.hpp:49-53)
+      for (int j = warp; j < n; j += NW) {
+        const double* c = Y + (size_t)j * ld;
+        double s = 0;
+        for (int i = lane; i < m; i += 32) s += c[i] * c[i];
+        s = warp_sum(s);
+        if (lane == 0) { nrm2[j] = s; last[j] = s; }
+      }
+      for (int j = tid; j < n; j += CT) perm[j] = j;
+      if (tid == 0) { s_r11 = 0; s_cert = 0; }
+      __syncthreads();
+      int k = 0;
+      while (true) {
+        // pivot: largest downdated norm, lowest index on ties
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int j = k + tid; j < n; j += CT)
+          if (nrm2[j] > bv) { bv = nrm2[j]; bi = j; }
+        warp_argmax(bv, bi);
+        if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+          double b = rv[0];
+          int p = ri[0];
+          for (int w = 1; w < NW; w++)
+            if (rv[w] > b || (rv[w] == b && ri[w] < p)) { b = rv[w]; p = ri[w]; }
+          const double pv = nrm2[p] > 0.0 ? sqrt(nrm2[p]) : 0.0;
+          int stop = 0;
+          if (k == 0) {
+            s_r11 = pv;
+            if (pv == 0.0 || pv <= abs_tol) { stop = 1; s_cert = 1; }
+          } else if (pv <= eps * s_r11 || pv <= abs_tol) {
+            stop = 1;
+            s_cert = 1;
+          }
+          if (!stop && k == kmax) {
+            stop = 1;
+            s_cert = (k == kmax_dim);
+          }
+          if (!stop && p != k) {
+            double t = nrm2[k]; nrm2[k] = nrm2[p]; nrm2[p] = t;
+            t = last[k]; last[k] = last[p]; last[p] = t;
+            const int q = perm[k]; perm[k] = perm[p]; perm[p] = q;
+          }
+          s_p = p;
+          s_stop = stop;
+        }
+        __syncthreads();
+        if (s_stop) break;
+        const int p = s_p;
+        double* ck = Y + (size_t)k * ld;
+        if (p != k) {
+          double* cp = Y + (size_t)p * ld;
+          for (int i = tid; i < m; i += CT) {
+            const double t = ck[i];
+            ck[i] = cp[i];
+            cp[i] = t;
+          }
+          __syncthreads();
+        }
+        // Householder reflector (rrqr.hpp:85-103)
+        double s = 0;
+        for (int i = k + 1 + tid; i < m; i += CT) s += ck[i] * ck[i];
+        s = warp_sum(s);
+        if (lane == 0) rv[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+          double xs = 0;
+          for (int w = 0; w < NW; w++) xs += rv[w];
+          const double xn = sqrt(xs);
+          const double alpha = ck[k];
+          double tk = 0, sc = 0;
+          if (xn != 0.0 || fabs(alpha) != 0.0) {
+            double beta = hypot(fabs(alpha), xn);
+            if (alpha > 0.0) beta = -beta;
+            if (beta != 0.0) {
+              tk = (beta - alpha) / beta;
+              sc = 1.0 / (alpha - beta);
+              ck[k] = beta;
+            }
+          }
+          s_tk = tk;
+          rv[0] = sc;
+        }
+        __syncthreads();
+        const double tk = s_tk, sc = rv[0];
+        for (int i = k + 1 + tid; i < m; i += CT) {
+          const double x = tk != 0.0 ? ck[i] * sc : ck[i];
+          if (tk != 0.0) ck[i] = x;
+          v[i] = x;
+        }
+        __syncthreads();
+        // apply the reflector to the trailing columns and downdate norms
+        for (int j = k + 1 + warp; j < n; j += NW) {
+          double* cj = Y + (size_t)j * ld;
+          if (tk != 0.0) {
+            double w = 0;
+            for (int i = k + 1 + lane; i < m; i += 32) w += v[i] * cj[i];
+            w = warp_sum(w) + cj[k];
+            w *= tk;
+            if (lane == 0) cj[k] -= w;
+            for (int i = k + 1 + lane; i < m; i += 32) cj[i] -= w * v[i];
+          }
+          __syncwarp();
+          const double rk = cj[k];
+          double nj = nrm2[j] - rk * rk;
+          if (nj < 0.0) nj = 0.0;
+          if (nj < 0.1 * last[j]) {
+            double q = 0;
+            for (int i = k + 1 + lane; i < m; i += 32) q += cj[i] * cj[i];
+            q = warp_sum(q);
+            if (lane == 0) { nrm2[j] = q; last[j] = q; }
+          } else if (lane == 0) {
+            nrm2[j] = nj;
+          }
+        }
+        __syncthreads();
+        k++;
+        if (k == kmax_dim) {
+          if (tid == 0) s_cert = 1;
+          break;
+        }
+      }
+      __syncthreads();
+      for (int j = tid; j < n; j += CT) T.perm[j] = perm[j];
+      if (tid == 0) { T.out[0] = k; T.out[1] = s_cert; }
+    }
+
+    // X = R1^-1 R2 (upper TRSM, rrqr.hpp:187-192), CPC columns per CTA held in
+    // smem, backward column sweep over R1
+    __global__ void id_solve_kernel(const CpqrTask* __restrict__ tasks, int cpc) {
+      extern __shared__ double xs[];
+      const CpqrTask T = tasks[blockIdx.y];
+      const int k = T.out[0], n = T.n, ld = T.ldy;
+      const int c0 = blockIdx.x * cpc;
+      if (k == 0 || c0 >= n - k) return;
+      const int nc = min(cpc, n - k - c0);
+      const double* R = T.Y;
+      for (int e = threadIdx.x; e < k * nc; e += blockDim.x) {
+        const int i = e % k, c = e / k;
+        xs[i + c * k] = R[i + (size_t)(k + c0 + c) * ld];
+      }
+      __syncthreads();
+      for (int i = k - 1; i >= 0; i--) {
+        const double d = R[i + (size_t)i * ld];
+        if (threadIdx.x < nc) xs[i + threadIdx.x * k] /= d;
+        __syncthreads();
+        for (int e = threadIdx.x; e < i * nc; e += blockDim.x) {
+          const int l = e % i, c = e / i;
+          xs[l + c * k] -= R[l + (size_t)i * ld] * xs[i + c * k];
+        }
+        __syncthreads();
+      }
+      for (int e = threadIdx.x; e < k * nc; e += blockDim.x) {
+        const int i = e % k, c = e / k;
+        T.X[i + (size_t)(c0 + c) * k] = xs[i + c * k];
+      }
+    }
+
+    void set_attr() {
+      static bool done = false;
+      if (done) return;
+      HSSMF_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      220 * 1024));
+      HSSMF_CUDA(cudaFuncSetAttribute(id_solve_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      done = true;
+    }
+  }  // namespace
+
+  void cpqr_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,
+                double abs_tol, cudaStream_t s) {
+    if (!ntask) return;
+    set_attr();
+    const size_t smem = (size_t)max_n * 20 + (size_t)max_m * 8 + 64;
+    if (smem > 220 * 1024) throw CudaError("cpqr: task too large for shared memory");
+    cpqr_kernel<<<ntask, CT, smem, s>>>(tasks, eps, abs_tol);
+    HSSMF_LAUNCH_CHECK();
+  }
+
+  void id_solve_run(const CpqrTask* tasks, int ntask, int max_rank, int max_cols,
+                    cudaStream_t s) {
+    if (!ntask || max_rank <= 0 || max_cols <= 0) return;
+    set_attr();
+    int cpc = (int)std::min<long long>(8, (200LL * 1024) / (8LL * max_rank));
+    if (cpc < 1) throw CudaError("id solve: rank too large");
+    dim3 grid(ceil_div(max_cols, cpc), ntask);
+    id_solve_kernel<<<grid, 256, (size_t)cpc * max_rank * 8, s>>>(tasks, cpc);
+    HSSMF_LAUNCH_CHECK();
+  }
+
+  void cpqr_id_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,
+                   double abs_tol, cudaStream_t s) {
+    cpqr_run(tasks, ntask, max_m, max_n, eps, abs_tol, s);
+    std::vector<CpqrTask> h(ntask);
+    HSSMF_CUDA(cudaMemcpyAsync(h.data(), tasks, ntask * sizeof(CpqrTask), cudaMemcpyDeviceToHost, s));
+    HSSMF_CUDA(cudaStreamSynchronize(s));
+    int max_rank = 0, max_cols = 0;
+    for (auto& t : h) {
+      int o[2];
+      HSSMF_CUDA(cudaMemcpy(o, t.out, sizeof(o), cudaMemcpyDeviceToHost));
+      max_rank = std::max(max_rank, o[0]);
+      max_cols = std::max(max_cols, t.n - o[0]);
+    }
+    id_solve_run(tasks, ntask, max_rank, max_cols, s);
+  }
+
+}  // namespace hssmf_b200

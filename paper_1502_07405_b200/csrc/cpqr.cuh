@@ -1,0 +1,31 @@
+// Batched tolerance-truncated column-pivoted Householder QR + interpolative
+// decomposition (reference rrqr_tolerance / interpolative_decomposition,
+// rrqr.hpp:32-194). One CTA per task; Y is overwritten by R (upper part) and
+// Householder vectors; the ID coefficients X = R1^-1 R2 are solved by a
+// second, column-tiled kernel once the ranks are known.
+#pragma once
+
+#include "common.cuh"
+
+namespace hssmf_b200 {
+
+  struct CpqrTask {
+    double* Y;     // m x n, ld ldy (overwritten)
+    int m, n, ldy;
+    int max_rank;  // < 0: min(m, n)
+    int* perm;     // n: perm[i] = original column of pivot i
+    double* X;     // rank x (n - rank), ld rank (ID coefficients)
+    int* out;      // [rank, certified]
+  };
+
+  // CPQR for all tasks (device array), then the ID solve; the ranks are read
+  // back to the host (one small D2H) between the two kernels.
+  void cpqr_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,
+                double abs_tol, cudaStream_t s);
+  void id_solve_run(const CpqrTask* tasks, int ntask, int max_rank, int max_cols,
+                    cudaStream_t s);
+  // convenience: both phases with an internal rank readback
+  void cpqr_id_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,
+                   double abs_tol, cudaStream_t s);
+
+}  // namespace hssmf_b200

@@ -1,0 +1,178 @@
+// Grouped variable-size DGEMM on DMMA (mma.sync m8n8k4 f64), cp.async-staged.
+//
+// CTA tile 64x64, k-step 16, 4 warps in a 2x2 grid of 32x32 warp tiles
+// (4x4 DMMA 8x8 accumulators per warp), 3-stage cp.async pipeline. One
+// launch covers all problems of a batch: blockIdx.x enumerates tiles, the
+// owning problem is found by binary search over the tile prefix.
+#include "gemm.cuh"
+
+namespace hssmf_b200 {
+
+  namespace {
+    constexpr int BM = kGemmBM, BN = kGemmBN, BK = 16, STAGES = 3, THREADS = 128;
+    constexpr int SA = BM + 4;  // A tile stored [k][m], conflict-free fragment loads
+    constexpr int SB = BK + 4;  // B tile stored [n][k]
+    constexpr int SMEM = STAGES * (BK * SA + BN * SB) * 8;
+
+    template<bool TA, bool TB>
+    __global__ void __launch_bounds__(THREADS)
+    gemm_grouped_kernel(const GemmProblem* __restrict__ probs, const int* __restrict__ prefix,
+                        int nprob, double alpha, double beta) {
+      extern __shared__ __align__(16) double gsm[];
+      double (*As)[BK * SA] = reinterpret_cast<double (*)[BK * SA]>(gsm);
+      double (*Bs)[BN * SB] = reinterpret_cast<double (*)[BN * SB]>(gsm + STAGES * BK * SA);
+
+      // locate problem
+      const int tile = blockIdx.x;
+      int lo = 0, hi = nprob - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(prefix + mid) <= tile) lo = mid; else hi = mid - 1;
+      }
+      const GemmProblem P = probs[lo];
+      const int tiles_m = (P.m + BM - 1) / BM;
+      const int t = tile - __ldg(prefix + lo);
+      const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+      const int K = P.k;
+
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      const int wm = warp & 1, wn = warp >> 1;
+
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+      auto load_stage = [&](int st, int k0) {
+        // A tile: BM x BK logical (rows m, cols k)
+#pragma unroll
+        for (int r = 0; r < (BM * BK) / THREADS; r++) {
+          int mm, kk;
+          if (!TA) { mm = tid % BM; kk = tid / BM + r * (THREADS / BM); }
+          else { kk = tid % BK; mm = tid / BK + r * (THREADS / BK); }
+          const int gm = m0 + mm, gk = k0 + kk;
+          const bool ok = gm < P.m && gk < K;
+          const double* src = ok ? (TA ? P.A + gk + (size_t)gm * P.lda
+                                       : P.A + gm + (size_t)gk * P.lda)
+                                 : P.A;
+          cp_async8(&As[st][kk * SA + mm], src, ok);
+        }
+        // B tile: BK x BN logical (rows k, cols n)
+#pragma unroll
+        for (int r = 0; r < (BN * BK) / THREADS; r++) {
+          int nn, kk;
+          if (!TB) { kk = tid % BK; nn = tid / BK + r * (THREADS / BK); }
+          else { nn = tid % BN; kk = tid / BN + r * (THREADS / BN); }
+          const int gn = n0 + nn, gk = k0 + kk;
+          const bool ok = gn < P.n && gk < K;
+          const double* src = ok ? (TB ? P.B + gn + (size_t)gk * P.ldb
+                                       : P.B + gk + (size_t)gn * P.ldb)
+                                 : P.B;
+          cp_async8(&Bs[st][nn * SB + kk], src, ok);
+        }
+      };
+
+      const int nk = (K + BK - 1) / BK;
+#pragma unroll
+      for (int s = 0; s < STAGES - 1; s++) {
+        if (s < nk) load_stage(s, s * BK);
+        cp_async_commit();
+      }
+      const int am = wm * 32 + (lane >> 2), bn = wn * 32 + (lane >> 2), kq = lane & 3;
+      for (int kt = 0; kt < nk; kt++) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+          const int nxt = kt + STAGES - 1;
+          if (nxt < nk) load_stage(nxt % STAGES, nxt * BK);
+          cp_async_commit();
+        }
+        const double* as = As[kt % STAGES];
+        const double* bs = Bs[kt % STAGES];
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; i++) a[i] = as[(kk + kq) * SA + am + i * 8];
+#pragma unroll
+          for (int j = 0; j < 4; j++) b[j] = bs[(bn + j * 8) * SB + kk + kq];
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) dmma8x8x4(acc[i][j], a[i], b[j]);
+        }
+      }
+      cp_async_wait<0>();
+
+      // epilogue
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int r = m0 + wm * 32 + i * 8 + (lane >> 2);
+        if (r >= P.m) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            const int c = n0 + wn * 32 + j * 8 + 2 * kq + v;
+            if (c >= P.n) continue;
+            double* cp = P.C + r + (size_t)c * P.ldc;
+            const double x = alpha * acc[i][j][v];
+            *cp = beta == 0.0 ? x : x + beta * *cp;
+          }
+      }
+    }
+  }  // namespace
+
+  std::vector<int> gemm_tile_prefix(const std::vector<GemmProblem>& p) {
+    std::vector<int> pre(p.size() + 1, 0);
+    for (size_t i = 0; i < p.size(); i++)
+      pre[i + 1] = pre[i] + ceil_div(p[i].m, BM) * ceil_div(p[i].n, BN);
+    return pre;
+  }
+
+  double gemm_flops(const std::vector<GemmProblem>& p) {
+    double f = 0;
+    for (const auto& q : p) f += 2.0 * q.m * q.n * q.k;
+    return f;
+  }
+
+  void gemm_run(const GemmBatchDev& b, char ta, char tb, double alpha, double beta,
+                cudaStream_t s) {
+    if (b.nprob == 0 || b.tiles == 0) return;
+    const bool TA = ta != 'N', TB = tb != 'N';
+    static bool attr = false;
+    if (!attr) {
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      attr = true;
+    }
+    dim3 grid(b.tiles), block(THREADS);
+    if (!TA && !TB) gemm_grouped_kernel<false, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
+    else if (TA && !TB) gemm_grouped_kernel<true, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
+    else if (!TA && TB) gemm_grouped_kernel<false, true><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
+    else gemm_grouped_kernel<true, true><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
+    HSSMF_LAUNCH_CHECK();
+  }
+
+  void gemm_run_host(const std::vector<GemmProblem>& p, char ta, char tb, double alpha,
+                     double beta, cudaStream_t s) {
+    std::vector<GemmProblem> q;
+    for (const auto& x : p)
+      if (x.m > 0 && x.n > 0) q.push_back(x);
+    if (q.empty()) return;
+    auto pre = gemm_tile_prefix(q);
+    const size_t pb = q.size() * sizeof(GemmProblem), xb = pre.size() * sizeof(int);
+    void* d = nullptr;
+    HSSMF_CUDA(cudaMallocAsync(&d, pb + xb, s));
+    HSSMF_CUDA(cudaMemcpyAsync(d, q.data(), pb, cudaMemcpyHostToDevice, s));
+    HSSMF_CUDA(cudaMemcpyAsync((char*)d + pb, pre.data(), xb, cudaMemcpyHostToDevice, s));
+    GemmBatchDev b{(const GemmProblem*)d, (const int*)((char*)d + pb), (int)q.size(),
+                   pre.back()};
+    gemm_run(b, ta, tb, alpha, beta, s);
+    HSSMF_CUDA(cudaFreeAsync(d, s));
+  }
+
+}  // namespace hssmf_b200

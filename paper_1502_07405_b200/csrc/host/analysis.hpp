@@ -1,0 +1,81 @@
+// Host-side symbolic analysis for the HSS-multifrontal path.
+//
+// Everything here is integer structure (plus the grid generators' values)
+// whose outputs must be bit-exact with the reference; it stays on the host
+// as the north star allows. Written fresh against the reference semantics:
+//   grid generators       grid_problems.hpp:65-117
+//   CSR permutation       sparse_matrix.hpp:24-46, 95-102
+//   geometric ND          ordering.cpp:123-169, 213-222
+//   etree from separators elimination_tree.cpp:10-35
+//   symbolic upd sets     elimination_tree.cpp:148-189
+//   cluster trees         cluster_tree.hpp:38-61, 90-96
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+namespace hssmf_b200 {
+
+  // square CSR, sorted duplicate-free rows (sparse_matrix.hpp:14-47)
+  struct Csr {
+    int n = 0;
+    std::vector<int> ptr{0}, ind;
+    std::vector<double> val;
+    std::int64_t nnz() const { return (std::int64_t)ind.size(); }
+    double get(int i, int j) const;
+    // symmetric permutation B[p[i]][p[j]] = A[i][j]
+    Csr permuted(const std::vector<int>& p) const;
+    // structurally symmetrized adjacency without the diagonal
+    void symmetric_graph(std::vector<int>& gptr, std::vector<int>& gind) const;
+  };
+
+  struct Geometry {
+    std::array<int, 3> dims{1, 1, 1};
+    int ndims = 0;
+    int vertex(int i, int j, int l) const { return i + dims[0] * (j + dims[1] * l); }
+  };
+
+  enum GridKind { P2D = 0, P3D = 1, C2D = 2, C3D = 3 };
+
+  Csr grid_problem(int kind, int k, double nu, Geometry& g);
+  // config 4: h^2-scaled -lap(u) + beta.grad(u) on k^3, beta = scale*(1,.5,.25)/h,
+  // first-order upwind with the reference's upwind rule (grid_problems.hpp:57-61)
+  Csr convdiff3d_const(int k, double scale, Geometry& g);
+
+  struct FrontNode {
+    int sep_begin = 0, sep_end = 0;
+    int child0 = -1, child1 = -1, parent = -1, level = 0;
+    std::vector<int> upd;
+    int ns() const { return sep_end - sep_begin; }
+    int nu() const { return (int)upd.size(); }
+    int m() const { return ns() + nu(); }
+    bool leaf() const { return child0 < 0 && child1 < 0; }
+  };
+
+  struct Etree {
+    int n = 0;
+    std::vector<FrontNode> nodes;  // postorder, root last
+    int root() const { return (int)nodes.size() - 1; }
+    void compute_levels();
+  };
+
+  // geometric nested dissection; perm[old] = new. nodes carry separators only
+  Etree nested_dissection_geometric(const Geometry& g, int leaf, std::vector<int>& perm);
+  void symbolic_factorization(const Csr& a, Etree& t);
+
+  struct Cluster {
+    int begin = 0, end = 0, child0 = -1, child1 = -1, parent = -1;
+    bool leaf() const { return child0 < 0; }
+    int size() const { return end - begin; }
+  };
+  struct ClusterTree {
+    std::vector<Cluster> nodes;  // postorder, root last
+    int root() const { return (int)nodes.size() - 1; }
+    static ClusterTree balanced(int n, int leaf);
+    static ClusterTree join(const ClusterTree& a, const ClusterTree& b);
+  };
+  // front_cluster_tree (multifrontal.hpp:318-326) without separator clusters
+  ClusterTree front_cluster_tree(int ns, int nu, int leaf);
+
+}  // namespace hssmf_b200

@@ -1,0 +1,27 @@
+// Standalone dense HSS compression + ULV (BASELINE config 2).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+namespace hssmf_b200 {
+
+  class DenseHss {
+  public:
+    explicit DenseHss(int device);
+    ~DenseHss();
+    void run(const double* a, int lda, int n, int leaf, double eps, int d0, int dd, int p,
+             int max_rank, bool on_device);
+    void solve(double* b, int ldb, int nrhs, bool on_device);
+    void ranks(std::vector<int>& u, std::vector<int>& v) const;
+    int rounds() const;
+    int d_final() const;
+    double compress_ms() const;
+    double ulv_ms() const;
+    struct Impl;
+
+  private:
+    std::unique_ptr<Impl> d_;
+  };
+
+}  // namespace hssmf_b200

@@ -1,0 +1,92 @@
+"""Kernel-level parity on the B200: DMMA GEMM vs a float64 reference, device
+LU vs the reference's lu_partial_pivot, device sampler vs SeededRowSampler,
+device CPQR/ID vs interpolative_decomposition (oracle/_ref)."""
+import numpy as np
+import pytest
+
+import paper_1502_07405_b200.api as A
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (64, 64, 16), (130, 67, 45),
+                                   (257, 129, 300)])
+def test_gemm_matches_fp64(ta, tb, m, n, k):
+    rng = np.random.default_rng(m * 1000 + n * 10 + k)
+    a = rng.standard_normal((m, k) if ta == "N" else (k, m))
+    b = rng.standard_normal((k, n) if tb == "N" else (n, k))
+    c = rng.standard_normal((m, n))
+    got = A.dev_gemm(ta, tb, -0.5, a, b, 2.0, c)
+    oa = a if ta == "N" else a.T
+    ob = b if tb == "N" else b.T
+    want = -0.5 * oa @ ob + 2.0 * c
+    # fp64 tolerance: k * eps * |a||b|
+    tol = 8 * k * np.finfo(float).eps * (np.abs(oa) @ np.abs(ob) + np.abs(c)).max()
+    assert np.abs(got - want).max() <= tol
+
+
+def test_gemm_beta_zero_ignores_nan():
+    a = np.ones((9, 4))
+    b = np.ones((4, 6))
+    c = np.full((9, 6), np.nan)
+    got = A.dev_gemm("N", "N", 1.0, a, b, 0.0, c)
+    assert np.all(got == 4.0)
+
+
+def test_sampler_matches_reference(oracle):
+    # test_sampler.cpp:34-41 rows, plus a spread of others; LCG states are
+    # integer-exact, Box-Muller differs from glibc by at most a few ulp
+    rows = np.array([0, 1, 5, 31, 4096, 1000000, 2**31 - 2, 2**31 - 1, 123456789], np.int64)
+    for c0, c1 in [(0, 10), (3, 8), (0, 257), (128, 384)]:
+        got = A.dev_random_rows(rows, c0, c1)
+        want = oracle.random_rows(rows, c0, c1)
+        assert np.allclose(got, want, rtol=1e-13, atol=1e-15)
+        assert np.mean(got == want) > 0.9
+
+
+@pytest.mark.parametrize("n", [1, 5, 32, 33, 100, 257])
+def test_lu_matches_reference(oracle, n):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n))
+    got, piv = A.dev_lu(a)
+    want, wpiv, col = oracle.lu(a)
+    assert col == -1
+    assert np.array_equal(piv, wpiv)
+    assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+def test_lu_singular_column(oracle):
+    # test_lu.cpp: an exactly zero column raises with its index
+    a = np.array([[1.0, 0.0, 2.0], [2.0, 0.0, 1.0], [3.0, 0.0, 5.0]])
+    with pytest.raises(A.SingularMatrixError) as e:
+        A.dev_lu(a)
+    assert e.value.column() == 1
+    assert oracle.lu(a)[2] == 1
+
+
+@pytest.mark.parametrize("m,n,rank", [(40, 30, 7), (128, 64, 20), (16, 50, 16), (300, 200, 60)])
+def test_id_matches_reference(oracle, m, n, rank):
+    rng = np.random.default_rng(m + n)
+    y = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n))
+    y += 1e-9 * rng.standard_normal((m, n))
+    for eps, mr, at in [(1e-6, -1, 0.0), (1e-12, -1, 0.0), (1e-6, rank // 2, 0.0),
+                        (1e-3, -1, 1e-2)]:
+        p, k, cert, x = A.dev_interpolative_decomposition(y, eps, mr, at)
+        wp, wk, wcert, wx = oracle.interpolative_decomposition(y, eps, mr, at)
+        assert k == wk and cert == wcert
+        assert np.array_equal(p[:k], wp[:k])
+        if k and n > k:
+            assert np.allclose(x, wx, rtol=1e-7, atol=1e-9 * np.abs(wx).max())
+        # interpolation property Y ~= Y(:,J) [I X] Pi^T
+        if k:
+            J = p[:k]
+            full = np.zeros((k, n))
+            full[:, J] = np.eye(k)
+            full[:, p[k:]] = x
+            assert np.linalg.norm(y[:, J] @ full - y) <= 1e3 * max(eps, 1e-12) * np.linalg.norm(y) + 1e-6
+
+
+def test_id_zero_and_empty():
+    p, k, cert, _ = A.dev_interpolative_decomposition(np.zeros((8, 5)), 1e-6)
+    assert k == 0 and cert and list(p) == [0, 1, 2, 3, 4]
