@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: HSS-multifrontal factor + solve on B200 (BASELINE.json metric
+"factor+solve time (s) ... 3D Poisson 128^3").
+
+A step = one numeric factorization + one solve of the configured workload
+(default: BASELINE config 5, 3D Poisson 128^3). Analysis (ordering, etree,
+symbolic) is input preparation and stays outside the timed region, as in the
+reference's own measurement protocol.
+
+  value : device-resident inputs (matrix values and b already in HBM), wall
+          time of K steps bracketed by cuda synchronize + barrier, max over ranks
+  e2e   : the public API call a user makes - mf_factor(A, tree, opts) with host
+          CSR + mf_solve_new(m, b_host) - host<->device copies inside the region
+  --impl reference : the reference CPU implementation (oracle/_ref, compiled
+          from /root/reference) on the host cores, on a bounded subtree sample of
+          the same workload, scaled by algorithmic flops to the full workload
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_CONFIG = "c5_mf"
+
+
+def dense_flops(ns, nu):
+    ns = ns.astype(np.float64)
+    nu = nu.astype(np.float64)
+    return 2 * ns ** 3 / 3 + 2 * ns ** 2 * nu + 2 * ns * nu ** 2
+
+
+def build_problem(cfg):
+    import paper_1502_07405_b200 as P
+    if cfg.kind == "cd3d":
+        g = P.generate_convdiff3d(cfg.k, 0.1)
+    else:
+        g = P.generate_grid_problem(cfg.kind, cfg.k)
+    return P.ordered_problem(g, cfg.nd_leaf)
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ peaks --------
+def measured_peaks(torch, dev):
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        peaks["hbm_gbs"] = float(mp["hbm_gbs"])
+        peaks["hbm_src"] = "MEASURED_PEAKS.json"
+    except Exception:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["hbm_src"] = "fallback B200_PROFILING.md"
+    # FP64: MEASURED_PEAKS.json has no FP64 entry; measure cuBLAS DGEMM (burst)
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize(dev)
+    best = 1e30
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1))
+    peaks["fp64_tflops"] = 2 * n ** 3 / best / 1e9
+    peaks["fp64_src"] = "measured in-run: cuBLAS DGEMM 8192^3 burst (torch float64 matmul)"
+    del a, b
+    torch.cuda.empty_cache()
+    return peaks
+
+
+# ------------------------------------------------------ reference sample ---
+def subtree_sample(op, target_flops):
+    """pick the leftmost subtree whose dense-front flops approach target_flops
+    and build its principal submatrix + relabelled tree (a self-contained
+    subproblem of the same workload); returns (pieces, sample_flops, desc)"""
+    t = op.t
+    ns = (t.sep_end - t.sep_begin).astype(np.int64)
+    nu = np.diff(t.upd_ptr).astype(np.int64)
+    fl = dense_flops(ns, nu)
+    nn = t.size()
+    sub = fl.copy()
+    lo = np.arange(nn)
+    for i in range(nn):  # postorder: children first
+        for c in (t.child0[i], t.child1[i]):
+            if c >= 0:
+                sub[i] += sub[c]
+                lo[i] = min(lo[i], lo[c])
+    # walk down from the root along child0 until the subtree fits the target
+    s = t.root_id()
+    while sub[s] > target_flops and t.child0[s] >= 0:
+        s = t.child0[s]
+    ids = np.arange(lo[s], s + 1)
+    start = int(t.sep_begin[lo[s]])
+    end = int(t.sep_end[s])
+    ptr, ind, val = op.a.arrays()
+    rows_ptr = [0]
+    sind, sval = [], []
+    for r in range(start, end):
+        cols = ind[ptr[r]:ptr[r + 1]]
+        keep = (cols >= start) & (cols < end)
+        sind.append(cols[keep] - start)
+        sval.append(val[ptr[r]:ptr[r + 1]][keep])
+        rows_ptr.append(rows_ptr[-1] + int(keep.sum()))
+    sptr = np.array(rows_ptr, np.int32)
+    sind = np.concatenate(sind).astype(np.int32)
+    sval = np.concatenate(sval)
+    off = lo[s]
+    remap = lambda v: np.where(v >= 0, v - off, -1).astype(np.int32)  # noqa: E731
+    par = remap(t.parent[ids])
+    par[-1] = -1
+    upd = []
+    for i in ids:
+        u = t.upd(i)
+        upd.append((u[u < end] - start).astype(np.int32))
+    up = np.zeros(len(ids) + 1, np.int32)
+    for q, u in enumerate(upd):
+        up[q + 1] = up[q] + len(u)
+    pieces = dict(n=end - start, ptr=sptr, ind=sind, val=sval,
+                  sep_begin=(t.sep_begin[ids] - start).astype(np.int32),
+                  sep_end=(t.sep_end[ids] - start).astype(np.int32),
+                  child0=remap(t.child0[ids]), child1=remap(t.child1[ids]), parent=par,
+                  upd_ptr=up, upd_ind=np.concatenate(upd) if upd else np.zeros(0, np.int32))
+    sns = (pieces["sep_end"] - pieces["sep_begin"]).astype(np.int64)
+    snu = np.diff(up).astype(np.int64)
+    sfl = float(dense_flops(sns, snu).sum())
+    desc = (f"subtree of front {s} (level {t.level[s]}, {len(ids)} fronts, n={end - start}) "
+            f"= {sfl / fl.sum():.4f} of the workload's dense-front flops")
+    return pieces, sfl, float(fl.sum()), desc
+
+
+def run_reference_sample(cfg, pieces, threads):
+    from oracle import ref
+    ref.set_threads(threads)
+    o = ref.ordered_from_arrays(pieces["n"], pieces["ptr"], pieces["ind"], pieces["val"],
+                                pieces["sep_begin"], pieces["sep_end"], pieces["child0"],
+                                pieces["child1"], pieces["parent"], pieces["upd_ptr"],
+                                pieces["upd_ind"])
+    from paper_1502_07405_b200.problems import csr_matvec, x_true
+    b = csr_matvec(pieces["ptr"], pieces["ind"], pieces["val"], x_true(pieces["n"], 1))
+    mode = {"auto": 0, "mf": 1, "mf-hss": 2}[cfg.mode]
+    t0 = time.perf_counter()
+    F = ref.Factors(o, eps=cfg.eps, ls=cfg.ls, leaf=cfg.leaf, d0=cfg.d0, dd=cfg.dd, p=cfg.p,
+                    min_hss=cfg.min_hss, mode=mode)
+    F.solve(b)
+    return time.perf_counter() - t0
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_arm(args, cfg, op):
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops)
+    thr = cpu_threads()
+    for _ in range(args.warmup):
+        run_reference_sample(cfg, pieces, thr)
+    ts = [run_reference_sample(cfg, pieces, thr) for _ in range(args.steps)]
+    t = float(np.mean(ts))
+    scaled = t * tfl / sfl
+    line = {
+        "metric": METRIC, "value": scaled, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": scaled * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_json(cfg, op, args),
+        "cpu_baseline": {"value": scaled, "unit": "s", "cores": thr, "kind": "reference",
+                         "sample": desc + f"; measured {t:.3f} s/step, scaled x{tfl / sfl:.1f}"},
+        "e2e": {"value": scaled, "unit": "s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+METRIC = "factor+solve time (s), 3D Poisson 128^3"
+
+
+def config_json(cfg, op, args):
+    return {"workload": cfg.name, "n": op.a.size(), "nnz": op.a.nnz(), "fronts": op.t.size(),
+            "nd_leaf": cfg.nd_leaf, "hss": {"ls": cfg.ls, "min_hss": cfg.min_hss,
+                                            "eps": cfg.eps, "leaf": cfg.leaf, "mode": cfg.mode},
+            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "l2": "inputs > L2 (factor storage tens of GB), no flush needed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--sample-flops", type=float, default=1.5e11)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1502_07405_b200.problems import CONFIGS
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        op = build_problem(cfg)
+        reference_arm(args, cfg, op)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_1502_07405_b200 as P
+    from paper_1502_07405_b200 import _native
+    from paper_1502_07405_b200.problems import csr_matvec, x_true
+
+    op = build_problem(cfg)
+    n = op.a.size()
+    ptr, ind, val = op.a.arrays()
+    b = csr_matvec(ptr, ind, val, x_true(n, 1))
+    opts = cfg.solver_options()
+    peaks = measured_peaks(torch, dev)
+
+    # first factorization (upload + schedule + numeric)
+    m = P.mf_factor(op.a, op.t, opts, device=local)
+    b_dev = torch.from_numpy(b).to(dev)
+    x_dev = torch.empty_like(b_dev)
+
+    def step():
+        m.refactor()
+        x_dev.copy_(b_dev)
+        torch.cuda.current_stream(dev).synchronize()
+        m.solve_device(x_dev.data_ptr(), n, 1)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    l0 = _native.lib().hssmf_launch_count()
+    t0 = time.perf_counter()
+    dev_ms = 0.0
+    for _ in range(args.steps):
+        step()
+        f, s = m.timing()
+        dev_ms += f + s
+    barrier()
+    t1 = time.perf_counter()
+    launches = (_native.lib().hssmf_launch_count() - l0) // args.steps
+    ck = clocks.stop()
+    ms = (t1 - t0) / args.steps * 1e3
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # correctness of the timed factors (relative residual)
+    x = x_dev.cpu().numpy()
+    relres = float(np.linalg.norm(op.a.matvec(x) - b) / np.linalg.norm(b))
+
+    # e2e through the public API: mf_factor(host CSR) + mf_solve_new(host b)
+    del m
+    torch.cuda.empty_cache()
+    barrier()
+    e0 = time.perf_counter()
+    for _ in range(max(1, min(args.steps, 2))):
+        m = P.mf_factor(op.a, op.t, opts, device=local)
+        xh = P.mf_solve_new(m, b)
+        del m
+    barrier()
+    e_ms = (time.perf_counter() - e0) / max(1, min(args.steps, 2)) * 1e3
+    h2d = int(ptr.nbytes + ind.nbytes + val.nbytes + b.nbytes)
+    d2h = int(xh.nbytes)
+
+    # per-kernel-class profile pass (events around each launch)
+    m = P.mf_factor(op.a, op.t, opts, device=local)
+    m.set_profile(True)
+    m.reset_kernel_stats()
+    m.refactor()
+    m.solve_device(x_dev.data_ptr(), n, 1)
+    ks = m.kernel_stats()
+    m.set_profile(False)
+    tot_ms = sum(k["ms"] for k in ks) or 1.0
+    top = max(ks, key=lambda k: k["ms"])
+    if top["flops"] > 0:
+        ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
+        roof = {"kernel": top["name"], "bound": "tensor", "achieved": ach,
+                "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": ach / peaks["fp64_tflops"], "peak_src": peaks["fp64_src"]}
+    else:
+        ach = top["bytes"] / (top["ms"] * 1e-3) / 1e9
+        roof = {"kernel": top["name"], "bound": "hbm", "achieved": ach,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                "peak_src": peaks["hbm_src"]}
+    roof["share_of_step"] = top["ms"] / tot_ms
+    roof["traffic"] = None
+    flops_total = sum(k["flops"] for k in ks)
+
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_json(cfg, op, args),
+        "device_ms_per_step": dev_ms / args.steps,
+        "relres": relres,
+        "fp64_tflops_step": flops_total / (ms * 1e-3) / 1e12,
+        "e2e": {"value": e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": ck,
+        "roofline": roof,
+        "kernels": [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in k.items()}
+                    for k in ks if k["launches"]],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            if ref.available():
+                pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops)
+                thr = cpu_threads()
+                t = run_reference_sample(cfg, pieces, thr)
+                line["cpu_baseline"] = {"value": t * tfl / sfl, "unit": "s", "cores": thr,
+                                        "kind": "reference",
+                                        "sample": desc + f"; measured {t:.3f} s, scaled x"
+                                                         f"{tfl / sfl:.1f} by flops"}
+        except Exception as e:  # reported, never fatal for the GPU arm
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

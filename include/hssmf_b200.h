@@ -171,6 +171,9 @@ int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st
  * the DMMA kernel, device-resident operands; used for the FP64 roofline */
 int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st);
 
+/* number of kernel launches this library has issued (process-wide) */
+long long hssmf_launch_count(void);
+
 const char* hssmf_version(void);
 
 #ifdef __cplusplus

@@ -34,6 +34,7 @@ _lib = None
 
 _SIGS = {
     "hssmf_version": (C.c_char_p, []),
+    "hssmf_launch_count": (C.c_longlong, []),
     "hssmf_csr_grid": (C.c_int, [C.c_int, C.c_int, C.c_double, C.POINTER(vp), i32p,
                                  C.POINTER(C.c_int), C.POINTER(Status)]),
     "hssmf_csr_convdiff3d": (C.c_int, [C.c_int, C.c_double, C.POINTER(vp), C.POINTER(Status)]),

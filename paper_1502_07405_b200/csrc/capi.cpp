@@ -16,6 +16,13 @@
 
 using namespace hssmf_b200;
 
+namespace hssmf_b200 {
+  long long& launch_counter() {
+    static long long c = 0;
+    return c;
+  }
+}  // namespace hssmf_b200
+
 struct hssmf_csr { Csr a; };
 struct hssmf_tree { Etree t; };
 struct hssmf_factors { std::unique_ptr<Engine> e; };
@@ -68,6 +75,8 @@ namespace {
 }  // namespace
 
 extern "C" {
+
+long long hssmf_launch_count(void) { return launch_counter(); }
 
 const char* hssmf_version(void) { return "hssmf_b200 0.1 (sm_100a)"; }
 

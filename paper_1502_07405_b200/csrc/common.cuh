@@ -21,7 +21,14 @@ namespace hssmf_b200 {
                                     " at " __FILE__ ":" + std::to_string(__LINE__));  \
   } while (0)
 
-#define HSSMF_LAUNCH_CHECK() HSSMF_CUDA(cudaGetLastError())
+  // host-side count of kernel launches issued by this library (bench.py
+  // reports it as gpu_launches)
+  long long& launch_counter();
+#define HSSMF_LAUNCH_CHECK()                 \
+  do {                                       \
+    ++::hssmf_b200::launch_counter();        \
+    HSSMF_CUDA(cudaGetLastError());          \
+  } while (0)
 
   inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 

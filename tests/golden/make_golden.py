@@ -1,0 +1,83 @@
+"""Generate golden fixtures from the reference (oracle/_ref) for the BASELINE
+configs: per-front stats, per-HSS-node ranks, relres, timings and (for the
+smaller configs) the solution. Runs in the build container, where
+/root/reference exists; the .npz files are committed so the GPU box needs no
+reference at run time.
+
+usage: python tests/golden/make_golden.py c1 c1_mf c3 c4 c5 [--threads N]
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import ref  # noqa: E402
+from paper_1502_07405_b200.problems import CONFIGS, csr_matvec, x_true  # noqa: E402
+
+
+def ordered(cfg):
+    if cfg.kind == "cd3d":
+        import paper_1502_07405_b200 as P  # product generator: config 4 is not a ref generator
+        g = P.generate_convdiff3d(cfg.k, 0.1)
+        ptr, ind, val = g.A.arrays()
+        return ref.ordered_csr_geom(ptr, ind, val, (cfg.k,) * 3, 3, cfg.nd_leaf)
+    return ref.ordered_grid(cfg.kind, cfg.k, cfg.nd_leaf)
+
+
+def run(name, threads):
+    cfg = CONFIGS[name]
+    ref.set_threads(threads)
+    t0 = time.time()
+    o = ordered(cfg)
+    t_an = time.time() - t0
+    b = csr_matvec(o.ptr, o.ind, o.val, x_true(o.n, 1))
+    mode = {"auto": 0, "mf": 1, "mf-hss": 2}[cfg.mode]
+    ref.lib().ref_reset_counters()
+    F = ref.Factors(o, eps=cfg.eps, ls=cfg.ls, leaf=cfg.leaf, d0=cfg.d0, dd=cfg.dd, p=cfg.p,
+                    min_hss=cfg.min_hss, mode=mode)
+    flops = ref.lib().ref_flops()
+    x = F.solve(b)[:, 0]
+    import scipy.sparse as sp
+    A = sp.csr_matrix((o.val, o.ind, o.ptr), shape=(o.n, o.n))
+    relres = np.linalg.norm(A @ x - b) / np.linalg.norm(b)
+    hss = [i for i in range(o.nnodes) if F.type[i] == 1]
+    node_u, node_v, node_ptr, rounds, dfin = [], [], [0], [], []
+    for i in hss:
+        u, v, r, d = F.front_hss(i)
+        node_u.append(u)
+        node_v.append(v)
+        node_ptr.append(node_ptr[-1] + len(u))
+        rounds.append(r)
+        dfin.append(d)
+    out = dict(
+        name=name, n=o.n, nnodes=o.nnodes, threads=threads, analysis_s=t_an,
+        factor_s=F.factor_seconds, solve_s=F.solve_seconds, flops=flops, relres=relres,
+        hss_fronts=F.hss_fronts, fallbacks=F.fallbacks, max_front_rank=F.max_front_rank,
+        factor_nnz=F.factor_nnz, rank=F.rank, type=F.type, level=F.level, dim=F.dim,
+        hss_ids=np.array(hss, np.int32),
+        node_ptr=np.array(node_ptr, np.int32),
+        node_u=np.concatenate(node_u) if node_u else np.zeros(0, np.int32),
+        node_v=np.concatenate(node_v) if node_v else np.zeros(0, np.int32),
+        rounds=np.array(rounds, np.int32), d_final=np.array(dfin, np.int32),
+        perm_sum=np.int64((o.perm.astype(np.int64) * np.arange(o.n)).sum()),
+    )
+    if o.n <= 300000:
+        out["x"] = x
+    path = os.path.join(ROOT, "tests", "golden", f"ref_{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: factor {F.factor_seconds:.2f}s solve {F.solve_seconds:.3f}s relres "
+          f"{relres:.3e} hss {F.hss_fronts} maxrank {F.max_front_rank} flops {flops:.3e}",
+          flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--threads", type=int, default=os.cpu_count())
+    a = ap.parse_args()
+    for c in a.configs:
+        run(c, a.threads)
