@@ -259,7 +259,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--sample-flops", type=float, default=1.5e11)
+    ap.add_argument("--sample-flops", type=float, default=5e11)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 

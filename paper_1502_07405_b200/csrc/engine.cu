@@ -252,6 +252,8 @@ namespace hssmf_b200 {
       h.child1 = f.child1;
       h.level = f.level;
       h.hss = 0;
+      h.ldu = h.ns;
+      h.ldc = h.nu;
       h.P = D.persist.as<double>(p_at[i]);
       h.U = D.persist.as<double>(u_at[i]);
       h.C = D.trans[f.level % 2].as<double>(c_at[i]);
@@ -316,7 +318,7 @@ namespace hssmf_b200 {
                              h.m});
             if (h.nu)  // U[k1:ns, :] -= P[k1:ns, k:k1] U[k:k1, :]
               probs.push_back({h.P + k1 + (size_t)k * h.m, h.U + k, h.U + k1, h.ns - k1, h.nu,
-                               nbk, h.m, h.ns, h.ns});
+                               nbk, h.m, h.ldu, h.ldu});
           }
         }
         P.flops_trail += gemm_flops(probs);
@@ -327,7 +329,7 @@ namespace hssmf_b200 {
       for (int i : lv[L]) {
         const auto& h = D.hf[i];
         if (h.ns && h.nu)  // C -= L21 U12 (Schur complement, multifrontal.hpp:340-344)
-          probs.push_back({h.P + h.ns, h.U, h.C, h.nu, h.nu, h.ns, h.m, h.ns, h.nu});
+          probs.push_back({h.P + h.ns, h.U, h.C, h.nu, h.nu, h.ns, h.m, h.ldu, h.ldc});
       }
       P.flops_schur = gemm_flops(probs);
       P.schur = add_batch(probs);
@@ -399,6 +401,7 @@ namespace hssmf_b200 {
           DenseKernels::lu_panel(F, ids, P.nf, sb.k, NB, D.status.as<int>(), stream_);
         });
         D.launch(K_TRSM, 0, 0, [&] {
+          DenseKernels::l21(F, ids, P.nf, sb.k, NB, P.max_nu, stream_);
           DenseKernels::swap_trsm(F, ids, P.nf, sb.k, NB, sb.max_cols, stream_);
         });
         D.launch(K_GEMM_TRAIL, 0, 0,

@@ -10,8 +10,8 @@ namespace hssmf_b200 {
     __device__ __forceinline__ double* front_at(const FrontDev& f, int i, int j) {
       if (j < f.ns) return f.P + i + (size_t)j * f.m;
       j -= f.ns;
-      if (i < f.ns) return f.U + i + (size_t)j * f.ns;
-      return f.C + (i - f.ns) + (size_t)j * f.nu;
+      if (i < f.ns) return f.U + i + (size_t)j * f.ldu;
+      return f.C + (i - f.ns) + (size_t)j * f.ldc;
     }
 
     __device__ __forceinline__ int lower_bound_dev(const int* a, int n, int key) {
@@ -74,14 +74,14 @@ namespace hssmf_b200 {
       const FrontDev c = fr[ci];
       const int bj = (int)(w - colpre[lo]);
       const int tj = pos[bj];
-      const double* src = c.C + (size_t)bj * c.nu;
+      const double* src = c.C + (size_t)bj * c.ldc;
       if (tj < f.ns) {
         double* dst = f.P + (size_t)tj * f.m;
         for (int bi = lane; bi < c.nu; bi += 32) dst[pos[bi]] += src[bi];
       } else {
         const int j = tj - f.ns;
-        double* du = f.U + (size_t)j * f.ns;
-        double* dc = f.C + (size_t)j * f.nu - f.ns;
+        double* du = f.U + (size_t)j * f.ldu;
+        double* dc = f.C + (size_t)j * f.ldc - f.ns;
         for (int bi = lane; bi < c.nu; bi += 32) {
           const int ti = pos[bi];
           (ti < f.ns ? du : dc)[ti] += src[bi];
@@ -152,16 +152,53 @@ namespace hssmf_b200 {
         }
         __syncthreads();
         const double d = sd;
-        for (int i = j + 1 + tid; i < f.m; i += PANEL_THREADS) colj[i] *= d;
+        for (int i = j + 1 + tid; i < f.ns; i += PANEL_THREADS) colj[i] *= d;
         __syncthreads();
-        // rank-1 update of the remaining panel columns
+        // rank-1 update of the remaining panel columns (F11 rows only; the
+        // L21 rows follow in l21_kernel as A21 U_kk^-1)
         for (int c = j + 1; c < k + nbk; c++) {
           double* cc = P + (size_t)c * ld;
           const double t = cc[j];
-          for (int i = j + 1 + tid; i < f.m; i += PANEL_THREADS) cc[i] -= colj[i] * t;
+          for (int i = j + 1 + tid; i < f.ns; i += PANEL_THREADS) cc[i] -= colj[i] * t;
         }
         __syncthreads();
       }
+    }
+
+    // L21 rows of the panel: x U_kk = a  (row-wise), with the same operation
+    // order as the unblocked elimination: x_j = (a_j - sum_c x_c u_cj) * (1/u_jj)
+    __global__ void __launch_bounds__(128)
+    l21_kernel(const FrontDev* __restrict__ fr, const int* __restrict__ ids, int k, int nb) {
+      const FrontDev f = fr[ids[blockIdx.y]];
+      if (f.ns <= k || f.nu == 0) return;
+      const int nbk = min(nb, f.ns - k);
+      __shared__ double Uk[32][33];
+      __shared__ double inv[32];
+      for (int e = threadIdx.x; e < nbk * nbk; e += blockDim.x) {
+        const int r = e % nbk, c = e / nbk;
+        Uk[r][c] = f.P[(k + r) + (size_t)(k + c) * f.m];
+      }
+      __syncthreads();
+      if (threadIdx.x < nbk) inv[threadIdx.x] = 1.0 / Uk[threadIdx.x][threadIdx.x];
+      __syncthreads();
+      const int i = f.ns + blockIdx.x * blockDim.x + threadIdx.x;
+      if (i >= f.m) return;
+      double* row = f.P + i + (size_t)k * f.m;
+      double x[32];
+#pragma unroll
+      for (int c = 0; c < 32; c++) x[c] = c < nbk ? row[(size_t)c * f.m] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        if (j < nbk) {
+          double v = x[j] * inv[j];
+          x[j] = v;
+#pragma unroll
+          for (int c = j + 1; c < 32; c++) x[c] -= v * Uk[j][c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; c++)
+        if (c < nbk) row[(size_t)c * f.m] = x[c];
     }
 
     constexpr int TRSM_COLS = 128;
@@ -190,7 +227,7 @@ namespace hssmf_b200 {
       bool solve;
       if (c < k) { col = f.P + (size_t)c * f.m; solve = false; }
       else if (c < f.ns - nbk) { col = f.P + (size_t)(c + nbk) * f.m; solve = true; }
-      else { col = f.U + (size_t)(c - (f.ns - nbk)) * f.ns; solve = true; }
+      else { col = f.U + (size_t)(c - (f.ns - nbk)) * f.ldu; solve = true; }
       for (int jj = 0; jj < nbk; jj++) {
         const int p = pv[jj], j = k + jj;
         if (p != j) {
@@ -290,7 +327,7 @@ namespace hssmf_b200 {
       if (r >= f.ns || !f.nu) return;
       double* xr = x + (size_t)blockIdx.z * ldx;
       double s = 0.0;
-      for (int c = 0; c < f.nu; c++) s += f.U[r + (size_t)c * f.ns] * xr[f.upd[c]];
+      for (int c = 0; c < f.nu; c++) s += f.U[r + (size_t)c * f.ldu] * xr[f.upd[c]];
       xr[f.sep_begin + r] -= s;
     }
 
@@ -362,6 +399,13 @@ namespace hssmf_b200 {
                               int* status, cudaStream_t s) {
     if (!nf) return;
     lu_panel_kernel<<<nf, PANEL_THREADS, 0, s>>>(f, ids, k, nb, status);
+    HSSMF_LAUNCH_CHECK();
+  }
+
+  void DenseKernels::l21(const FrontDev* f, const int* ids, int nf, int k, int nb, int max_nu,
+                         cudaStream_t s) {
+    if (!nf || max_nu <= 0) return;
+    l21_kernel<<<dim3(ceil_div(max_nu, 128), nf), 128, 0, s>>>(f, ids, k, nb);
     HSSMF_LAUNCH_CHECK();
   }
 

@@ -18,6 +18,7 @@ namespace hssmf_b200 {
   struct FrontDev {
     int ns, nu, m, sep_begin;
     int child0, child1, level, hss;
+    int ldu, ldc;     // leading dimensions of U and C (ns / nu for a dense front)
     double* P;
     double* U;
     double* C;        // update matrix (dense child) or densified update (HSS child)
@@ -39,6 +40,9 @@ namespace hssmf_b200 {
                            const long long* colpre, long long ncols, cudaStream_t s);
     static void lu_panel(const FrontDev* f, const int* ids, int nf, int k, int nb,
                          int* status, cudaStream_t s);
+    // L21 part of panel k: rows [ns, m) <- A21 U_kk^-1 (after lu_panel)
+    static void l21(const FrontDev* f, const int* ids, int nf, int k, int nb, int max_nu,
+                    cudaStream_t s);
     static void swap_trsm(const FrontDev* f, const int* ids, int nf, int k, int nb,
                           int max_cols, cudaStream_t s);
     // solve

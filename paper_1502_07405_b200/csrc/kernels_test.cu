@@ -77,6 +77,8 @@ namespace hssmf_b200 {
     f.ns = n;
     f.nu = 0;
     f.m = n;
+    f.ldu = n;
+    f.ldc = 1;
     f.child0 = f.child1 = -1;
     f.P = A.as<double>();
     f.piv = I.as<int>();
