@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "engine.hpp"
+#include "hss.hpp"
 #include "hss_dense.hpp"
 #include "host/analysis.hpp"
 #include "kernels_test.hpp"
@@ -52,6 +53,10 @@ namespace {
       return ok(st);
     } catch (const SolverFailure& e) {
       return fail(st, e.code, e.what(), e.front, e.column);
+    } catch (const HssSingular& e) {
+      return fail(st, HSSMF_ERR_SINGULAR, e.what(), -1, e.column);
+    } catch (const HssRankError& e) {
+      return fail(st, HSSMF_ERR_RANK, e.what(), e.node, -1);
     } catch (const CudaError& e) {
       return fail(st, HSSMF_ERR_CUDA, e.what());
     } catch (const std::exception& e) {

@@ -1,4 +1,13 @@
 // Level-synchronous multifrontal factorization / solve orchestrator.
+//
+// factor(): for every elimination-tree level, deepest first,
+//   dense fronts  -> one static batch: zero, sparse scatter, extend-add of both
+//                    children, panel LU of F11 (+ L21, U12), Schur GEMM
+//   HSS fronts    -> one at a time: dense assembly in HBM, adaptive randomized
+//                    HSS compression, partial ULV, densified low-rank update
+//                    for the parent (factor_front_hss, multifrontal.hpp:348-377);
+//                    rank-guard trip -> dense fallback on the assembled front
+// solve(): forward sweep bottom-up, backward sweep top-down, same batching.
 #include "engine.hpp"
 
 #include <algorithm>
@@ -8,6 +17,8 @@
 #include "common.cuh"
 #include "front.cuh"
 #include "gemm.cuh"
+#include "hss.hpp"
+#include "hss_kernels.cuh"
 
 namespace hssmf_b200 {
 
@@ -17,6 +28,9 @@ namespace hssmf_b200 {
     struct DevMem {
       void* p = nullptr;
       size_t bytes = 0;
+      DevMem() = default;
+      DevMem(const DevMem&) = delete;
+      DevMem(DevMem&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
       void alloc(size_t b) {
         free();
         if (b) HSSMF_CUDA(cudaMalloc(&p, b));
@@ -35,50 +49,65 @@ namespace hssmf_b200 {
 
     template<typename T> void upload(DevMem& m, const std::vector<T>& v) {
       m.alloc(std::max<size_t>(v.size() * sizeof(T), 16));
-      if (!v.empty()) HSSMF_CUDA(cudaMemcpy(m.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+      if (!v.empty())
+        HSSMF_CUDA(cudaMemcpy(m.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     }
 
+    // analytic per-front estimates (multifrontal.hpp:391-396)
     inline long long dense_front_flops(long long ns, long long nu) {
       return 2 * ns * ns * ns / 3 + 2 * ns * ns * nu + 2 * ns * nu * nu;
     }
+    inline long long hss_front_flops(long long m, long long r, long long d) {
+      return 4 * m * m * d + 8 * m * r * r;
+    }
 
-    enum KClass { K_ASM, K_EXTADD, K_PANEL, K_TRSM, K_GEMM_TRAIL, K_GEMM_SCHUR, K_SOLVE_FWD,
-                  K_SOLVE_BWD, K_NCLASS };
+    enum KClass { K_ASM, K_EXTADD, K_PANEL, K_TRSM, K_GEMM_TRAIL, K_GEMM_SCHUR, K_HSS,
+                  K_SOLVE_FWD, K_SOLVE_BWD, K_NCLASS };
     const char* kclass_name[K_NCLASS] = {"assemble_sparse", "extend_add", "lu_panel",
-                                         "swap_trsm", "gemm_trailing", "gemm_schur",
-                                         "solve_forward", "solve_backward"};
+                                         "l21_swap_trsm", "gemm_trailing", "gemm_schur",
+                                         "hss_front", "solve_forward", "solve_backward"};
   }  // namespace
 
   struct StepBatch {
     int k = 0, max_cols = 0;
     GemmBatchDev trail;
+    double flops = 0;
   };
 
   struct LevelPlan {
-    int ids_off = 0, nf = 0;
-    int max_ns = 0, max_nu = 0, max_m = 0;
-    size_t p_off = 0, p_bytes = 0;    // persistent P/U region (bytes)
-    size_t c_off = 0, c_bytes = 0;    // transient C region within its parity half
-    size_t b_off = 0, b_count = 0;    // bupd region (doubles per rhs)
+    int ids_off = 0, nf = 0;        // all fronts of the level (fold)
+    int dids_off = 0, ndf = 0;      // dense fronts (static factor plan)
+    int sids_off = 0, nsf = 0;      // dense + fallback fronts (solve), rebuilt per factor
+    std::vector<int> hss;           // HSS fronts (host)
+    int max_ns = 0, max_nu = 0;
+    size_t p_off = 0, p_bytes = 0;  // persistent P/U region (bytes)
+    size_t c_bytes = 0;             // transient C region within its parity half
+    size_t b_off = 0, b_count = 0;  // bupd region (doubles per rhs)
     long long ncols[2] = {0, 0};
     int max_child_nu[2] = {0, 0};
     size_t colpre_off[2] = {0, 0};
     std::vector<StepBatch> steps;
     GemmBatchDev schur;
-    double flops_trail = 0, flops_schur = 0, bytes_ea = 0;
+    double flops_schur = 0, bytes_ea[2] = {0, 0}, bytes_asm = 0;
   };
 
   struct Engine::Impl {
     Csr a;
     Etree t;
     Options opt;
-    std::vector<FrontDev> hf;
-    std::vector<LevelPlan> levels;  // index = tree level
+    std::vector<FrontDev> hf, hf0;  // live descriptors, analysis-time descriptors
+    std::vector<LevelPlan> levels;
+    std::vector<std::vector<int>> lv;  // front ids per tree level
     std::vector<long long> bupd_off;
-    DevMem d_ptr, d_ind, d_val, d_upd, d_pos, d_fronts, d_ids, d_colpre, d_gemm, d_gpre;
-    DevMem persist, ipersist, trans[2], bupd, status, xbuf;
+    std::vector<char> want_hss;
+    DevMem d_ptr, d_ind, d_val, d_upd, d_pos, d_fronts, d_ids, d_colpre, d_gemm, d_gpre, d_sids;
+    DevMem persist, ipersist, trans[2], bupd, status, xbuf, x2buf, scratch;
+    std::vector<DevMem> fallback_mem;
+    std::vector<std::unique_ptr<HssMatrixDev>> hss;
+    std::vector<int> hss_rounds, hss_dfinal;
     int bupd_nr = 1;
     size_t bupd_total = 0;
+    int n_hss = 0, n_fallback = 0, max_rank = 0;
     // profiling
     struct Ev { int cls; cudaEvent_t a, b; double flops, bytes; };
     std::vector<Ev> evs;
@@ -98,7 +127,10 @@ namespace hssmf_b200 {
       return e;
     }
     template<typename F> void launch(int cls, double flops, double bytes, F&& f) {
-      if (!profile) { f(); return; }
+      if (!profile) {
+        f();
+        return;
+      }
       Ev e{cls, get_ev(), get_ev(), flops, bytes};
       HSSMF_CUDA(cudaEventRecord(e.a, s));
       f();
@@ -120,25 +152,50 @@ namespace hssmf_b200 {
       evs.clear();
     }
     ~Impl() {
-      for (auto& e : evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+      hss.clear();
+      if (s) cudaStreamSynchronize(s);
+      for (auto& e : evs) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+      }
       for (auto e : pool) cudaEventDestroy(e);
     }
-    void set_bupd_capacity(int nr);
+    void upload_fronts() {
+      HSSMF_CUDA(cudaMemcpyAsync(d_fronts.p, hf.data(), hf.size() * sizeof(FrontDev),
+                                 cudaMemcpyHostToDevice, s));
+      HSSMF_CUDA(cudaStreamSynchronize(s));
+    }
+    void upload_front(int i) {
+      HSSMF_CUDA(cudaMemcpyAsync(d_fronts.as<FrontDev>() + i, &hf[i], sizeof(FrontDev),
+                                 cudaMemcpyHostToDevice, s));
+      HSSMF_CUDA(cudaStreamSynchronize(s));
+    }
+    void set_bupd_capacity(int nr) {
+      bupd_nr = std::max(nr, 1);
+      bupd.alloc(std::max<size_t>(bupd_total * bupd_nr * sizeof(double), 16));
+      for (size_t i = 0; i < hf.size(); i++) {
+        hf[i].bupd = bupd.as<double>() + bupd_off[i] * bupd_nr;
+        hf0[i].bupd = hf[i].bupd;
+      }
+      upload_fronts();
+    }
+    int* scratch_ints(size_t n) {
+      if (scratch.bytes < n * sizeof(int)) scratch.alloc(std::max<size_t>(n * sizeof(int), 4096));
+      return scratch.as<int>();
+    }
+    void factor_hss_front(int i, int level);
   };
-
-  void Engine::Impl::set_bupd_capacity(int nr) {
-    bupd_nr = std::max(nr, 1);
-    bupd.alloc(std::max<size_t>(bupd_total * bupd_nr * sizeof(double), 16));
-    for (size_t i = 0; i < hf.size(); i++) hf[i].bupd = bupd.as<double>() + bupd_off[i] * bupd_nr;
-    HSSMF_CUDA(cudaMemcpy(d_fronts.p, hf.data(), hf.size() * sizeof(FrontDev),
-                          cudaMemcpyHostToDevice));
-  }
 
   Engine::Engine(int device) : d_(new Impl), device_(device) {
     HSSMF_CUDA(cudaSetDevice(device));
     HSSMF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     d_->s = stream_;
     for (int k = 0; k < K_NCLASS; k++) d_->kstat[k].name = kclass_name[k];
+    // keep stream-ordered allocations (HSS path) in the pool between factorizations
+    cudaMemPool_t mp;
+    HSSMF_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
+    unsigned long long thr = ~0ull;
+    HSSMF_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
   }
 
   Engine::~Engine() {
@@ -161,7 +218,6 @@ namespace hssmf_b200 {
     int nlev = 0;
     for (const auto& f : D.t.nodes) nlev = std::max(nlev, f.level + 1);
 
-    // upload CSR
     upload(D.d_ptr, a.ptr);
     upload(D.d_ind, a.ind);
     upload(D.d_val, a.val);
@@ -191,15 +247,22 @@ namespace hssmf_b200 {
     upload(D.d_upd, upd_all);
     upload(D.d_pos, pos_all);
 
-    // level lists
-    std::vector<std::vector<int>> lv(nlev);
+    // HSS selection (multifrontal.hpp:410-412)
+    D.want_hss.assign(nn, 0);
+    for (int i = 0; i < nn; i++) {
+      const auto& f = D.t.nodes[i];
+      D.want_hss[i] = f.level < o.switch_level() && f.m() >= o.min_hss && f.ns() > 0;
+    }
+
+    D.lv.assign(nlev, {});
+    auto& lv = D.lv;
     for (int i = 0; i < nn; i++) lv[D.t.nodes[i].level].push_back(i);
     D.levels.assign(nlev, LevelPlan());
     std::vector<int> ids;
 
     // persistent / transient layout, level-major from the deepest level
     size_t poff = 0, ipoff = 0, cmax[2] = {0, 0}, boff = 0;
-    std::vector<size_t> p_at(nn), u_at(nn), c_at(nn), piv_at(nn);
+    std::vector<size_t> p_at(nn, 0), u_at(nn, 0), c_at(nn), piv_at(nn, 0);
     D.bupd_off.assign(nn, 0);
     for (int L = nlev - 1; L >= 0; L--) {
       auto& P = D.levels[L];
@@ -207,30 +270,40 @@ namespace hssmf_b200 {
       P.nf = (int)lv[L].size();
       ids.insert(ids.end(), lv[L].begin(), lv[L].end());
       P.p_off = poff;
+      P.b_off = boff;
       size_t coff = 0;
       for (int i : lv[L]) {
         const auto& f = D.t.nodes[i];
         const size_t ns = f.ns(), nu = f.nu(), m = ns + nu;
         P.max_ns = std::max(P.max_ns, (int)ns);
         P.max_nu = std::max(P.max_nu, (int)nu);
-        P.max_m = std::max(P.max_m, (int)m);
+        c_at[i] = coff;
+        coff += ((nu * nu * 8 + 255) / 256) * 256;
+        D.bupd_off[i] = boff;
+        boff += nu;
+        if (D.want_hss[i]) {
+          P.hss.push_back(i);
+          continue;
+        }
         p_at[i] = poff;
         poff += ((m * ns * 8 + 255) / 256) * 256;
         u_at[i] = poff;
         poff += ((ns * nu * 8 + 255) / 256) * 256;
-        c_at[i] = coff;
-        coff += ((nu * nu * 8 + 255) / 256) * 256;
         piv_at[i] = ipoff;
         ipoff += 2 * ns;
-        D.bupd_off[i] = boff;
-        boff += nu;
       }
-      P.b_off = boff - [&] { size_t c = 0; for (int i : lv[L]) c += D.t.nodes[i].nu(); return c; }();
       P.b_count = boff - P.b_off;
       P.p_bytes = poff - P.p_off;
-      P.c_off = 0;
       P.c_bytes = coff;
       cmax[L % 2] = std::max(cmax[L % 2], coff);
+    }
+    // dense-front id lists (static plan)
+    for (int L = nlev - 1; L >= 0; L--) {
+      auto& P = D.levels[L];
+      P.dids_off = (int)ids.size();
+      for (int i : lv[L])
+        if (!D.want_hss[i]) ids.push_back(i);
+      P.ndf = (int)ids.size() - P.dids_off;
     }
     D.bupd_total = boff;
     D.persist.alloc(std::max<size_t>(poff, 256));
@@ -251,22 +324,23 @@ namespace hssmf_b200 {
       h.child0 = f.child0;
       h.child1 = f.child1;
       h.level = f.level;
-      h.hss = 0;
+      h.hss = D.want_hss[i];
       h.ldu = h.ns;
       h.ldc = h.nu;
-      h.P = D.persist.as<double>(p_at[i]);
-      h.U = D.persist.as<double>(u_at[i]);
+      h.P = D.want_hss[i] ? nullptr : D.persist.as<double>(p_at[i]);
+      h.U = D.want_hss[i] ? nullptr : D.persist.as<double>(u_at[i]);
       h.C = D.trans[f.level % 2].as<double>(c_at[i]);
-      h.piv = D.ipersist.as<int>() + piv_at[i];
-      h.perm = h.piv + h.ns;
+      h.piv = D.want_hss[i] ? nullptr : D.ipersist.as<int>() + piv_at[i];
+      h.perm = h.piv ? h.piv + h.ns : nullptr;
       h.upd = D.d_upd.as<int>() + upd_off[i];
       h.pos0 = pos_off0[i] >= 0 ? D.d_pos.as<int>() + pos_off0[i] : nullptr;
       h.pos1 = pos_off1[i] >= 0 ? D.d_pos.as<int>() + pos_off1[i] : nullptr;
     }
+    D.hf0 = D.hf;
     D.d_fronts.alloc(nn * sizeof(FrontDev));
     D.set_bupd_capacity(1);
 
-    // extend-add column prefixes and GEMM batches
+    // extend-add column prefixes (dense fronts) and GEMM batches
     std::vector<long long> colpre;
     std::vector<GemmProblem> gp;
     std::vector<int> gpre;
@@ -284,28 +358,42 @@ namespace hssmf_b200 {
     };
     for (int L = nlev - 1; L >= 0; L--) {
       auto& P = D.levels[L];
+      std::vector<int> dl;
+      for (int i : lv[L])
+        if (!D.want_hss[i]) dl.push_back(i);
+      int dmax_ns = 0;
+      for (int i : dl) {
+        dmax_ns = std::max(dmax_ns, D.hf[i].ns);
+        P.bytes_asm += 8.0 * ((double)D.hf[i].m * D.hf[i].ns + (double)D.hf[i].ns * D.hf[i].nu +
+                              (double)D.hf[i].nu * D.hf[i].nu);
+      }
       for (int slot = 0; slot < 2; slot++) {
         P.colpre_off[slot] = colpre.size();
         long long acc = 0;
-        for (int q = 0; q < P.nf; q++) {
+        for (int i : dl) {
           colpre.push_back(acc);
-          const auto& f = D.t.nodes[lv[L][q]];
+          const auto& f = D.t.nodes[i];
           const int c = slot ? f.child1 : f.child0;
           if (c >= 0) {
             const long long nuc = D.t.nodes[c].nu();
-            P.max_child_nu[slot] = std::max(P.max_child_nu[slot], (int)nuc);
             acc += nuc;
-            P.bytes_ea += 24.0 * nuc * nuc + 4.0 * nuc;
+            // read cb 8 + read-modify-write the parent 16 + map 4
+            P.bytes_ea[slot] += 24.0 * nuc * nuc + 4.0 * nuc;
           }
         }
         colpre.push_back(acc);
         P.ncols[slot] = acc;
       }
-      for (int k = 0; k < P.max_ns; k += NB) {
+      for (int i : lv[L])
+        for (int slot = 0; slot < 2; slot++) {
+          const int c = slot ? D.t.nodes[i].child1 : D.t.nodes[i].child0;
+          if (c >= 0) P.max_child_nu[slot] = std::max(P.max_child_nu[slot], D.t.nodes[c].nu());
+        }
+      for (int k = 0; k < dmax_ns; k += NB) {
         StepBatch sb;
         sb.k = k;
         std::vector<GemmProblem> probs;
-        for (int i : lv[L]) {
+        for (int i : dl) {
           const auto& h = D.hf[i];
           if (h.ns <= k) continue;
           const int nbk = std::min(NB, h.ns - k);
@@ -321,12 +409,12 @@ namespace hssmf_b200 {
                                nbk, h.m, h.ldu, h.ldu});
           }
         }
-        P.flops_trail += gemm_flops(probs);
+        sb.flops = gemm_flops(probs);
         sb.trail = add_batch(probs);
         P.steps.push_back(sb);
       }
       std::vector<GemmProblem> probs;
-      for (int i : lv[L]) {
+      for (int i : dl) {
         const auto& h = D.hf[i];
         if (h.ns && h.nu)  // C -= L21 U12 (Schur complement, multifrontal.hpp:340-344)
           probs.push_back({h.P + h.ns, h.U, h.C, h.nu, h.nu, h.ns, h.m, h.ldu, h.ldc});
@@ -346,6 +434,10 @@ namespace hssmf_b200 {
       for (auto& sb : P.steps) fix(sb.trail);
       fix(P.schur);
     }
+    D.hss.clear();
+    D.hss.resize(nn);
+    D.hss_rounds.assign(nn, 0);
+    D.hss_dfinal.assign(nn, 0);
 
     stats_.assign(nn, FrontStat());
     for (int i = 0; i < nn; i++) {
@@ -368,11 +460,116 @@ namespace hssmf_b200 {
     factored_ = false;
   }
 
+  // one HSS front (factor_front_hss, multifrontal.hpp:348-377) with the
+  // rank-guard fallback of factor_front (multifrontal.hpp:414-421)
+  void Engine::Impl::factor_hss_front(int i, int level) {
+    const auto& fn = t.nodes[i];
+    auto& h = hf[i];
+    const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
+    double* F = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&F, (size_t)m * m * sizeof(double) + 8, s));
+    HSSMF_CUDA(cudaMemsetAsync(F, 0, (size_t)m * m * sizeof(double), s));
+    // dense assembly of the front in HBM: temporary descriptor over F
+    FrontDev view = h;
+    view.P = F;
+    view.U = F + (size_t)ns * m;
+    view.C = F + ns + (size_t)ns * m;
+    view.ldu = m;
+    view.ldc = m;
+    int* scr = scratch_ints(ns + 8);
+    view.perm = scr + 8;
+    hf[i] = view;
+    upload_front(i);
+    std::vector<int> one_id{i};
+    std::vector<long long> cp0{0, fn.child0 >= 0 ? t.nodes[fn.child0].nu() : 0};
+    std::vector<long long> cp1{0, fn.child1 >= 0 ? t.nodes[fn.child1].nu() : 0};
+    HSSMF_CUDA(cudaMemcpyAsync(scr, one_id.data(), sizeof(int), cudaMemcpyHostToDevice, s));
+    long long* dcp = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&dcp, 4 * sizeof(long long), s));
+    HSSMF_CUDA(cudaMemcpyAsync(dcp, cp0.data(), 2 * sizeof(long long), cudaMemcpyHostToDevice, s));
+    HSSMF_CUDA(cudaMemcpyAsync(dcp + 2, cp1.data(), 2 * sizeof(long long), cudaMemcpyHostToDevice, s));
+    const FrontDev* Fd = d_fronts.as<FrontDev>();
+    DenseKernels::assemble_sparse(Fd, scr, 1, d_ptr.as<int>(), d_ind.as<int>(), d_val.as<double>(), s);
+    DenseKernels::extend_add(Fd, scr, 1, 0, dcp, cp0[1], s);
+    DenseKernels::extend_add(Fd, scr, 1, 1, dcp + 2, cp1[1], s);
+    HSSMF_CUDA(cudaFreeAsync(dcp, s));
+
+    auto tree = front_cluster_tree(ns, nu, opt.leaf);
+    std::vector<long long> seeds(m);
+    for (int l = 0; l < m; l++) seeds[l] = l < ns ? fn.sep_begin + l : fn.upd[l - ns];
+    HssOpts ho;
+    ho.eps = opt.eps;
+    ho.d0 = std::min(opt.d0, m + opt.p);
+    ho.dd = opt.dd;
+    ho.p = opt.p;
+    ho.max_rank = std::min(opt.resolved_max_rank(t.n), m);
+    auto H = std::make_unique<HssMatrixDev>(s);
+    bool fallback = false;
+    try {
+      H->compress(F, m, tree, seeds, ho);
+      if (nu) H->ulv_partial(hf0[i].C, nu);
+      else H->ulv_full();
+    } catch (const HssRankError&) {
+      fallback = true;
+    } catch (const HssSingular& e) {
+      HSSMF_CUDA(cudaFreeAsync(F, s));
+      hf[i] = hf0[i];
+      upload_front(i);
+      throw SolverFailure(3, i, e.column,
+                          "front " + std::to_string(i) + ": " + e.what());
+    }
+    if (!fallback) {
+      H->drop_dense();
+      HSSMF_CUDA(cudaFreeAsync(F, s));
+      hf[i] = hf0[i];
+      hf[i].hss = 1;
+      upload_front(i);
+      hss[i] = std::move(H);
+      return;
+    }
+    // rank guard tripped: densify this front (factor_front_dense on the
+    // assembled front); F becomes the front's persistent storage
+    H.reset();
+    DevMem keep;
+    keep.p = F;  // adopt (freed with the engine's fallback list)
+    keep.bytes = (size_t)m * m * sizeof(double);
+    DevMem piv;
+    piv.alloc(2 * (size_t)ns * sizeof(int) + 8);
+    FrontDev f = view;
+    f.hss = 0;
+    f.piv = piv.as<int>();
+    f.perm = piv.as<int>() + ns;
+    auto st = partial_lu_dynamic({f}, s);
+    if (st[0] >= 0)
+      throw SolverFailure(3, i, st[0],
+                          "front " + std::to_string(i) + ": exactly singular, zero pivot column " +
+                              std::to_string(st[0]));
+    // hand the Schur complement to the parent's transient slot (ld nu)
+    if (nu)
+      HSSMF_CUDA(cudaMemcpy2DAsync(hf0[i].C, (size_t)nu * sizeof(double), f.C,
+                                   (size_t)m * sizeof(double), (size_t)nu * sizeof(double), nu,
+                                   cudaMemcpyDeviceToDevice, s));
+    f.C = hf0[i].C;
+    f.ldc = nu;
+    hf[i] = f;
+    upload_front(i);
+    fallback_mem.push_back(std::move(keep));
+    fallback_mem.push_back(std::move(piv));
+    (void)level;
+  }
+
   void Engine::factor() {
     HSSMF_CUDA(cudaSetDevice(device_));
     auto& D = *d_;
     D.profile = profile_;
     const int nn = (int)D.hf.size();
+    // previous HSS / fallback state is rebuilt
+    D.hss.clear();
+    D.hss.resize(nn);
+    D.fallback_mem.clear();
+    D.hf = D.hf0;
+    D.upload_fronts();
+    D.n_hss = D.n_fallback = D.max_rank = 0;
     cudaEvent_t e0, e1;
     HSSMF_CUDA(cudaEventCreate(&e0));
     HSSMF_CUDA(cudaEventCreate(&e1));
@@ -380,35 +577,46 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemsetAsync(D.status.p, 0xff, nn * sizeof(int), stream_));
     const FrontDev* F = D.d_fronts.as<FrontDev>();
     const int nlev = (int)D.levels.size();
+    std::vector<int> hss_fail_front, hss_fail_col;
     for (int L = nlev - 1; L >= 0; L--) {
       auto& P = D.levels[L];
-      const int* ids = D.d_ids.as<int>() + P.ids_off;
-      HSSMF_CUDA(cudaMemsetAsync(D.persist.as<char>(P.p_off), 0, P.p_bytes, stream_));
-      if (P.c_bytes)
-        HSSMF_CUDA(cudaMemsetAsync(D.trans[L % 2].as<char>(P.c_off), 0, P.c_bytes, stream_));
-      D.launch(K_ASM, 0, 0, [&] {
-        DenseKernels::assemble_sparse(F, ids, P.nf, D.d_ptr.as<int>(), D.d_ind.as<int>(),
-                                      D.d_val.as<double>(), stream_);
-      });
-      for (int slot = 0; slot < 2; slot++)
-        D.launch(K_EXTADD, 0, P.bytes_ea / 2, [&] {
-          DenseKernels::extend_add(F, ids, P.nf, slot,
-                                   D.d_colpre.as<long long>() + P.colpre_off[slot],
-                                   P.ncols[slot], stream_);
+      const int* ids = D.d_ids.as<int>() + P.dids_off;
+      if (P.p_bytes)
+        HSSMF_CUDA(cudaMemsetAsync(D.persist.as<char>(P.p_off), 0, P.p_bytes, stream_));
+      if (P.c_bytes) HSSMF_CUDA(cudaMemsetAsync(D.trans[L % 2].p, 0, P.c_bytes, stream_));
+      if (P.ndf) {
+        D.launch(K_ASM, 0, P.bytes_asm, [&] {
+          DenseKernels::assemble_sparse(F, ids, P.ndf, D.d_ptr.as<int>(), D.d_ind.as<int>(),
+                                        D.d_val.as<double>(), stream_);
         });
-      for (auto& sb : P.steps) {
-        D.launch(K_PANEL, 0, 0, [&] {
-          DenseKernels::lu_panel(F, ids, P.nf, sb.k, NB, D.status.as<int>(), stream_);
-        });
-        D.launch(K_TRSM, 0, 0, [&] {
-          DenseKernels::l21(F, ids, P.nf, sb.k, NB, P.max_nu, stream_);
-          DenseKernels::swap_trsm(F, ids, P.nf, sb.k, NB, sb.max_cols, stream_);
-        });
-        D.launch(K_GEMM_TRAIL, 0, 0,
-                 [&] { gemm_run(sb.trail, 'N', 'N', -1.0, 1.0, stream_); });
+        for (int slot = 0; slot < 2; slot++)
+          D.launch(K_EXTADD, 0, P.bytes_ea[slot], [&] {
+            DenseKernels::extend_add(F, ids, P.ndf, slot,
+                                     D.d_colpre.as<long long>() + P.colpre_off[slot],
+                                     P.ncols[slot], stream_);
+          });
+        for (auto& sb : P.steps) {
+          D.launch(K_PANEL, 0, 0, [&] {
+            DenseKernels::lu_panel(F, ids, P.ndf, sb.k, NB, D.status.as<int>(), stream_);
+          });
+          D.launch(K_TRSM, 0, 0, [&] {
+            DenseKernels::l21(F, ids, P.ndf, sb.k, NB, P.max_nu, stream_);
+            DenseKernels::swap_trsm(F, ids, P.ndf, sb.k, NB, sb.max_cols, stream_);
+          });
+          D.launch(K_GEMM_TRAIL, sb.flops, 0,
+                   [&] { gemm_run(sb.trail, 'N', 'N', -1.0, 1.0, stream_); });
+        }
+        D.launch(K_GEMM_SCHUR, P.flops_schur, 0,
+                 [&] { gemm_run(P.schur, 'N', 'N', -1.0, 1.0, stream_); });
       }
-      D.launch(K_GEMM_SCHUR, P.flops_schur, 0,
-               [&] { gemm_run(P.schur, 'N', 'N', -1.0, 1.0, stream_); });
+      for (int i : P.hss) {
+        double hfl = 0;
+        D.launch(K_HSS, 0, 0, [&] {
+          D.factor_hss_front(i, L);
+          if (D.hss[i]) hfl = D.hss[i]->flops();
+        });
+        if (profile_ && !D.evs.empty()) D.evs.back().flops = hfl;
+      }
     }
     HSSMF_CUDA(cudaEventRecord(e1, stream_));
     std::vector<int> st(nn);
@@ -427,6 +635,32 @@ namespace hssmf_b200 {
         throw SolverFailure(3, i, st[i],
                             "front " + std::to_string(i) +
                                 ": exactly singular, zero pivot column " + std::to_string(st[i]));
+    // stats (multifrontal.hpp:432-445, 496-500) and the solve lists
+    std::vector<int> sids;
+    for (int L = nlev - 1; L >= 0; L--) {
+      auto& P = D.levels[L];
+      P.sids_off = (int)sids.size();
+      for (int i : D.lv[L])
+        if (!D.hss[i]) sids.push_back(i);
+      P.nsf = (int)sids.size() - P.sids_off;
+    }
+    upload(D.d_sids, sids);
+    for (int i = 0; i < nn; i++) {
+      auto& s = stats_[i];
+      const auto& f = D.t.nodes[i];
+      if (D.hss[i]) {
+        s.type = 1;
+        s.rank = D.hss[i]->hss_rank();
+        s.flops = hss_front_flops(f.m(), s.rank, D.hss[i]->d_final());
+        D.n_hss++;
+      } else {
+        s.rank = 0;
+        s.type = D.want_hss[i] ? 2 : 0;
+        s.flops = dense_front_flops(f.ns(), f.nu());
+        if (D.want_hss[i]) D.n_fallback++;
+      }
+      D.max_rank = std::max(D.max_rank, s.rank);
+    }
     factored_ = true;
   }
 
@@ -449,6 +683,10 @@ namespace hssmf_b200 {
                                    on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                    stream_));
     }
+    int max_nu = 0;
+    for (const auto& f : D.t.nodes) max_nu = std::max(max_nu, f.nu());
+    if (D.x2buf.bytes < (size_t)max_nu * sizeof(double) + 8)
+      D.x2buf.alloc((size_t)max_nu * sizeof(double) + 8);
     cudaEvent_t e0, e1;
     HSSMF_CUDA(cudaEventCreate(&e0));
     HSSMF_CUDA(cudaEventCreate(&e1));
@@ -460,6 +698,7 @@ namespace hssmf_b200 {
     for (int L = nlev - 1; L >= 0; L--) {
       auto& P = D.levels[L];
       const int* ids = D.d_ids.as<int>() + P.ids_off;
+      const int* sids = D.d_sids.as<int>() + P.sids_off;
       if (P.b_count)
         HSSMF_CUDA(cudaMemsetAsync(D.bupd.as<double>() + P.b_off * nr, 0,
                                    P.b_count * nr * sizeof(double), stream_));
@@ -467,17 +706,42 @@ namespace hssmf_b200 {
         for (int slot = 0; slot < 2; slot++)
           DenseKernels::fold_children(F, ids, P.nf, slot, x, ldx, nrhs, P.max_child_nu[slot],
                                       stream_);
-        DenseKernels::fwd_trsv(F, ids, P.nf, x, ldx, nrhs, P.max_ns, stream_);
-        DenseKernels::fwd_gemv(F, ids, P.nf, x, ldx, nrhs, P.max_nu, stream_);
+        if (P.nsf) {
+          DenseKernels::fwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
+          DenseKernels::fwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_nu, stream_);
+        }
+        for (int i : P.hss) {
+          if (!D.hss[i]) continue;
+          const auto& h = D.hf[i];
+          for (int r = 0; r < nrhs; r++) {
+            double* xr = x + (size_t)r * ldx + h.sep_begin;
+            if (h.nu) D.hss[i]->partial_forward(xr, h.bupd + (size_t)r * h.nu);
+            else D.hss[i]->solve_full(xr);
+          }
+        }
       });
     }
     // backward sweep, root first (mf_backward, multifrontal.hpp:569-607)
     for (int L = 0; L < nlev; L++) {
       auto& P = D.levels[L];
-      const int* ids = D.d_ids.as<int>() + P.ids_off;
+      const int* sids = D.d_sids.as<int>() + P.sids_off;
       D.launch(K_SOLVE_BWD, 0, 0, [&] {
-        DenseKernels::bwd_gemv(F, ids, P.nf, x, ldx, nrhs, P.max_ns, stream_);
-        DenseKernels::bwd_trsv(F, ids, P.nf, x, ldx, nrhs, P.max_ns, stream_);
+        if (P.nsf) {
+          DenseKernels::bwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
+          DenseKernels::bwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
+        }
+        for (int i : P.hss) {
+          if (!D.hss[i]) continue;
+          const auto& h = D.hf[i];
+          if (!h.nu) continue;
+          for (int r = 0; r < nrhs; r++) {
+            double* xr = x + (size_t)r * ldx;
+            CopyDesc g{xr, 1, 0, h.upd, nullptr, 0, 0, D.x2buf.as<double>(), h.nu, nullptr,
+                       nullptr, 0, 0, h.nu, 1, 1.0, 0, 0};
+            index_copy_run({g}, stream_);
+            D.hss[i]->partial_backward(xr + h.sep_begin, D.x2buf.as<double>());
+          }
+        }
       });
     }
     HSSMF_CUDA(cudaEventRecord(e1, stream_));
@@ -497,25 +761,44 @@ namespace hssmf_b200 {
 
   long long Engine::factor_nnz() const {
     long long s = 0;
-    for (const auto& f : d_->t.nodes) s += (long long)f.ns() * f.ns() + 2LL * f.ns() * f.nu();
+    const auto& D = *d_;
+    for (size_t i = 0; i < D.t.nodes.size(); i++) {
+      const auto& f = D.t.nodes[i];
+      if (i < D.hss.size() && D.hss[i]) {
+        s += D.hss[i]->stored_scalars();
+        s += 2LL * f.nu() * D.hss[i]->hss_rank();  // Theta, Phi
+      } else {
+        s += (long long)f.ns() * f.ns() + 2LL * f.ns() * f.nu();
+      }
+    }
     return s;
   }
-  int Engine::hss_fronts() const { return 0; }
-  int Engine::fallbacks() const { return 0; }
-  int Engine::max_front_rank() const { return 0; }
-  bool Engine::front_hss(int, std::vector<int>&, std::vector<int>&, int&, int&) const {
-    return false;
+  int Engine::hss_fronts() const { return d_->n_hss; }
+  int Engine::fallbacks() const { return d_->n_fallback; }
+  int Engine::max_front_rank() const { return d_->max_rank; }
+  bool Engine::front_hss(int f, std::vector<int>& u, std::vector<int>& v, int& rounds,
+                         int& d_final) const {
+    if (f < 0 || f >= (int)d_->hss.size() || !d_->hss[f]) return false;
+    d_->hss[f]->ranks(u, v);
+    rounds = d_->hss[f]->rounds();
+    d_final = d_->hss[f]->d_final();
+    return true;
   }
   std::vector<KernelStat> Engine::kernel_stats() const {
     return std::vector<KernelStat>(d_->kstat, d_->kstat + K_NCLASS);
   }
   void Engine::reset_kernel_stats() {
-    for (auto& k : d_->kstat) { k.launches = 0; k.ms = k.flops = k.bytes = 0; }
+    for (auto& k : d_->kstat) {
+      k.launches = 0;
+      k.ms = k.flops = k.bytes = 0;
+    }
   }
   size_t Engine::device_bytes() const {
     const auto& D = *d_;
-    return D.persist.bytes + D.ipersist.bytes + D.trans[0].bytes + D.trans[1].bytes +
-           D.bupd.bytes + D.d_val.bytes + D.d_ind.bytes + D.d_ptr.bytes + D.d_gemm.bytes;
+    size_t s = D.persist.bytes + D.ipersist.bytes + D.trans[0].bytes + D.trans[1].bytes +
+               D.bupd.bytes + D.d_val.bytes + D.d_ind.bytes + D.d_ptr.bytes + D.d_gemm.bytes;
+    for (auto& m : D.fallback_mem) s += m.bytes;
+    return s;
   }
 
 }  // namespace hssmf_b200

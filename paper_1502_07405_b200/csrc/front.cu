@@ -1,7 +1,10 @@
 // Dense-front kernels, batched over all fronts of one elimination-tree level.
 #include "front.cuh"
 
+#include <algorithm>
 #include <stdexcept>
+
+#include "gemm.cuh"
 
 namespace hssmf_b200 {
 
@@ -457,6 +460,71 @@ namespace hssmf_b200 {
     set_smem_attr();
     bwd_trsv_kernel<<<dim3(nf, nrhs), TRSV_THREADS, max_ns * 8, s>>>(f, ids, x, ldx);
     HSSMF_LAUNCH_CHECK();
+  }
+
+  namespace {
+    __global__ void init_perm_kernel(const FrontDev* __restrict__ fr) {
+      const FrontDev f = fr[blockIdx.x];
+      for (int r = threadIdx.x; r < f.ns; r += blockDim.x) f.perm[r] = r;
+    }
+  }  // namespace
+
+  std::vector<int> partial_lu_dynamic(const std::vector<FrontDev>& fronts, cudaStream_t s,
+                                      double* flops) {
+    const int nf = (int)fronts.size();
+    std::vector<int> st(nf, -1);
+    if (!nf) return st;
+    int max_ns = 0, max_nu = 0;
+    for (const auto& h : fronts) {
+      max_ns = std::max(max_ns, h.ns);
+      max_nu = std::max(max_nu, h.nu);
+    }
+    std::vector<int> ids(nf);
+    for (int i = 0; i < nf; i++) ids[i] = i;
+    const size_t fb = nf * sizeof(FrontDev), ib = nf * sizeof(int);
+    char* d = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&d, fb + 2 * ib, s));
+    FrontDev* F = reinterpret_cast<FrontDev*>(d);
+    int* dids = reinterpret_cast<int*>(d + fb);
+    int* dst = reinterpret_cast<int*>(d + fb + ib);
+    HSSMF_CUDA(cudaMemcpyAsync(F, fronts.data(), fb, cudaMemcpyHostToDevice, s));
+    HSSMF_CUDA(cudaMemcpyAsync(dids, ids.data(), ib, cudaMemcpyHostToDevice, s));
+    HSSMF_CUDA(cudaMemsetAsync(dst, 0xff, ib, s));
+    init_perm_kernel<<<nf, 128, 0, s>>>(F);
+    HSSMF_LAUNCH_CHECK();
+    const int NB = 32;
+    double fl = 0;
+    for (int k = 0; k < max_ns; k += NB) {
+      int max_cols = 0;
+      std::vector<GemmProblem> probs;
+      for (const auto& h : fronts) {
+        if (h.ns <= k) continue;
+        const int nbk = std::min(NB, h.ns - k), k1 = k + nbk;
+        max_cols = std::max(max_cols, h.m - nbk);
+        if (h.ns > k1) {
+          probs.push_back({h.P + k1 + (size_t)k * h.m, h.P + k + (size_t)k1 * h.m,
+                           h.P + k1 + (size_t)k1 * h.m, h.m - k1, h.ns - k1, nbk, h.m, h.m, h.m});
+          if (h.nu)
+            probs.push_back({h.P + k1 + (size_t)k * h.m, h.U + k, h.U + k1, h.ns - k1, h.nu, nbk,
+                             h.m, h.ldu, h.ldu});
+        }
+      }
+      DenseKernels::lu_panel(F, dids, nf, k, NB, dst, s);
+      DenseKernels::l21(F, dids, nf, k, NB, max_nu, s);
+      DenseKernels::swap_trsm(F, dids, nf, k, NB, max_cols, s);
+      fl += gemm_flops(probs);
+      gemm_run_host(probs, 'N', 'N', -1.0, 1.0, s);
+    }
+    std::vector<GemmProblem> probs;
+    for (const auto& h : fronts)
+      if (h.ns && h.nu) probs.push_back({h.P + h.ns, h.U, h.C, h.nu, h.nu, h.ns, h.m, h.ldu, h.ldc});
+    fl += gemm_flops(probs);
+    gemm_run_host(probs, 'N', 'N', -1.0, 1.0, s);
+    HSSMF_CUDA(cudaMemcpyAsync(st.data(), dst, ib, cudaMemcpyDeviceToHost, s));
+    HSSMF_CUDA(cudaFreeAsync(d, s));
+    HSSMF_CUDA(cudaStreamSynchronize(s));
+    if (flops) *flops += fl;
+    return st;
   }
 
 }  // namespace hssmf_b200

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
@@ -29,6 +30,13 @@ namespace hssmf_b200 {
     const int* pos1;
     double* bupd;     // solve scratch: nu x nrhs (ld nu)
   };
+
+  // Partial LU of a host-described batch of fronts (dynamic shapes: HSS ULV
+  // nodes, top blocks, fallback fronts): perm initialised to identity, panel
+  // loop of lu_panel / l21 / swap_trsm / trailing GEMM, then the Schur GEMM.
+  // Returns per front the first singular column (-1 if none).
+  std::vector<int> partial_lu_dynamic(const std::vector<FrontDev>& fronts, cudaStream_t s,
+                                      double* flops = nullptr);
 
   struct DenseKernels {
     // assembly (a4): zero is done by the caller (memset of the level's arenas)

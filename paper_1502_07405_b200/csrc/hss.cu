@@ -1,0 +1,1141 @@
+// Device HSS: adaptive randomized compression, ULV factorization, low-rank
+// Schur update and ULV solves. See hss.hpp for the reference mapping.
+#include "hss.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "common.cuh"
+#include "cpqr.cuh"
+#include "front.cuh"
+#include "gemm.cuh"
+#include "hss_kernels.cuh"
+#include "rng.cuh"
+
+namespace hssmf_b200 {
+
+  namespace {
+
+    template<typename T> struct DBuf {
+      T* p = nullptr;
+      size_t n = 0;
+      cudaStream_t s = nullptr;
+      DBuf() = default;
+      DBuf(const DBuf&) = delete;
+      DBuf& operator=(const DBuf&) = delete;
+      DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+      DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+          free();
+          p = o.p; n = o.n; s = o.s;
+          o.p = nullptr; o.n = 0;
+        }
+        return *this;
+      }
+      void alloc(size_t cnt, cudaStream_t st) {
+        free();
+        s = st;
+        n = cnt;
+        if (cnt) HSSMF_CUDA(cudaMallocAsync((void**)&p, cnt * sizeof(T), s));
+      }
+      void zero() {
+        if (n) HSSMF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+      }
+      void free() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+      }
+      ~DBuf() { free(); }
+    };
+
+    // rows x cols matrix (ld = rows) whose column count grows by appending
+    struct Grow {
+      DBuf<double> b;
+      int rows = 0, cols = 0, cap = 0;
+      void init(int r, cudaStream_t s) {
+        rows = r;
+        cols = cap = 0;
+        b.s = s;
+      }
+      void ensure(int c) {
+        if (c <= cap) return;
+        const int nc = std::max(c, cap + cap / 2);
+        DBuf<double> nb;
+        nb.alloc((size_t)rows * nc + 1, b.s);
+        if (cols && rows)
+          HSSMF_CUDA(cudaMemcpyAsync(nb.p, b.p, (size_t)rows * cols * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, b.s));
+        b = std::move(nb);
+        cap = nc;
+      }
+      double* col(int c) const { return b.p + (size_t)c * rows; }
+      void release() {
+        b.free();
+        cols = cap = 0;
+      }
+    };
+
+    // host staging of index lists, uploaded once per phase
+    struct IdxPool {
+      std::vector<int> h;
+      DBuf<int> d;
+      size_t add(const std::vector<int>& v) {
+        const size_t o = h.size();
+        h.insert(h.end(), v.begin(), v.end());
+        return o;
+      }
+      void upload(cudaStream_t s) {
+        d.alloc(std::max<size_t>(h.size(), 1), s);
+        if (!h.empty())
+          HSSMF_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      }
+      const int* at(size_t o) const { return d.p + o; }
+    };
+
+    enum { UNCOMPRESSED = 0, PARTIAL = 1, DONE = 2 };
+
+    struct GemmGroups {
+      std::vector<GemmProblem> nn, tn, nt, tn_plus;
+      double flops = 0;
+      void run(cudaStream_t s) {
+        flops += gemm_flops(nn) + gemm_flops(tn) + gemm_flops(nt) + gemm_flops(tn_plus);
+        gemm_run_host(nn, 'N', 'N', -1.0, 1.0, s);
+        gemm_run_host(tn, 'T', 'N', -1.0, 1.0, s);
+        gemm_run_host(nt, 'N', 'T', -1.0, 1.0, s);
+        gemm_run_host(tn_plus, 'T', 'N', 1.0, 1.0, s);
+        nn.clear(); tn.clear(); nt.clear(); tn_plus.clear();
+      }
+    };
+
+    CopyDesc cd(const double* src, long long srs, long long scs, const int* sr, int sr_off,
+                const int* sc, int sc_off, double* dst, long long ldd, const int* dr, int dr_off,
+                const int* dc, int dc_off, int nr, int nc) {
+      return {src, srs, scs, sr, sc, sr_off, sc_off, dst, ldd, dr, dc, dr_off, dc_off, nr, nc,
+              1.0, 0, 0};
+    }
+
+  }  // namespace
+
+  struct HssNode {
+    int begin = 0, end = 0, c0 = -1, c1 = -1, parent = -1, depth = 0;
+    bool leaf = true;
+    int state = UNCOMPRESSED, cols_built = 0, mt = 0, r = 0;
+    std::vector<int> ir, ic, up, vp;
+    DBuf<int> d_ir, d_ic, d_up, d_vp;
+    DBuf<double> Eu, Ev;  // (mt - r) x r, ld (mt - r)
+    const double* D = nullptr;
+    long long ldD = 0;
+    DBuf<double> B12, B21;
+    Grow slr, slc, sr, sc, rr, rc;
+    DBuf<double> dr, dc;
+    // ULV
+    DBuf<double> G;
+    DBuf<int> lpiv;  // k pivots + k composed perm
+    int k = 0;
+    const double* red = nullptr;
+    long long red_ld = 0;
+    // solve scratch (offsets into the solve buffer)
+    double* ws = nullptr;
+    double* fout = nullptr;
+    double* xkeep = nullptr;
+    // densify
+    DBuf<double> Ub, Vb;
+    int size() const { return end - begin; }
+  };
+
+  struct HssImpl {
+    cudaStream_t s;
+    ClusterTree tree;
+    int m = 0;
+    const double* A = nullptr;
+    long long lda = 0;
+    HssOpts o;
+    std::vector<HssNode> nodes;
+    std::vector<std::vector<int>> levels;
+    int root = 0, maxdepth = 0;
+    DBuf<long long> seeds;
+    Grow R, Sr, Sc;
+    DBuf<double> scale, one;
+    int d = 0, rounds = 0;
+    double flops = 0;
+    // top factorization
+    bool partial = false;
+    DBuf<double> Z;
+    DBuf<int> Zpiv;
+    int zn = 0, r0 = 0, r1 = 0, nsep = 0, nu = 0;
+    DBuf<double> Ubig1, Vbig1;
+    // solve scratch
+    DBuf<double> sbuf;
+    double* bhat = nullptr;  // r0 (partial) / r0 + r1 (full)
+    double* tmp = nullptr;
+
+    explicit HssImpl(cudaStream_t st) : s(st) {}
+
+    // ---------------------------------------------------------- compression
+    void init_tree(const ClusterTree& t) {
+      tree = t;
+      const int nn = (int)t.nodes.size();
+      nodes.clear();
+      nodes.resize(nn);
+      root = nn - 1;
+      for (int i = nn - 1; i >= 0; i--) {
+        auto& N = nodes[i];
+        const auto& c = t.nodes[i];
+        N.begin = c.begin;
+        N.end = c.end;
+        N.c0 = c.child0;
+        N.c1 = c.child1;
+        N.parent = c.parent;
+        N.leaf = c.child0 < 0;
+        N.depth = c.parent >= 0 ? nodes[c.parent].depth + 1 : 0;
+        for (Grow* g : {&N.slr, &N.slc, &N.sr, &N.sc, &N.rr, &N.rc}) g->b.s = s;
+      }
+      maxdepth = 0;
+      for (auto& N : nodes) maxdepth = std::max(maxdepth, N.depth);
+      levels.assign(maxdepth + 1, {});
+      for (int i = 0; i < nn; i++) levels[nodes[i].depth].push_back(i);
+    }
+
+    void compress(const double* a, long long ld, const ClusterTree& t,
+                  const std::vector<long long>& sd, const HssOpts& opts) {
+      A = a;
+      lda = ld;
+      o = opts;
+      m = t.nodes.back().end;
+      init_tree(t);
+      seeds.alloc(std::max<size_t>(sd.size(), 1), s);
+      HSSMF_CUDA(cudaMemcpyAsync(seeds.p, sd.data(), sd.size() * sizeof(long long),
+                                 cudaMemcpyHostToDevice, s));
+      R.init(m, s);
+      Sr.init(m, s);
+      Sc.init(m, s);
+      scale.alloc(1, s);
+      scale.zero();
+      one.alloc(1, s);
+      const double h1 = 1.0;
+      HSSMF_CUDA(cudaMemcpyAsync(one.p, &h1, sizeof(double), cudaMemcpyHostToDevice, s));
+      d = std::min(o.d0, o.max_rank + o.p);
+      rounds = 0;
+      if (m == 0) {
+        nodes[root].state = DONE;
+        return;
+      }
+      while (true) {
+        rounds++;
+        const int dold = R.cols, dn = d - dold;
+        R.ensure(d);
+        Sr.ensure(d);
+        Sc.ensure(d);
+        rng_fill(seeds.p, 0, m, dold, d, R.col(dold), m, s);
+        // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
+        // hss_compress.hpp:359-363)
+        std::vector<GemmProblem> p1{{A, R.col(dold), Sr.col(dold), m, dn, m, (int)lda, m, m}};
+        gemm_run_host(p1, 'N', 'N', 1.0, 0.0, s);
+        std::vector<GemmProblem> p2{{A, R.col(dold), Sc.col(dold), m, dn, m, (int)lda, m, m}};
+        gemm_run_host(p2, 'T', 'N', 1.0, 0.0, s);
+        flops += 4.0 * m * m * dn;
+        R.cols = Sr.cols = Sc.cols = d;
+        maxabs_run(Sr.col(dold), m, m, dn, scale.p, s);
+        maxabs_run(Sc.col(dold), m, m, dn, scale.p, s);
+        double sc = 0;
+        HSSMF_CUDA(cudaMemcpyAsync(&sc, scale.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+        HSSMF_CUDA(cudaStreamSynchronize(s));
+        const int cap_id = std::min(d - o.p, o.max_rank);
+        const double abs_tol = o.eps * sc;
+        int fail = -1;
+        for (int lv = maxdepth; lv >= 0; lv--) pass_level(lv, cap_id, abs_tol, fail);
+        if (nodes[root].state == DONE) break;
+        if (d - o.p >= o.max_rank) throw HssRankError(fail, o.max_rank);
+        d += o.dd;
+      }
+    }
+
+    // index lists for the permuted gather of a stacked pair of r-row blocks
+    struct Stack2 {
+      std::vector<int> d0, s0, d1, s1;
+    };
+    static Stack2 split_perm(const std::vector<int>& perm, int n, int rtop) {
+      Stack2 st;
+      for (int i = 0; i < n; i++) {
+        if (perm[i] < rtop) { st.d0.push_back(i); st.s0.push_back(perm[i]); }
+        else { st.d1.push_back(i); st.s1.push_back(perm[i] - rtop); }
+      }
+      return st;
+    }
+
+    // V^H X (or U^H X) for X = R(I) rows / stacked child blocks, columns
+    // [c0, c0 + nc): out (r x nc, ld r) = Xp[0:r] + E^T Xp[r:mt], Xp = X(perm,:)
+    struct BasisApplyJob {
+      HssNode* N;
+      bool vside;  // V (rr) or U (rc)
+      int c0, nc;
+      double* out;
+      int ldo;
+      DBuf<double> Xp;
+    };
+
+    void run_basis_apply(std::vector<BasisApplyJob>& jobs) {
+      if (jobs.empty()) return;
+      IdxPool pool;
+      struct Pend { size_t o0, o1, o2, o3; int n0, n1; };
+      std::vector<Pend> pend(jobs.size());
+      for (size_t q = 0; q < jobs.size(); q++) {
+        auto& J = jobs[q];
+        HssNode& N = *J.N;
+        const auto& perm = J.vside ? N.vp : N.up;
+        if (N.leaf) {
+          std::vector<int> rows(N.mt);
+          for (int i = 0; i < N.mt; i++) rows[i] = N.begin + perm[i];
+          pend[q].o0 = pool.add(rows);
+          pend[q].n0 = N.mt;
+          pend[q].n1 = 0;
+        } else {
+          const int rtop = nodes[N.c0].r;
+          auto st = split_perm(perm, N.mt, rtop);
+          pend[q].o0 = pool.add(st.d0);
+          pend[q].o1 = pool.add(st.s0);
+          pend[q].o2 = pool.add(st.d1);
+          pend[q].o3 = pool.add(st.s1);
+          pend[q].n0 = (int)st.d0.size();
+          pend[q].n1 = (int)st.d1.size();
+        }
+        J.Xp.alloc((size_t)N.mt * J.nc + 1, s);
+      }
+      pool.upload(s);
+      std::vector<CopyDesc> c1, c2;
+      for (size_t q = 0; q < jobs.size(); q++) {
+        auto& J = jobs[q];
+        HssNode& N = *J.N;
+        if (N.leaf) {
+          c1.push_back(cd(R.b.p, 1, m, pool.at(pend[q].o0), 0, nullptr, J.c0, J.Xp.p, N.mt,
+                          nullptr, 0, nullptr, 0, N.mt, J.nc));
+        } else {
+          const HssNode& A0 = nodes[N.c0];
+          const HssNode& A1 = nodes[N.c1];
+          const Grow& g0 = J.vside ? A0.rr : A0.rc;
+          const Grow& g1 = J.vside ? A1.rr : A1.rc;
+          c1.push_back(cd(g0.b.p, 1, g0.rows, pool.at(pend[q].o1), 0, nullptr, J.c0, J.Xp.p, N.mt,
+                          pool.at(pend[q].o0), 0, nullptr, 0, pend[q].n0, J.nc));
+          c1.push_back(cd(g1.b.p, 1, g1.rows, pool.at(pend[q].o3), 0, nullptr, J.c0, J.Xp.p, N.mt,
+                          pool.at(pend[q].o2), 0, nullptr, 0, pend[q].n1, J.nc));
+        }
+        c2.push_back(cd(J.Xp.p, 1, N.mt, nullptr, 0, nullptr, 0, J.out, J.ldo, nullptr, 0, nullptr,
+                        0, N.r, J.nc));
+      }
+      index_copy_run(c1, s);
+      index_copy_run(c2, s);
+      GemmGroups gg;
+      for (auto& J : jobs) {
+        HssNode& N = *J.N;
+        const int k = N.mt - N.r;
+        if (k && N.r)
+          gg.tn_plus.push_back({(J.vside ? N.Ev : N.Eu).p, J.Xp.p + N.r, J.out, N.r, J.nc, k, k,
+                                N.mt, J.ldo});
+      }
+      gg.run(s);
+      flops += gg.flops;
+      for (auto& J : jobs) J.Xp.free();
+    }
+
+    void pass_level(int lv, int cap_id, double abs_tol, int& fail) {
+      std::vector<int> updl, act;
+      for (int n : levels[lv]) {
+        auto& N = nodes[n];
+        if (N.state == DONE) {
+          if (n != root) updl.push_back(n);
+          continue;
+        }
+        if (!N.leaf && (nodes[N.c0].state != DONE || nodes[N.c1].state != DONE)) continue;
+        act.push_back(n);
+      }
+      update_done(updl);
+      if (act.empty()) return;
+      // extract the dense pieces once (compress_pass, hss_compress.hpp:226-237)
+      std::vector<CopyDesc> ext;
+      for (int n : act) {
+        auto& N = nodes[n];
+        if (N.state != UNCOMPRESSED) continue;
+        if (N.leaf) {
+          N.mt = N.size();
+          N.D = A + N.begin + (size_t)N.begin * lda;
+          N.ldD = lda;
+        } else {
+          auto& a = nodes[N.c0];
+          auto& b = nodes[N.c1];
+          N.mt = a.r + b.r;
+          N.B12.alloc((size_t)a.r * b.r + 1, s);
+          N.B21.alloc((size_t)b.r * a.r + 1, s);
+          ext.push_back(cd(A, 1, lda, a.d_ir.p, 0, b.d_ic.p, 0, N.B12.p, a.r, nullptr, 0, nullptr,
+                           0, a.r, b.r));
+          ext.push_back(cd(A, 1, lda, b.d_ir.p, 0, a.d_ic.p, 0, N.B21.p, b.r, nullptr, 0, nullptr,
+                           0, b.r, a.r));
+        }
+        N.slr.init(N.mt, s);
+        N.slc.init(N.mt, s);
+        N.state = PARTIAL;
+      }
+      index_copy_run(ext, s);
+      // the root keeps no bases: its local samples would be discarded
+      // (hss_compress.hpp:239-245), so they are not formed
+      if (std::find(act.begin(), act.end(), root) != act.end()) {
+        nodes[root].state = DONE;
+        act.erase(std::find(act.begin(), act.end(), root));
+      }
+      if (act.empty()) return;
+      build_local_samples(act);
+      id_batch(act, cap_id, abs_tol, fail);
+    }
+
+    // local samples of partial nodes, new columns [cols_built, d)
+    // (build_local_samples, hss_compress.hpp:101-144)
+    void build_local_samples(const std::vector<int>& act) {
+      std::vector<CopyDesc> cp;
+      GemmGroups gg;
+      for (int n : act) {
+        auto& N = nodes[n];
+        const int cb = N.cols_built, nc = d - cb;
+        if (nc <= 0) continue;
+        N.slr.ensure(d);
+        N.slc.ensure(d);
+        const int mt = N.mt;
+        if (N.leaf) {
+          cp.push_back(copy_block(Sr.col(cb) + N.begin, m, N.slr.col(cb), mt, mt, nc));
+          cp.push_back(copy_block(Sc.col(cb) + N.begin, m, N.slc.col(cb), mt, mt, nc));
+          gg.nn.push_back({N.D, R.col(cb) + N.begin, N.slr.col(cb), mt, nc, mt, (int)N.ldD, m, mt});
+          gg.tn.push_back({N.D, R.col(cb) + N.begin, N.slc.col(cb), mt, nc, mt, (int)N.ldD, m, mt});
+        } else {
+          auto& a = nodes[N.c0];
+          auto& b = nodes[N.c1];
+          const int ra = a.r, rb = b.r;
+          cp.push_back(copy_block(a.sr.col(cb), ra, N.slr.col(cb), mt, ra, nc));
+          cp.push_back(copy_block(b.sr.col(cb), rb, N.slr.col(cb) + ra, mt, rb, nc));
+          cp.push_back(copy_block(a.sc.col(cb), ra, N.slc.col(cb), mt, ra, nc));
+          cp.push_back(copy_block(b.sc.col(cb), rb, N.slc.col(cb) + ra, mt, rb, nc));
+          if (rb) gg.nn.push_back({N.B12.p, b.rr.col(cb), N.slr.col(cb), ra, nc, rb, ra, rb, mt});
+          if (ra) gg.nn.push_back({N.B21.p, a.rr.col(cb), N.slr.col(cb) + ra, rb, nc, ra, rb, ra, mt});
+          if (rb) gg.tn.push_back({N.B21.p, b.rc.col(cb), N.slc.col(cb), ra, nc, rb, rb, rb, mt});
+          if (ra) gg.tn.push_back({N.B12.p, a.rc.col(cb), N.slc.col(cb) + ra, rb, nc, ra, ra, ra, mt});
+        }
+        N.cols_built = d;
+        N.slr.cols = N.slc.cols = d;
+      }
+      index_copy_run(cp, s);
+      gg.run(s);
+      flops += gg.flops;
+    }
+
+    // IDs of the local samples; certified nodes become Done
+    // (compress_pass, hss_compress.hpp:250-297)
+    void id_batch(const std::vector<int>& act, int cap_id, double abs_tol, int& fail) {
+      const int na = (int)act.size();
+      std::vector<DBuf<double>> Y(2 * na), X(2 * na);
+      std::vector<DBuf<int>> perm(2 * na);
+      DBuf<int> outs;
+      outs.alloc(4 * na, s);
+      std::vector<CopyDesc> tr;
+      std::vector<CpqrTask> tasks(2 * na);
+      int max_n = 0;
+      for (int q = 0; q < na; q++) {
+        auto& N = nodes[act[q]];
+        const int mt = N.mt;
+        max_n = std::max(max_n, mt);
+        for (int side = 0; side < 2; side++) {
+          const int t = 2 * q + side;
+          const Grow& src = side ? N.slc : N.slr;
+          Y[t].alloc((size_t)d * mt + 1, s);
+          X[t].alloc((size_t)std::min(d, mt) * mt + 1, s);
+          perm[t].alloc(mt + 1, s);
+          // Y = S_loc^T (d x mt)
+          tr.push_back(cd(src.b.p, mt, 1, nullptr, 0, nullptr, 0, Y[t].p, d, nullptr, 0, nullptr, 0,
+                          d, mt));
+          tasks[t] = {Y[t].p, d, mt, d, std::max(cap_id, 0), perm[t].p, X[t].p, outs.p + 2 * t};
+        }
+      }
+      index_copy_run(tr, s);
+      DBuf<CpqrTask> dt;
+      dt.alloc(tasks.size(), s);
+      HSSMF_CUDA(cudaMemcpyAsync(dt.p, tasks.data(), tasks.size() * sizeof(CpqrTask),
+                                 cudaMemcpyHostToDevice, s));
+      cpqr_run(dt.p, (int)tasks.size(), d, max_n, o.eps, abs_tol, s);
+      std::vector<int> ho(4 * na);
+      HSSMF_CUDA(cudaMemcpyAsync(ho.data(), outs.p, ho.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+      HSSMF_CUDA(cudaStreamSynchronize(s));
+      for (int q = 0; q < 2 * na; q++) {
+        const int mt = tasks[q].n, k = ho[2 * q];
+        flops += 2.0 * d * mt;
+        for (int j = 0; j < k; j++) flops += 4.0 * (d - j) * (mt - j);
+      }
+      std::vector<int> okq;
+      std::vector<CpqrTask> solve_tasks;
+      int max_rank_ok = 0, max_cols = 0;
+      for (int q = 0; q < na; q++) {
+        const int kr = ho[4 * q], cr = ho[4 * q + 1], kc = ho[4 * q + 2], cc = ho[4 * q + 3];
+        if (!cr || kr > cap_id || !cc || kc > cap_id) {
+          fail = act[q];
+          continue;
+        }
+        okq.push_back(q);
+        for (int side = 0; side < 2; side++) {
+          const int t = 2 * q + side, k = ho[2 * t];
+          if (k > 0 && tasks[t].n > k) {
+            solve_tasks.push_back(tasks[t]);
+            max_rank_ok = std::max(max_rank_ok, k);
+            max_cols = std::max(max_cols, tasks[t].n - k);
+            flops += (double)k * k * (tasks[t].n - k);
+          }
+        }
+      }
+      if (okq.empty()) return;
+      if (!solve_tasks.empty()) {
+        DBuf<CpqrTask> ds;
+        ds.alloc(solve_tasks.size(), s);
+        HSSMF_CUDA(cudaMemcpyAsync(ds.p, solve_tasks.data(), solve_tasks.size() * sizeof(CpqrTask),
+                                   cudaMemcpyHostToDevice, s));
+        id_solve_run(ds.p, (int)solve_tasks.size(), max_rank_ok, max_cols, s);
+      }
+      // perms to the host (skeleton index bookkeeping)
+      std::vector<std::vector<int>> hp(2 * okq.size());
+      for (size_t i = 0; i < okq.size(); i++)
+        for (int side = 0; side < 2; side++) {
+          const int t = 2 * okq[i] + side;
+          hp[2 * i + side].resize(tasks[t].n);
+          HSSMF_CUDA(cudaMemcpyAsync(hp[2 * i + side].data(), perm[t].p, tasks[t].n * sizeof(int),
+                                     cudaMemcpyDeviceToHost, s));
+        }
+      HSSMF_CUDA(cudaStreamSynchronize(s));
+      // bases, skeletons, reduced samples
+      std::vector<CopyDesc> ce, cg;
+      std::vector<BasisApplyJob> jobs;
+      for (size_t i = 0; i < okq.size(); i++) {
+        const int q = okq[i];
+        auto& N = nodes[act[q]];
+        const int mt = N.mt;
+        const int kr = ho[4 * q], kc = ho[4 * q + 2];
+        const int r = std::max(kr, kc);
+        N.r = r;
+        N.up = std::move(hp[2 * i]);
+        N.vp = std::move(hp[2 * i + 1]);
+        N.d_up = std::move(perm[2 * q]);
+        N.d_vp = std::move(perm[2 * q + 1]);
+        const int kk = mt - r;
+        // E = coeffs^H padded to rank r (BasisId ctor + pad_to, hss_matrix.hpp:21-58)
+        N.Eu.alloc((size_t)kk * r + 1, s);
+        N.Ev.alloc((size_t)kk * r + 1, s);
+        N.Eu.zero();
+        N.Ev.zero();
+        for (int side = 0; side < 2; side++) {
+          const int kid = side ? kc : kr, t = r - kid;
+          if (kid && kk)
+            ce.push_back(cd(X[2 * q + side].p + (size_t)t * kid, kid, 1, nullptr, 0, nullptr, 0,
+                            (side ? N.Ev : N.Eu).p, kk, nullptr, 0, nullptr, 0, kk, kid));
+        }
+        // skeleton indices
+        std::vector<int> rows_all, cols_all;
+        if (N.leaf) {
+          rows_all.resize(mt);
+          for (int j = 0; j < mt; j++) rows_all[j] = N.begin + j;
+          cols_all = rows_all;
+        } else {
+          rows_all = nodes[N.c0].ir;
+          rows_all.insert(rows_all.end(), nodes[N.c1].ir.begin(), nodes[N.c1].ir.end());
+          cols_all = nodes[N.c0].ic;
+          cols_all.insert(cols_all.end(), nodes[N.c1].ic.begin(), nodes[N.c1].ic.end());
+        }
+        N.ir.resize(r);
+        N.ic.resize(r);
+        for (int j = 0; j < r; j++) {
+          N.ir[j] = rows_all[N.up[j]];
+          N.ic[j] = cols_all[N.vp[j]];
+        }
+        N.d_ir.alloc(r + 1, s);
+        N.d_ic.alloc(r + 1, s);
+        if (r) {
+          HSSMF_CUDA(cudaMemcpyAsync(N.d_ir.p, N.ir.data(), r * sizeof(int), cudaMemcpyHostToDevice, s));
+          HSSMF_CUDA(cudaMemcpyAsync(N.d_ic.p, N.ic.data(), r * sizeof(int), cudaMemcpyHostToDevice, s));
+        }
+        // reduced samples sr = S_loc(skel rows), sc likewise
+        N.sr.init(r, s);
+        N.sc.init(r, s);
+        N.rr.init(r, s);
+        N.rc.init(r, s);
+        N.sr.ensure(d);
+        N.sc.ensure(d);
+        N.rr.ensure(d);
+        N.rc.ensure(d);
+        N.sr.cols = N.sc.cols = N.rr.cols = N.rc.cols = d;
+        cg.push_back(cd(N.slr.b.p, 1, mt, N.d_up.p, 0, nullptr, 0, N.sr.b.p, r, nullptr, 0, nullptr,
+                        0, r, d));
+        cg.push_back(cd(N.slc.b.p, 1, mt, N.d_vp.p, 0, nullptr, 0, N.sc.b.p, r, nullptr, 0, nullptr,
+                        0, r, d));
+        if (N.leaf) {
+          N.dr.alloc((size_t)r * mt + 1, s);
+          N.dc.alloc((size_t)mt * r + 1, s);
+          cg.push_back(cd(N.D, 1, N.ldD, N.d_up.p, 0, nullptr, 0, N.dr.p, r, nullptr, 0, nullptr, 0,
+                          r, mt));
+          cg.push_back(cd(N.D, 1, N.ldD, nullptr, 0, N.d_vp.p, 0, N.dc.p, mt, nullptr, 0, nullptr,
+                          0, mt, r));
+        }
+        jobs.push_back({&N, true, 0, d, N.rr.b.p, r, {}});
+        jobs.push_back({&N, false, 0, d, N.rc.b.p, r, {}});
+      }
+      index_copy_run(ce, s);
+      index_copy_run(cg, s);
+      run_basis_apply(jobs);
+      for (int q : okq) {
+        auto& N = nodes[act[q]];
+        N.slr.release();
+        N.slc.release();
+        N.state = DONE;
+      }
+    }
+
+    // Done nodes fold in only the new columns (update_done, hss_compress.hpp:148-206)
+    void update_done(const std::vector<int>& lst) {
+      std::vector<int> todo;
+      for (int n : lst)
+        if (d - nodes[n].cols_built > 0) todo.push_back(n);
+      if (todo.empty()) return;
+      std::vector<CopyDesc> c1, c3;
+      GemmGroups gg;
+      std::vector<DBuf<double>> tr(todo.size()), tc(todo.size());
+      std::vector<BasisApplyJob> jobs;
+      for (size_t q = 0; q < todo.size(); q++) {
+        auto& N = nodes[todo[q]];
+        const int cb = N.cols_built, nc = d - cb, r = N.r, mt = N.mt;
+        for (Grow* g : {&N.sr, &N.sc, &N.rr, &N.rc}) {
+          g->ensure(d);
+          g->cols = d;
+        }
+        if (N.leaf) {
+          c1.push_back(cd(Sr.b.p, 1, m, N.d_ir.p, 0, nullptr, cb, N.sr.col(cb), r, nullptr, 0,
+                          nullptr, 0, r, nc));
+          c1.push_back(cd(Sc.b.p, 1, m, N.d_ic.p, 0, nullptr, cb, N.sc.col(cb), r, nullptr, 0,
+                          nullptr, 0, r, nc));
+          gg.nn.push_back({N.dr.p, R.col(cb) + N.begin, N.sr.col(cb), r, nc, mt, r, m, r});
+          gg.tn.push_back({N.dc.p, R.col(cb) + N.begin, N.sc.col(cb), r, nc, mt, mt, m, r});
+        } else {
+          auto& a = nodes[N.c0];
+          auto& b = nodes[N.c1];
+          const int ra = a.r, rb = b.r;
+          tr[q].alloc((size_t)mt * nc + 1, s);
+          tc[q].alloc((size_t)mt * nc + 1, s);
+          c1.push_back(copy_block(a.sr.col(cb), ra, tr[q].p, mt, ra, nc));
+          c1.push_back(copy_block(b.sr.col(cb), rb, tr[q].p + ra, mt, rb, nc));
+          c1.push_back(copy_block(a.sc.col(cb), ra, tc[q].p, mt, ra, nc));
+          c1.push_back(copy_block(b.sc.col(cb), rb, tc[q].p + ra, mt, rb, nc));
+          if (rb) gg.nn.push_back({N.B12.p, b.rr.col(cb), tr[q].p, ra, nc, rb, ra, rb, mt});
+          if (ra) gg.nn.push_back({N.B21.p, a.rr.col(cb), tr[q].p + ra, rb, nc, ra, rb, ra, mt});
+          if (rb) gg.tn.push_back({N.B21.p, b.rc.col(cb), tc[q].p, ra, nc, rb, rb, rb, mt});
+          if (ra) gg.tn.push_back({N.B12.p, a.rc.col(cb), tc[q].p + ra, rb, nc, ra, ra, ra, mt});
+          c3.push_back(cd(tr[q].p, 1, mt, N.d_up.p, 0, nullptr, 0, N.sr.col(cb), r, nullptr, 0,
+                          nullptr, 0, r, nc));
+          c3.push_back(cd(tc[q].p, 1, mt, N.d_vp.p, 0, nullptr, 0, N.sc.col(cb), r, nullptr, 0,
+                          nullptr, 0, r, nc));
+        }
+        jobs.push_back({&N, true, cb, nc, N.rr.col(cb), r, {}});
+        jobs.push_back({&N, false, cb, nc, N.rc.col(cb), r, {}});
+      }
+      index_copy_run(c1, s);
+      gg.run(s);
+      flops += gg.flops;
+      index_copy_run(c3, s);
+      run_basis_apply(jobs);
+      for (int n : todo) nodes[n].cols_built = d;
+    }
+
+    // ------------------------------------------------------------------ ULV
+    // transformed node block G = Omega X Psi, then partial LU of its leading
+    // k x k block (ulv_eliminate, hss_ulv.hpp:76-121), batched per level
+    void eliminate(const std::vector<int>& set) {
+      std::vector<std::vector<int>> byd(maxdepth + 1);
+      for (int n : set) byd[nodes[n].depth].push_back(n);
+      for (int lv = maxdepth; lv >= 0; lv--) {
+        auto& L = byd[lv];
+        if (L.empty()) continue;
+        IdxPool pool;
+        struct Pend { size_t rl, cl; size_t bl[4][4]; int bn[4][2]; };
+        std::vector<Pend> pend(L.size());
+        for (size_t q = 0; q < L.size(); q++) {
+          auto& N = nodes[L[q]];
+          const int mt = N.mt, r = N.r;
+          N.k = mt - r;
+          std::vector<int> urow(mt), vcol(mt);
+          for (int i = 0; i < mt; i++) {
+            urow[i] = i < N.k ? N.up[r + i] : N.up[i - N.k];
+            vcol[i] = i < N.k ? N.vp[r + i] : N.vp[i - N.k];
+          }
+          if (N.leaf) {
+            pend[q].rl = pool.add(urow);
+            pend[q].cl = pool.add(vcol);
+          } else {
+            const int ra = nodes[N.c0].r;
+            for (int a = 0; a < 2; a++)
+              for (int b = 0; b < 2; b++) {
+                std::vector<int> dr, sr, dcv, scv;
+                for (int i = 0; i < mt; i++)
+                  if ((urow[i] >= ra) == (a == 1)) { dr.push_back(i); sr.push_back(urow[i] - a * ra); }
+                for (int j = 0; j < mt; j++)
+                  if ((vcol[j] >= ra) == (b == 1)) { dcv.push_back(j); scv.push_back(vcol[j] - b * ra); }
+                const int bi = 2 * a + b;
+                pend[q].bl[bi][0] = pool.add(dr);
+                pend[q].bl[bi][1] = pool.add(sr);
+                pend[q].bl[bi][2] = pool.add(dcv);
+                pend[q].bl[bi][3] = pool.add(scv);
+                pend[q].bn[bi][0] = (int)dr.size();
+                pend[q].bn[bi][1] = (int)dcv.size();
+              }
+          }
+          N.G.alloc((size_t)mt * mt + 1, s);
+        }
+        pool.upload(s);
+        std::vector<CopyDesc> cps;
+        for (size_t q = 0; q < L.size(); q++) {
+          auto& N = nodes[L[q]];
+          const int mt = N.mt;
+          if (N.leaf) {
+            cps.push_back(cd(N.D, 1, N.ldD, pool.at(pend[q].rl), 0, pool.at(pend[q].cl), 0, N.G.p,
+                             mt, nullptr, 0, nullptr, 0, mt, mt));
+          } else {
+            const auto& a = nodes[N.c0];
+            const auto& b = nodes[N.c1];
+            const double* src[4] = {a.red, N.B12.p, N.B21.p, b.red};
+            const long long lds[4] = {a.red_ld, a.r, b.r, b.red_ld};
+            for (int bi = 0; bi < 4; bi++)
+              cps.push_back(cd(src[bi], 1, lds[bi], pool.at(pend[q].bl[bi][1]), 0,
+                               pool.at(pend[q].bl[bi][3]), 0, N.G.p, mt, pool.at(pend[q].bl[bi][0]),
+                               0, pool.at(pend[q].bl[bi][2]), 0, pend[q].bn[bi][0],
+                               pend[q].bn[bi][1]));
+          }
+        }
+        index_copy_run(cps, s);
+        GemmGroups rows, cols;
+        for (int n : L) {
+          auto& N = nodes[n];
+          const int mt = N.mt, r = N.r, k = N.k;
+          if (!k || !r) continue;
+          rows.nn.push_back({N.Eu.p, N.G.p + k, N.G.p, k, mt, r, k, mt, mt});
+          cols.nt.push_back({N.G.p + (size_t)k * mt, N.Ev.p, N.G.p, mt, k, r, mt, k, mt});
+        }
+        rows.run(s);
+        cols.run(s);
+        flops += rows.flops + cols.flops;
+        std::vector<FrontDev> fr;
+        std::vector<int> fid;
+        for (int n : L) {
+          auto& N = nodes[n];
+          const int mt = N.mt, k = N.k;
+          if (!k) {
+            N.red = N.G.p;
+            N.red_ld = mt;
+            continue;
+          }
+          N.lpiv.alloc(2 * k, s);
+          FrontDev f{};
+          f.ns = k;
+          f.nu = N.r;
+          f.m = mt;
+          f.ldu = mt;
+          f.ldc = mt;
+          f.child0 = f.child1 = -1;
+          f.P = N.G.p;
+          f.U = N.G.p + (size_t)k * mt;
+          f.C = N.G.p + k + (size_t)k * mt;
+          f.piv = N.lpiv.p;
+          f.perm = N.lpiv.p + k;
+          fr.push_back(f);
+          fid.push_back(n);
+          N.red = f.C;
+          N.red_ld = mt;
+        }
+        auto st = partial_lu_dynamic(fr, s, &flops);
+        for (size_t q = 0; q < st.size(); q++)
+          if (st[q] >= 0) throw HssSingular(fid[q], st[q]);
+      }
+    }
+
+    void subtree(int n, std::vector<int>& out) const {
+      out.push_back(n);
+      if (!nodes[n].leaf) {
+        subtree(nodes[n].c0, out);
+        subtree(nodes[n].c1, out);
+      }
+    }
+
+    // dense LU of Z (zn x zn) with ns leading columns eliminated
+    void factor_top(int ns, int nus, int blame) {
+      Zpiv.alloc(2 * ns + 1, s);
+      FrontDev f{};
+      f.ns = ns;
+      f.nu = nus;
+      f.m = zn;
+      f.ldu = zn;
+      f.ldc = zn;
+      f.child0 = f.child1 = -1;
+      f.P = Z.p;
+      f.U = Z.p + (size_t)ns * zn;
+      f.C = Z.p + ns + (size_t)ns * zn;
+      f.piv = Zpiv.p;
+      f.perm = Zpiv.p + ns;
+      auto st = partial_lu_dynamic({f}, s, &flops);
+      if (st[0] >= 0) throw HssSingular(blame, st[0]);
+    }
+
+    // X = [g0 B12; B21 g1] (g1 optional) into Z
+    void assemble_top(bool with_g1) {
+      const auto& R0 = nodes[nodes[root].c0];
+      const auto& R1 = nodes[nodes[root].c1];
+      r0 = R0.r;
+      r1 = R1.r;
+      zn = r0 + r1;
+      Z.alloc((size_t)zn * zn + 1, s);
+      Z.zero();
+      const auto& N = nodes[root];
+      std::vector<CopyDesc> c;
+      c.push_back(copy_block(R0.red, R0.red_ld, Z.p, zn, r0, r0));
+      c.push_back(copy_block(N.B12.p, r0, Z.p + (size_t)r0 * zn, zn, r0, r1));
+      c.push_back(copy_block(N.B21.p, r1, Z.p + r0, zn, r1, r0));
+      if (with_g1) c.push_back(copy_block(R1.red, R1.red_ld, Z.p + r0 + (size_t)r0 * zn, zn, r1, r1));
+      index_copy_run(c, s);
+    }
+
+    void ulv_full() {
+      partial = false;
+      auto& Rt = nodes[root];
+      if (Rt.leaf) {
+        zn = m;
+        Z.alloc((size_t)m * m + 1, s);
+        index_copy_run({copy_block(A, lda, Z.p, m, m, m)}, s);
+        factor_top(m, 0, root);
+        return;
+      }
+      std::vector<int> set;
+      subtree(Rt.c0, set);
+      subtree(Rt.c1, set);
+      eliminate(set);
+      assemble_top(true);
+      factor_top(zn, 0, root);
+    }
+
+    // dense nested bases Ubig/Vbig of a subtree, bottom-up
+    void big_bases(const std::vector<int>& set) {
+      std::vector<std::vector<int>> byd(maxdepth + 1);
+      for (int n : set) byd[nodes[n].depth].push_back(n);
+      for (int lv = maxdepth; lv >= 0; lv--) {
+        if (byd[lv].empty()) continue;
+        std::vector<CopyDesc> c;
+        std::vector<DBuf<double>> dU(byd[lv].size()), dV(byd[lv].size());
+        for (size_t q = 0; q < byd[lv].size(); q++) {
+          auto& N = nodes[byd[lv][q]];
+          const int mt = N.mt, r = N.r, k = mt - r;
+          // dense U = Pi [I; E] (BasisId::dense, hss_matrix.hpp:61-67)
+          DBuf<double>& u = N.leaf ? N.Ub : dU[q];
+          DBuf<double>& v = N.leaf ? N.Vb : dV[q];
+          u.alloc((size_t)mt * r + 1, s);
+          v.alloc((size_t)mt * r + 1, s);
+          u.zero();
+          v.zero();
+          CopyDesc e1 = cd(one.p, 0, 0, nullptr, 0, nullptr, 0, u.p, mt, N.d_up.p, 0, nullptr, 0, r, r);
+          e1.diag = 1;
+          CopyDesc e2 = e1;
+          e2.dst = v.p;
+          e2.dr = N.d_vp.p;
+          c.push_back(e1);
+          c.push_back(e2);
+          if (k && r) {
+            c.push_back(cd(N.Eu.p, 1, k, nullptr, 0, nullptr, 0, u.p, mt, N.d_up.p + r, 0, nullptr, 0, k, r));
+            c.push_back(cd(N.Ev.p, 1, k, nullptr, 0, nullptr, 0, v.p, mt, N.d_vp.p + r, 0, nullptr, 0, k, r));
+          }
+        }
+        index_copy_run(c, s);
+        std::vector<GemmProblem> pp;
+        for (size_t q = 0; q < byd[lv].size(); q++) {
+          auto& N = nodes[byd[lv][q]];
+          if (N.leaf) continue;
+          auto& a = nodes[N.c0];
+          auto& b = nodes[N.c1];
+          const int ma = a.size(), mb = b.size(), r = N.r;
+          N.Ub.alloc((size_t)N.size() * r + 1, s);
+          N.Vb.alloc((size_t)N.size() * r + 1, s);
+          if (!r) continue;
+          pp.push_back({a.Ub.p, dU[q].p, N.Ub.p, ma, r, a.r, ma, N.mt, N.size()});
+          pp.push_back({b.Ub.p, dU[q].p + a.r, N.Ub.p + ma, mb, r, b.r, mb, N.mt, N.size()});
+          pp.push_back({a.Vb.p, dV[q].p, N.Vb.p, ma, r, a.r, ma, N.mt, N.size()});
+          pp.push_back({b.Vb.p, dV[q].p + a.r, N.Vb.p + ma, mb, r, b.r, mb, N.mt, N.size()});
+        }
+        flops += gemm_flops(pp);
+        gemm_run_host(pp, 'N', 'N', 1.0, 0.0, s);
+      }
+    }
+
+    void ulv_partial(double* upd, long long ldu) {
+      partial = true;
+      auto& Rt = nodes[root];
+      const int c0 = Rt.c0, c1 = Rt.c1;
+      nsep = nodes[c0].end;
+      nu = m - nsep;
+      std::vector<int> set0;
+      subtree(c0, set0);
+      eliminate(set0);
+      // Z = [g0 B12; B21 0]: partial LU of the r0 leading columns gives
+      // top_lu = LU(g0), L21 = B21 U^-1, U12 = L^-1 P B12 and C = -B21 g0^-1 B12
+      assemble_top(false);
+      factor_top(r0, r1, c0);
+      // densified update  F22|hss - Theta^* Phi = F22|hss + Ubig1 C Vbig1^*
+      std::vector<int> set1;
+      subtree(c1, set1);
+      big_bases(set1);
+      std::vector<CopyDesc> cp;
+      std::vector<std::pair<int, int>> blocks;
+      for (int n : set1) {
+        const auto& N = nodes[n];
+        if (N.leaf)
+          cp.push_back(copy_block(N.D, N.ldD, upd + (N.begin - nsep) + (size_t)(N.begin - nsep) * ldu,
+                                  ldu, N.size(), N.size()));
+      }
+      index_copy_run(cp, s);
+      std::vector<DBuf<double>> T;
+      std::vector<GemmProblem> p1, p2;
+      for (int n : set1) {
+        const auto& N = nodes[n];
+        if (N.leaf) continue;
+        const auto& a = nodes[N.c0];
+        const auto& b = nodes[N.c1];
+        const int ma = a.size(), mb = b.size();
+        DBuf<double> t1, t2;
+        t1.alloc((size_t)ma * b.r + 1, s);
+        t2.alloc((size_t)mb * a.r + 1, s);
+        if (a.r && b.r) {
+          p1.push_back({a.Ub.p, N.B12.p, t1.p, ma, b.r, a.r, ma, a.r, ma});
+          p1.push_back({b.Ub.p, N.B21.p, t2.p, mb, a.r, b.r, mb, b.r, mb});
+        }
+        double* o_ab = upd + (a.begin - nsep) + (size_t)(b.begin - nsep) * ldu;
+        double* o_ba = upd + (b.begin - nsep) + (size_t)(a.begin - nsep) * ldu;
+        p2.push_back({t1.p, b.Vb.p, o_ab, ma, mb, b.r, ma, mb, (int)ldu});
+        p2.push_back({t2.p, a.Vb.p, o_ba, mb, ma, a.r, mb, ma, (int)ldu});
+        T.push_back(std::move(t1));
+        T.push_back(std::move(t2));
+      }
+      flops += gemm_flops(p1) + gemm_flops(p2);
+      gemm_run_host(p1, 'N', 'N', 1.0, 0.0, s);
+      gemm_run_host(p2, 'N', 'T', 1.0, 0.0, s);
+      auto& N1 = nodes[c1];
+      if (r1) {
+        DBuf<double> t;
+        t.alloc((size_t)nu * r1 + 1, s);
+        std::vector<GemmProblem> q1{{N1.Ub.p, Z.p + r0 + (size_t)r0 * zn, t.p, nu, r1, r1, nu, zn, nu}};
+        gemm_run_host(q1, 'N', 'N', 1.0, 0.0, s);
+        std::vector<GemmProblem> q2{{t.p, N1.Vb.p, upd, nu, nu, r1, nu, nu, (int)ldu}};
+        gemm_run_host(q2, 'N', 'T', 1.0, 1.0, s);
+        flops += gemm_flops(q1) + gemm_flops(q2);
+      }
+      Ubig1 = std::move(N1.Ub);
+      Vbig1 = std::move(N1.Vb);
+      for (int n : set1) {
+        nodes[n].Ub.free();
+        nodes[n].Vb.free();
+      }
+    }
+
+    // -------------------------------------------------------------- solves
+    void alloc_solve_scratch() {
+      if (sbuf.p) return;
+      size_t tot = 2 * (size_t)m + 64;
+      for (auto& N : nodes) tot += (size_t)N.k + 2 * N.r + 8;
+      sbuf.alloc(tot, s);
+      double* p = sbuf.p;
+      for (auto& N : nodes) {
+        N.ws = p; p += N.k + 2;
+        N.fout = p; p += N.r + 2;
+        N.xkeep = p; p += N.r + 2;
+      }
+      bhat = p; p += m + 8;
+      tmp = p;
+    }
+
+    void forward_set(const std::vector<int>& set, const double* b) {
+      std::vector<std::vector<int>> byd(maxdepth + 1);
+      for (int n : set) byd[nodes[n].depth].push_back(n);
+      for (int lv = maxdepth; lv >= 0; lv--) {
+        if (byd[lv].empty()) continue;
+        std::vector<UlvSolveNode> v;
+        for (int n : byd[lv]) {
+          auto& N = nodes[n];
+          UlvSolveNode u{};
+          u.uperm = N.d_up.p;
+          u.vperm = N.d_vp.p;
+          u.Eu = N.Eu.p;
+          u.Ev = N.Ev.p;
+          u.G = N.G.p;
+          u.lperm = N.k ? N.lpiv.p + N.k : nullptr;
+          u.m = N.mt;
+          u.r = N.r;
+          u.k = N.k;
+          if (N.leaf) {
+            u.in0 = b + N.begin;
+            u.n0 = N.mt;
+            u.in1 = nullptr;
+          } else {
+            u.in0 = nodes[N.c0].fout;
+            u.n0 = nodes[N.c0].r;
+            u.in1 = nodes[N.c1].fout;
+          }
+          u.ws = N.ws;
+          u.fout = N.fout;
+          v.push_back(u);
+        }
+        ulv_fwd_level(v, 0, s);
+      }
+    }
+
+    void backward_set(const std::vector<int>& set, double* x) {
+      std::vector<std::vector<int>> byd(maxdepth + 1);
+      for (int n : set) byd[nodes[n].depth].push_back(n);
+      for (int lv = 0; lv <= maxdepth; lv++) {
+        if (byd[lv].empty()) continue;
+        std::vector<UlvSolveNode> v;
+        for (int n : byd[lv]) {
+          auto& N = nodes[n];
+          UlvSolveNode u{};
+          u.uperm = N.d_up.p;
+          u.vperm = N.d_vp.p;
+          u.Eu = N.Eu.p;
+          u.Ev = N.Ev.p;
+          u.G = N.G.p;
+          u.m = N.mt;
+          u.r = N.r;
+          u.k = N.k;
+          u.ws = N.ws;
+          u.xkeep = N.xkeep;
+          if (N.leaf) {
+            u.out0 = x + N.begin;
+            u.n0 = N.mt;
+            u.out1 = nullptr;
+          } else {
+            u.out0 = nodes[N.c0].xkeep;
+            u.n0 = nodes[N.c0].r;
+            u.out1 = nodes[N.c1].xkeep;
+          }
+          v.push_back(u);
+        }
+        ulv_bwd_level(v, s);
+      }
+    }
+
+    void solve_full(double* x) {
+      alloc_solve_scratch();
+      auto& Rt = nodes[root];
+      if (Rt.leaf) {
+        lu_solve_vec(Z.p, zn, Zpiv.p + zn, zn, x, s);
+        return;
+      }
+      std::vector<int> set;
+      subtree(Rt.c0, set);
+      subtree(Rt.c1, set);
+      forward_set(set, x);
+      auto& a = nodes[Rt.c0];
+      auto& b = nodes[Rt.c1];
+      HSSMF_CUDA(cudaMemcpyAsync(bhat, a.fout, r0 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      HSSMF_CUDA(cudaMemcpyAsync(bhat + r0, b.fout, r1 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      lu_solve_vec(Z.p, zn, Zpiv.p + zn, zn, bhat, s);
+      HSSMF_CUDA(cudaMemcpyAsync(a.xkeep, bhat, r0 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      HSSMF_CUDA(cudaMemcpyAsync(b.xkeep, bhat + r0, r1 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      backward_set(set, x);
+    }
+
+    // mf_forward HSS branch (multifrontal.hpp:553-566)
+    void partial_forward(const double* b1, double* bupd) {
+      alloc_solve_scratch();
+      auto& Rt = nodes[root];
+      std::vector<int> set0;
+      subtree(Rt.c0, set0);
+      forward_set(set0, b1);
+      auto& a = nodes[Rt.c0];
+      // bhat kept for the backward sweep; tt = top_lu^-1 bhat
+      HSSMF_CUDA(cudaMemcpyAsync(bhat, a.fout, r0 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      double* tt = tmp;
+      double* w = tmp + r0 + 1;
+      HSSMF_CUDA(cudaMemcpyAsync(tt, bhat, r0 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      lu_solve_vec(Z.p, zn, Zpiv.p + r0, r0, tt, s);
+      gemv_run('N', r1, r0, 1.0, nodes[root].B21.p, r1, tt, 0.0, w, s);
+      gemv_run('N', nu, r1, -1.0, Ubig1.p, nu, w, 1.0, bupd, s);
+    }
+
+    // mf_backward HSS branch (multifrontal.hpp:586-598)
+    void partial_backward(double* x1, const double* x2) {
+      auto& Rt = nodes[root];
+      auto& a = nodes[Rt.c0];
+      double* w2 = tmp;
+      double* bk = a.xkeep;
+      gemv_run('T', nu, r1, 1.0, Vbig1.p, nu, x2, 0.0, w2, s);
+      HSSMF_CUDA(cudaMemcpyAsync(bk, bhat, r0 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      gemv_run('N', r0, r1, -1.0, nodes[root].B12.p, r0, w2, 1.0, bk, s);
+      lu_solve_vec(Z.p, zn, Zpiv.p + r0, r0, bk, s);
+      std::vector<int> set0;
+      subtree(Rt.c0, set0);
+      backward_set(set0, x1);
+    }
+  };
+
+  HssMatrixDev::HssMatrixDev(cudaStream_t s) : d_(new HssImpl(s)) {}
+  HssMatrixDev::~HssMatrixDev() = default;
+
+  void HssMatrixDev::compress(const double* A, long long lda, const ClusterTree& tree,
+                              const std::vector<long long>& seeds, const HssOpts& o) {
+    d_->compress(A, lda, tree, seeds, o);
+  }
+  void HssMatrixDev::ulv_full() { d_->ulv_full(); }
+  void HssMatrixDev::ulv_partial(double* update, long long ldu) { d_->ulv_partial(update, ldu); }
+  void HssMatrixDev::drop_dense() {
+    d_->A = nullptr;
+    for (auto& N : d_->nodes) {
+      N.D = nullptr;
+      N.dr.free();
+      N.dc.free();
+      N.sr.release();
+      N.sc.release();
+      N.rr.release();
+      N.rc.release();
+      N.slr.release();
+      N.slc.release();
+    }
+    d_->R.release();
+    d_->Sr.release();
+    d_->Sc.release();
+  }
+  void HssMatrixDev::solve_full(double* x) { d_->solve_full(x); }
+  void HssMatrixDev::partial_forward(const double* b1, double* bupd) { d_->partial_forward(b1, bupd); }
+  void HssMatrixDev::partial_backward(double* x1, const double* x2) { d_->partial_backward(x1, x2); }
+  int HssMatrixDev::rows() const { return d_->m; }
+  int HssMatrixDev::rounds() const { return d_->rounds; }
+  int HssMatrixDev::d_final() const { return d_->d; }
+  int HssMatrixDev::hss_rank() const {
+    int r = 0;
+    for (int i = 0; i < (int)d_->nodes.size(); i++)
+      if (i != d_->root) r = std::max(r, d_->nodes[i].r);
+    return r;
+  }
+  void HssMatrixDev::ranks(std::vector<int>& u, std::vector<int>& v) const {
+    u.clear();
+    v.clear();
+    for (int i = 0; i < (int)d_->nodes.size(); i++) {
+      const int r = i == d_->root ? 0 : d_->nodes[i].r;
+      u.push_back(r);
+      v.push_back(r);
+    }
+  }
+  long long HssMatrixDev::stored_scalars() const {
+    long long s = 0;
+    for (const auto& N : d_->nodes) {
+      if (N.leaf) s += (long long)N.size() * N.size();
+      s += (long long)N.B12.n + N.B21.n - (N.B12.n ? 2 : 0);
+      s += 2LL * (N.mt - N.r) * N.r;
+      s += (long long)N.mt * N.mt;  // ULV node factors
+    }
+    s += (long long)d_->zn * d_->zn;
+    return s;
+  }
+  double HssMatrixDev::flops() const { return d_->flops; }
+
+}  // namespace hssmf_b200

@@ -1,0 +1,91 @@
+// HSS compression (adaptive randomized, Algorithm 1 of the paper), ULV-like
+// factorization, low-rank Schur update and ULV solves on the device.
+//
+// Reference counterparts:
+//   hss_compress_adaptive / compress_pass / build_local_samples / update_done
+//                                               hss_compress.hpp:101-352
+//   BasisId (Pi [I; E] interpolative bases)     hss_matrix.hpp:18-172
+//   ulv_eliminate / ulv_factor / partial_ulv_and_schur / LowRankSchur
+//                                               hss_ulv.hpp:18-121, 284-358
+//   UlvFactors::fwd/bwd/solve/partial_*         hss_ulv.hpp:150-276
+//
+// The compressed matrix is a dense device matrix A (a multifrontal front,
+// assembled in HBM, or the standalone config-2 matrix): sampling products
+// are two DMMA GEMMs per round and element extraction is an indexed gather.
+// Every HSS level of a round is one batch of launches; ranks are read back
+// once per level to size the next batch.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host/analysis.hpp"
+
+namespace hssmf_b200 {
+
+  struct HssOpts {
+    double eps = 1e-8;
+    int d0 = 128, dd = 128, p = 10, max_rank = 5000;
+  };
+
+  struct HssRankError : std::runtime_error {
+    int node, cap;
+    HssRankError(int n, int c)
+        : std::runtime_error("hss compression: rank cap " + std::to_string(c) +
+                             " exceeded at cluster " + std::to_string(n)),
+          node(n), cap(c) {}
+  };
+
+  struct HssSingular : std::runtime_error {
+    int node, column;
+    HssSingular(int n, int c)
+        : std::runtime_error("ulv_factor cluster " + std::to_string(n) +
+                             ": exactly singular, zero pivot column " + std::to_string(c)),
+          node(n), column(c) {}
+  };
+
+  struct HssImpl;
+
+  class HssMatrixDev {
+  public:
+    HssMatrixDev(cudaStream_t s);
+    ~HssMatrixDev();
+    HssMatrixDev(const HssMatrixDev&) = delete;
+
+    // compress the dense device matrix A (m x m, lda) over the cluster tree;
+    // seeds[i] names the random stream of row i (host array)
+    void compress(const double* A, long long lda, const ClusterTree& tree,
+                  const std::vector<long long>& seeds, const HssOpts& o);
+    // full ULV factorization (ulv_factor)
+    void ulv_full();
+    // partial ULV of the leading n_sep rows (root child0) + low-rank Schur;
+    // writes the densified update  F22|hss - Theta^* Phi  (nu x nu, ld ldu)
+    void ulv_partial(double* update, long long ldu);
+    // release the reference to A (front storage about to be freed)
+    void drop_dense();
+
+    // solves (single right-hand side, device vectors)
+    void solve_full(double* x);  // in place, length m
+    // partial: forward on b1 (ns) -> subtract the coupling from bupd (nu);
+    // backward from x2 = x(upd) (nu) -> x1 (ns) written in place of b1
+    void partial_forward(const double* b1, double* bupd);
+    void partial_backward(double* x1, const double* x2);
+
+    int rows() const;
+    int rounds() const;
+    int d_final() const;
+    int hss_rank() const;
+    void ranks(std::vector<int>& u, std::vector<int>& v) const;
+    long long stored_scalars() const;
+    double flops() const;
+
+  private:
+    std::unique_ptr<HssImpl> d_;
+  };
+
+}  // namespace hssmf_b200

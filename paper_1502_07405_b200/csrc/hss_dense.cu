@@ -1,0 +1,94 @@
+// Standalone dense HSS (BASELINE config 2): hss_compress + ulv_factor +
+// UlvFactors::solve (hss_compress.hpp:373-383, hss_ulv.hpp:150-176, 284-319).
+#include "hss_dense.hpp"
+
+#include "common.cuh"
+#include "hss.hpp"
+
+namespace hssmf_b200 {
+
+  struct DenseHss::Impl {
+    int device = 0, n = 0;
+    cudaStream_t s = nullptr;
+    double* A = nullptr;
+    double* x = nullptr;
+    std::unique_ptr<HssMatrixDev> h;
+    double cms = 0, ums = 0;
+    ~Impl() {
+      h.reset();
+      if (s) cudaStreamSynchronize(s);
+      if (A) cudaFree(A);
+      if (x) cudaFree(x);
+      if (s) cudaStreamDestroy(s);
+    }
+  };
+
+  DenseHss::DenseHss(int device) : d_(new Impl) {
+    d_->device = device;
+    HSSMF_CUDA(cudaSetDevice(device));
+    HSSMF_CUDA(cudaStreamCreateWithFlags(&d_->s, cudaStreamNonBlocking));
+  }
+  DenseHss::~DenseHss() = default;
+
+  void DenseHss::run(const double* a, int lda, int n, int leaf, double eps, int d0, int dd, int p,
+                     int max_rank, bool on_device) {
+    auto& D = *d_;
+    HSSMF_CUDA(cudaSetDevice(D.device));
+    D.n = n;
+    HSSMF_CUDA(cudaMalloc(&D.A, (size_t)n * n * sizeof(double) + 8));
+    HSSMF_CUDA(cudaMalloc(&D.x, (size_t)n * sizeof(double) + 8));
+    HSSMF_CUDA(cudaMemcpy2DAsync(D.A, n * sizeof(double), a, (size_t)lda * sizeof(double),
+                                 n * sizeof(double), n,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, D.s));
+    std::vector<long long> seeds(n);
+    for (int i = 0; i < n; i++) seeds[i] = i;
+    HssOpts o;
+    o.eps = eps;
+    o.d0 = d0;
+    o.dd = dd;
+    o.p = p;
+    o.max_rank = max_rank;
+    cudaEvent_t e0, e1, e2;
+    HSSMF_CUDA(cudaEventCreate(&e0));
+    HSSMF_CUDA(cudaEventCreate(&e1));
+    HSSMF_CUDA(cudaEventCreate(&e2));
+    D.h = std::make_unique<HssMatrixDev>(D.s);
+    HSSMF_CUDA(cudaEventRecord(e0, D.s));
+    D.h->compress(D.A, n, ClusterTree::balanced(n, leaf), seeds, o);
+    HSSMF_CUDA(cudaEventRecord(e1, D.s));
+    D.h->ulv_full();
+    HSSMF_CUDA(cudaEventRecord(e2, D.s));
+    HSSMF_CUDA(cudaStreamSynchronize(D.s));
+    float a1 = 0, a2 = 0;
+    HSSMF_CUDA(cudaEventElapsedTime(&a1, e0, e1));
+    HSSMF_CUDA(cudaEventElapsedTime(&a2, e1, e2));
+    D.cms = a1;
+    D.ums = a2;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+  }
+
+  void DenseHss::solve(double* b, int ldb, int nrhs, bool on_device) {
+    auto& D = *d_;
+    HSSMF_CUDA(cudaSetDevice(D.device));
+    for (int c = 0; c < nrhs; c++) {
+      double* col = b + (size_t)c * ldb;
+      if (on_device) {
+        D.h->solve_full(col);
+      } else {
+        HSSMF_CUDA(cudaMemcpyAsync(D.x, col, D.n * sizeof(double), cudaMemcpyHostToDevice, D.s));
+        D.h->solve_full(D.x);
+        HSSMF_CUDA(cudaMemcpyAsync(col, D.x, D.n * sizeof(double), cudaMemcpyDeviceToHost, D.s));
+      }
+    }
+    HSSMF_CUDA(cudaStreamSynchronize(D.s));
+  }
+
+  void DenseHss::ranks(std::vector<int>& u, std::vector<int>& v) const { d_->h->ranks(u, v); }
+  int DenseHss::rounds() const { return d_->h->rounds(); }
+  int DenseHss::d_final() const { return d_->h->d_final(); }
+  double DenseHss::compress_ms() const { return d_->cms; }
+  double DenseHss::ulv_ms() const { return d_->ums; }
+
+}  // namespace hssmf_b200

@@ -17,9 +17,9 @@ namespace hssmf_b200 {
       }
       const CopyDesc d = ds[lo];
       const long long base = (b - pre[lo]) * CPB;
-      const long long tot = (long long)d.nr * d.nc;
+      const long long tot = d.diag ? d.nr : (long long)d.nr * d.nc;
       for (long long e = base + threadIdx.x; e < base + CPB && e < tot; e += blockDim.x) {
-        const int i = (int)(e % d.nr), j = (int)(e / d.nr);
+        const int i = d.diag ? (int)e : (int)(e % d.nr), j = d.diag ? (int)e : (int)(e / d.nr);
         const long long si = d.sr ? d.sr[i] : d.sr_off + i;
         const long long sj = d.sc ? d.sc[j] : d.sc_off + j;
         const long long di = d.dr ? d.dr[i] : d.dr_off + i;
@@ -254,11 +254,12 @@ namespace hssmf_b200 {
   void index_copy_run(const std::vector<CopyDesc>& d0, cudaStream_t s) {
     std::vector<CopyDesc> d;
     for (const auto& x : d0)
-      if (x.nr > 0 && x.nc > 0) d.push_back(x);
+      if (x.nr > 0 && (x.nc > 0 || x.diag)) d.push_back(x);
     if (d.empty()) return;
     std::vector<long long> pre(d.size() + 1, 0);
     for (size_t i = 0; i < d.size(); i++)
-      pre[i + 1] = pre[i] + ((long long)d[i].nr * d[i].nc + CPB - 1) / CPB;
+      pre[i + 1] = pre[i] + ((d[i].diag ? (long long)d[i].nr : (long long)d[i].nr * d[i].nc) +
+                             CPB - 1) / CPB;
     auto* dd = upload_async(d, s);
     auto* dp = upload_async(pre, s);
     index_copy_kernel<<<(unsigned)pre.back(), 256, 0, s>>>(dd, dp, (int)d.size());

@@ -27,11 +27,13 @@ namespace hssmf_b200 {
     int nr, nc;
     double alpha;
     int accumulate;
+    int diag;  // copy only the pairs (i, i), i < nr
   };
 
   inline CopyDesc copy_block(const double* src, long long lds, double* dst, long long ldd, int nr,
                              int nc) {
-    return {src, 1, lds, nullptr, nullptr, 0, 0, dst, ldd, nullptr, nullptr, 0, 0, nr, nc, 1.0, 0};
+    return {src, 1, lds, nullptr, nullptr, 0, 0, dst, ldd, nullptr, nullptr, 0, 0, nr, nc, 1.0, 0,
+            0};
   }
 
   // runs a host list of descriptors (uploads them stream-ordered)

@@ -1,0 +1,244 @@
+"""HSS compression / ULV / HSS-multifrontal on the B200 vs the reference.
+
+Restates the reference's HSS and multifrontal KATs (test_hss.cpp,
+test_multifrontal.cpp:385-481) and checks the north-star gates: per-node
+ranks within +-10% of the reference's (at least +-2 for tiny ranks), final
+relative residual no worse than 10x the reference's at the same tolerance."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1502_07405_b200 as P
+from paper_1502_07405_b200.problems import csr_matvec, dense_c2, x_true
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def balanced_leaves(n, leaf):
+    out = []
+
+    def rec(b, e):
+        if e - b <= leaf:
+            out.append((b, e))
+            return
+        mid = b + (e - b) // 2
+        rec(b, mid)
+        rec(mid, e)
+    rec(0, n)
+    return out
+
+
+def structured(n, leaf, rank, shift, seed):
+    """global rank-`rank` product + dense leaf-diagonal blocks + shift
+    (test_hss.cpp:27-41, restated with numpy's generator)"""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(-1, 1, (n, rank)) @ rng.uniform(-1, 1, (rank, n))
+    for b, e in balanced_leaves(n, leaf):
+        a[b:e, b:e] += rng.uniform(-1, 1, (e - b, e - b))
+    a += shift * np.eye(n)
+    return a
+
+
+def staggered(seed):
+    """leaf couplings rank 6, top-level couplings rank 10 (test_hss.cpp:53-80)"""
+    rng = np.random.default_rng(seed)
+    n = 128
+    a = np.zeros((n, n))
+    for b, e in balanced_leaves(n, 32):
+        a[b:e, b:e] += rng.uniform(-1, 1, (32, 32))
+    a += 80 * np.eye(n)
+    for b0 in (0, 64):
+        a[b0:b0 + 32, b0 + 32:b0 + 64] += np.outer(rng.uniform(-1, 1, 32), rng.uniform(-1, 1, 32))
+        a[b0 + 32:b0 + 64, b0:b0 + 32] += np.outer(rng.uniform(-1, 1, 32), rng.uniform(-1, 1, 32))
+    for i0, j0 in ((0, 64), (64, 0)):
+        for q in (0, 32):
+            a[i0 + q:i0 + q + 32, j0 + q:j0 + q + 32] += (
+                rng.uniform(-1, 1, (32, 5)) @ rng.uniform(-1, 1, (5, 32)))
+    return a
+
+
+def hopts(**kw):
+    return P.HssOptions(**kw)
+
+
+def ranks_close(mine, ref, rel=0.10, slack=2):
+    mine = np.asarray(mine)
+    ref = np.asarray(ref)
+    return np.all(np.abs(mine - ref) <= np.maximum(slack, rel * ref))
+
+
+def test_diagonal_rank_zero_and_exact_division():
+    n = 64
+    d = 1.0 + np.arange(n)
+    h = P.hss_compress(np.diag(d), 16, hopts())
+    assert h.rounds == 1 and h.hss_rank() == 0
+    a2 = np.diag(2.0 + np.arange(n))
+    h2 = P.hss_compress(a2, 16, hopts())
+    b = np.random.default_rng(17).uniform(-1, 1, (n, 2))
+    x = h2.solve(b)
+    assert np.array_equal(x, b / (2.0 + np.arange(n))[:, None])
+    assert np.all(h2.solve(np.zeros(n)) == 0.0)
+
+
+def test_rank_one_recovered_exactly(oracle):
+    n = 128
+    rng = np.random.default_rng(21)
+    a = np.outer(rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)) + np.eye(n)
+    h = P.hss_compress(a, 32, hopts(eps=1e-12))
+    assert np.all(h.u_rank[:-1] == 1) and np.all(h.v_rank[:-1] == 1)
+    r = oracle.DenseHss(a, leaf=32, eps=1e-12)
+    assert np.array_equal(r.u_rank[:-1], h.u_rank[:-1])
+
+
+def test_adaptation_rounds(oracle):
+    # test_hss.cpp:206-220: d0=4, dd=8 -> rounds 3, d_final 20, rank 8
+    a = structured(256, 32, 8, 40.0, 31)
+    h = P.hss_compress(a, 32, hopts(eps=1e-8, d0=4, dd=8))
+    assert (h.rounds, h.d_final, h.hss_rank()) == (3, 20, 8)
+    r = oracle.DenseHss(a, leaf=32, eps=1e-8, d0=4, dd=8)
+    assert (r.rounds, r.d_final) == (3, 20)
+    x = h.solve(np.ones(256))
+    assert np.linalg.norm(a @ x - 1) / 16 <= 1e-6
+
+
+def test_staggered_two_rounds(oracle):
+    a = staggered(71)
+    h = P.hss_compress(a, 32, hopts(eps=1e-8, d0=16, dd=16))
+    r = oracle.DenseHss(a, leaf=32, eps=1e-8, d0=16, dd=16)
+    assert (h.rounds, h.hss_rank()) == (r.rounds, 10) == (2, 10)
+
+
+def test_ulv_solve_matches_dense_and_multi_rhs_bitwise():
+    n = 256
+    a = structured(n, 64, 6, 500.0, 23)
+    h = P.hss_compress(a, 64, hopts(eps=1e-12))
+    b = np.random.default_rng(24).uniform(-1, 1, n)
+    x = h.solve(b)
+    xr = np.linalg.solve(a, b)
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-10
+    bm = np.asfortranarray(np.random.default_rng(25).uniform(-1, 1, (n, 3)))
+    xm = h.solve(bm)
+    for k in range(3):
+        assert h.solve(bm[:, k]).tobytes() == np.ascontiguousarray(xm[:, k]).tobytes()
+
+
+def test_high_rank_compression_solves():
+    n = 128
+    rng = np.random.default_rng(33)
+    a = rng.uniform(-1, 1, (n, n)) + 70 * np.eye(n)
+    h = P.hss_compress(a, 32, hopts(eps=1e-15))
+    b = rng.uniform(-1, 1, n)
+    xr = np.linalg.solve(a, b)
+    assert np.linalg.norm(h.solve(b) - xr) / np.linalg.norm(xr) <= 1e-10
+
+
+def test_rank_cap_raises():
+    a = structured(128, 32, 8, 40.0, 97)
+    with pytest.raises(P.HssRankExceeded):
+        P.hss_compress(a, 32, hopts(eps=1e-8, max_rank=4))
+
+
+def test_singular_cluster_reported():
+    d = 1.0 + np.arange(64)
+    d[37] = 0.0
+    with pytest.raises(P.SingularMatrixError) as e:
+        P.hss_compress(np.diag(d), 16, hopts())
+    assert "cluster" in str(e.value)
+
+
+def test_dense_c2_reduced_size_vs_reference(oracle):
+    # BASELINE config 2 operator at N=4096 (full size in bench/slow test)
+    n = 4096
+    a = dense_c2(n)
+    h = P.hss_compress(a, 128, hopts(eps=1e-8))
+    r = oracle.DenseHss(a, leaf=128, eps=1e-8)
+    assert ranks_close(h.u_rank[:-1], r.u_rank[:-1])
+    b = x_true(n, 1)
+    x = h.solve(b)
+    xr = r.solve(b)[:, 0]
+    res = np.linalg.norm(a @ x - b) / np.linalg.norm(b)
+    rres = np.linalg.norm(a @ xr - b) / np.linalg.norm(b)
+    assert res <= 10 * max(rres, 1e-15)
+
+
+# ---------------------------------------------------------------- multifrontal
+def run_mf(kind, k, nd_leaf, **so):
+    op = P.ordered_grid(kind, k, nd_leaf)
+    ptr, ind, val = op.a.arrays()
+    b = csr_matvec(ptr, ind, val, x_true(op.a.size(), 1))
+    m = P.mf_factor(op.a, op.t, P.SolverOptions(nd_leaf=nd_leaf, **so))
+    x = P.mf_solve_new(m, b)
+    res = np.linalg.norm(op.a.matvec(x) - b) / np.linalg.norm(b)
+    return op, m, b, x, res
+
+
+def ref_mf(oracle, kind, k, nd_leaf, b, **so):
+    o = oracle.ordered_grid(kind, k, nd_leaf)
+    mode = {"auto": 0, "mf": 1, "mf-hss": 2}[so.pop("mode", "auto")]
+    F = oracle.Factors(o, mode=mode, **so)
+    xr = F.solve(b)[:, 0]
+    import scipy.sparse as sp
+    A = sp.csr_matrix((o.val, o.ind, o.ptr), shape=(o.n, o.n))
+    return F, np.linalg.norm(A @ xr - b) / np.linalg.norm(b)
+
+
+def compare_fronts(m, F):
+    assert np.array_equal(m.type, F.type)
+    hs = np.nonzero(F.type == 1)[0]
+    assert ranks_close(m.rank[hs], F.rank[hs])
+    for i in hs:
+        mine = m.front_hss(int(i))
+        ref = F.front_hss(int(i))
+        assert ranks_close(mine[0][:-1], ref[0][:-1]), (i, mine[0], ref[0])
+
+
+def test_compressed_fronts_kat(oracle):
+    # test_multifrontal.cpp:385-441
+    so = dict(ls=3, min_hss=24, leaf=16, eps=1e-10, d0=32, dd=32, p=8)
+    op, m, b, x, res = run_mf("p2d", 31, 16, **so)
+    assert m.hss_fronts >= 1 and m.fallbacks == 0 and m.max_front_rank >= 1
+    assert res <= 1e-6
+    F, rres = ref_mf(oracle, "p2d", 31, 16, b, **so)
+    compare_fronts(m, F)
+    assert res <= 10 * max(rres, 1e-16)
+
+
+def test_compressed_root_full_ulv(oracle):
+    # test_multifrontal.cpp:443-460
+    so = dict(ls=1, min_hss=16, leaf=8, eps=1e-12, d0=16, dd=16, p=4)
+    op, m, b, x, res = run_mf("p2d", 31, 16, **so)
+    assert m.hss_fronts == 1 and m.front_stats[op.t.root_id()].type == "hss"
+    assert res <= 1e-9
+
+
+def test_rank_guard_fallback(oracle):
+    # test_multifrontal.cpp:462-481
+    so = dict(ls=9, min_hss=16, leaf=16, eps=1e-12, max_rank=4, d0=8, dd=4, p=2)
+    op, m, b, x, res = run_mf("p2d", 15, 16, **so)
+    assert m.fallbacks >= 1
+    assert any(f.type == "hss_dense" for f in m.front_stats)
+    assert res <= 1e-9
+    F, _ = ref_mf(oracle, "p2d", 15, 16, b, **so)
+    assert np.array_equal(m.type, F.type)
+
+
+def test_c1_hss_vs_golden():
+    g = np.load(os.path.join(GOLD, "ref_c1.npz"))
+    so = dict(ls=64, min_hss=256, leaf=64, eps=1e-6, d0=128, dd=128, p=10)
+    op, m, b, x, res = run_mf("p2d", 256, 64, **so)
+    assert np.array_equal(m.type, g["type"])
+    hs = g["hss_ids"]
+    assert ranks_close(m.rank[hs], g["rank"][hs])
+    for q, i in enumerate(hs):
+        u = m.front_hss(int(i))[0]
+        ru = g["node_u"][g["node_ptr"][q]:g["node_ptr"][q + 1]]
+        assert ranks_close(u[:-1], ru[:-1])
+    assert res <= 10 * float(g["relres"])
+
+
+def test_c1_hss_off_vs_golden():
+    g = np.load(os.path.join(GOLD, "ref_c1_mf.npz"))
+    op, m, b, x, res = run_mf("p2d", 256, 64, mode="mf")
+    assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-10
