@@ -62,10 +62,10 @@ namespace hssmf_b200 {
     }
 
     enum KClass { K_ASM, K_EXTADD, K_PANEL, K_TRSM, K_GEMM_TRAIL, K_GEMM_SCHUR, K_HSS,
-                  K_SOLVE_FWD, K_SOLVE_BWD, K_NCLASS };
-    const char* kclass_name[K_NCLASS] = {"assemble_sparse", "extend_add", "lu_panel",
+                  K_SOLVE_FWD, K_SOLVE_BWD, K_HSS_PH, K_NCLASS = K_HSS_PH + kHssPhases };
+    const char* kclass_name[K_HSS_PH] = {"assemble_sparse", "extend_add", "lu_panel",
                                          "l21_swap_trsm", "gemm_trailing", "gemm_schur",
-                                         "hss_front", "solve_forward", "solve_backward"};
+                                         "hss_front_total", "solve_forward", "solve_backward"};
   }  // namespace
 
   struct StepBatch {
@@ -190,7 +190,8 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaSetDevice(device));
     HSSMF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     d_->s = stream_;
-    for (int k = 0; k < K_NCLASS; k++) d_->kstat[k].name = kclass_name[k];
+    for (int k = 0; k < K_NCLASS; k++)
+      d_->kstat[k].name = k < K_HSS_PH ? kclass_name[k] : hss_phase_name(k - K_HSS_PH);
     // keep stream-ordered allocations (HSS path) in the pool between factorizations
     cudaMemPool_t mp;
     HSSMF_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
@@ -628,7 +629,19 @@ namespace hssmf_b200 {
     factor_ms_ = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (profile_) D.collect();
+    if (profile_) {
+      D.collect();
+      for (auto& h : D.hss) {
+        if (!h) continue;
+        auto ps = h->phase_stats();
+        for (int p = 0; p < kHssPhases; p++) {
+          auto& k = D.kstat[K_HSS_PH + p];
+          k.launches += ps[p].count;
+          k.ms += ps[p].ms;
+          k.flops += ps[p].flops;
+        }
+      }
+    }
     // first failure in postorder = the one the sequential reference reports
     for (int i = 0; i < nn; i++)
       if (st[i] >= 0)

@@ -171,6 +171,41 @@ namespace hssmf_b200 {
     double* bhat = nullptr;  // r0 (partial) / r0 + r1 (full)
     double* tmp = nullptr;
 
+    // per-phase device time (CUDA events on the HSS stream), collected on demand
+    struct PhEv { int ph; cudaEvent_t a, b; double flops; };
+    std::vector<PhEv> phev;
+    double ph_ms[kHssPhases] = {}, ph_fl[kHssPhases] = {};
+    int ph_n[kHssPhases] = {};
+    struct Ph {
+      HssImpl* h;
+      int id;
+      cudaEvent_t a;
+      double f0;
+      Ph(HssImpl* hh, int i) : h(hh), id(i), f0(hh->flops) {
+        HSSMF_CUDA(cudaEventCreate(&a));
+        HSSMF_CUDA(cudaEventRecord(a, h->s));
+      }
+      ~Ph() {
+        cudaEvent_t b;
+        if (cudaEventCreate(&b) == cudaSuccess && cudaEventRecord(b, h->s) == cudaSuccess)
+          h->phev.push_back({id, a, b, h->flops - f0});
+      }
+    };
+    void collect_phases() {
+      if (!phev.empty()) cudaStreamSynchronize(s);
+      for (auto& e : phev) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e.a, e.b);
+        ph_ms[e.ph] += ms;
+        ph_fl[e.ph] += e.flops;
+        ph_n[e.ph]++;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+      }
+      phev.clear();
+    }
+    ~HssImpl() { collect_phases(); }
+
     explicit HssImpl(cudaStream_t st) : s(st) {}
 
     // ---------------------------------------------------------- compression
@@ -228,17 +263,20 @@ namespace hssmf_b200 {
         R.ensure(d);
         Sr.ensure(d);
         Sc.ensure(d);
-        rng_fill(seeds.p, 0, m, dold, d, R.col(dold), m, s);
-        // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
-        // hss_compress.hpp:359-363)
-        std::vector<GemmProblem> p1{{A, R.col(dold), Sr.col(dold), m, dn, m, (int)lda, m, m}};
-        gemm_run_host(p1, 'N', 'N', 1.0, 0.0, s);
-        std::vector<GemmProblem> p2{{A, R.col(dold), Sc.col(dold), m, dn, m, (int)lda, m, m}};
-        gemm_run_host(p2, 'T', 'N', 1.0, 0.0, s);
-        flops += 4.0 * m * m * dn;
-        R.cols = Sr.cols = Sc.cols = d;
-        maxabs_run(Sr.col(dold), m, m, dn, scale.p, s);
-        maxabs_run(Sc.col(dold), m, m, dn, scale.p, s);
+        {
+          Ph ph_(this, 0);
+          rng_fill(seeds.p, 0, m, dold, d, R.col(dold), m, s);
+          // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
+          // hss_compress.hpp:359-363)
+          std::vector<GemmProblem> p1{{A, R.col(dold), Sr.col(dold), m, dn, m, (int)lda, m, m}};
+          gemm_run_host(p1, 'N', 'N', 1.0, 0.0, s);
+          std::vector<GemmProblem> p2{{A, R.col(dold), Sc.col(dold), m, dn, m, (int)lda, m, m}};
+          gemm_run_host(p2, 'T', 'N', 1.0, 0.0, s);
+          flops += 4.0 * m * m * dn;
+          R.cols = Sr.cols = Sc.cols = d;
+          maxabs_run(Sr.col(dold), m, m, dn, scale.p, s);
+          maxabs_run(Sc.col(dold), m, m, dn, scale.p, s);
+        }
         double sc = 0;
         HSSMF_CUDA(cudaMemcpyAsync(&sc, scale.p, sizeof(double), cudaMemcpyDeviceToHost, s));
         HSSMF_CUDA(cudaStreamSynchronize(s));
@@ -350,8 +388,12 @@ namespace hssmf_b200 {
         if (!N.leaf && (nodes[N.c0].state != DONE || nodes[N.c1].state != DONE)) continue;
         act.push_back(n);
       }
-      update_done(updl);
+      {
+        Ph ph_(this, 5);
+        update_done(updl);
+      }
       if (act.empty()) return;
+      Ph ph_(this, 1);
       // extract the dense pieces once (compress_pass, hss_compress.hpp:226-237)
       std::vector<CopyDesc> ext;
       for (int n : act) {
@@ -384,7 +426,10 @@ namespace hssmf_b200 {
         act.erase(std::find(act.begin(), act.end(), root));
       }
       if (act.empty()) return;
-      build_local_samples(act);
+      {
+        Ph ph2(this, 2);
+        build_local_samples(act);
+      }
       id_batch(act, cap_id, abs_tol, fail);
     }
 
@@ -458,7 +503,11 @@ namespace hssmf_b200 {
       dt.alloc(tasks.size(), s);
       HSSMF_CUDA(cudaMemcpyAsync(dt.p, tasks.data(), tasks.size() * sizeof(CpqrTask),
                                  cudaMemcpyHostToDevice, s));
-      cpqr_run(dt.p, (int)tasks.size(), d, max_n, o.eps, abs_tol, s);
+      {
+        Ph ph_(this, 3);
+        cpqr_run(dt.p, (int)tasks.size(), d, max_n, o.eps, abs_tol, s);
+      }
+      Ph ph4(this, 4);
       std::vector<int> ho(4 * na);
       HSSMF_CUDA(cudaMemcpyAsync(ho.data(), outs.p, ho.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
       HSSMF_CUDA(cudaStreamSynchronize(s));
@@ -649,6 +698,7 @@ namespace hssmf_b200 {
     // transformed node block G = Omega X Psi, then partial LU of its leading
     // k x k block (ulv_eliminate, hss_ulv.hpp:76-121), batched per level
     void eliminate(const std::vector<int>& set) {
+      Ph ph_(this, 6);
       std::vector<std::vector<int>> byd(maxdepth + 1);
       for (int n : set) byd[nodes[n].depth].push_back(n);
       for (int lv = maxdepth; lv >= 0; lv--) {
@@ -765,6 +815,7 @@ namespace hssmf_b200 {
 
     // dense LU of Z (zn x zn) with ns leading columns eliminated
     void factor_top(int ns, int nus, int blame) {
+      Ph ph_(this, 7);
       Zpiv.alloc(2 * ns + 1, s);
       FrontDev f{};
       f.ns = ns;
@@ -883,6 +934,7 @@ namespace hssmf_b200 {
       assemble_top(false);
       factor_top(r0, r1, c0);
       // densified update  F22|hss - Theta^* Phi = F22|hss + Ubig1 C Vbig1^*
+      Ph ph_(this, 8);
       std::vector<int> set1;
       subtree(c1, set1);
       big_bases(set1);
@@ -1137,5 +1189,15 @@ namespace hssmf_b200 {
     return s;
   }
   double HssMatrixDev::flops() const { return d_->flops; }
+  std::vector<HssPhaseStat> HssMatrixDev::phase_stats() {
+    d_->collect_phases();
+    std::vector<HssPhaseStat> v(kHssPhases);
+    for (int i = 0; i < kHssPhases; i++) {
+      v[i].ms = d_->ph_ms[i];
+      v[i].flops = d_->ph_fl[i];
+      v[i].count = d_->ph_n[i];
+    }
+    return v;
+  }
 
 }  // namespace hssmf_b200

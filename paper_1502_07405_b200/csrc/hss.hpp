@@ -51,6 +51,19 @@ namespace hssmf_b200 {
 
   struct HssImpl;
 
+  // device-time phases of the HSS path (profiling)
+  constexpr int kHssPhases = 9;
+  inline const char* hss_phase_name(int i) {
+    static const char* n[kHssPhases] = {"hss_sample_gemm", "hss_extract", "hss_local_samples",
+                                        "hss_cpqr", "hss_id_finalize", "hss_update_done",
+                                        "hss_ulv_eliminate", "hss_ulv_top", "hss_densify"};
+    return n[i];
+  }
+  struct HssPhaseStat {
+    double ms = 0, flops = 0;
+    int count = 0;
+  };
+
   class HssMatrixDev {
   public:
     HssMatrixDev(cudaStream_t s);
@@ -83,6 +96,7 @@ namespace hssmf_b200 {
     void ranks(std::vector<int>& u, std::vector<int>& v) const;
     long long stored_scalars() const;
     double flops() const;
+    std::vector<HssPhaseStat> phase_stats();
 
   private:
     std::unique_ptr<HssImpl> d_;
