@@ -1,6 +1,9 @@
 #include "cpqr.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace hssmf_b200 {
@@ -196,11 +199,225 @@ namespace hssmf_b200 {
       }
     }
 
+    // ---- cluster CPQR: one thread-block cluster (CL CTAs) per task --------
+    // Columns are dealt cyclically to the CTAs of the cluster (column j lives
+    // in CTA j % CL, its norms in that CTA's shared memory). Per elimination
+    // step: local pivot candidates -> cluster barrier -> every CTA reduces
+    // the CL candidates over DSMEM (identical decision everywhere) -> the
+    // owner of column k swaps, builds the reflector -> cluster barrier ->
+    // every CTA applies it to its own trailing columns and downdates norms.
+    // The matrix stays in global memory and is only accessed with L2-coherent
+    // (.cg) loads, since columns migrate between CTAs on pivot swaps.
+    struct ClPub {
+      double bv;
+      int bi;
+      int pad;
+      double tau;
+    };
+
+    __global__ void __launch_bounds__(CT)
+    cpqr_cluster_kernel(const CpqrTask* __restrict__ tasks, double eps, double abs_tol,
+                        int CL) {
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      const int rank = (int)cl.block_rank();
+      extern __shared__ double sm[];
+      const CpqrTask T = tasks[blockIdx.x / CL];
+      const int m = T.m, n = T.n, ld = T.ldy;
+      double* Y = T.Y;
+      const int nloc = (n + CL - 1) / CL;
+      double* nrm2 = sm;
+      double* last = nrm2 + nloc;
+      double* v = last + nloc;
+      __shared__ ClPub pub;
+      __shared__ double rv[NW];
+      __shared__ int ri[NW];
+      __shared__ int s_p, s_stop, s_cert;
+      __shared__ double s_r11, s_tau;
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      const int kmax_dim = min(m, n);
+      const int kmax = T.max_rank < 0 ? kmax_dim : min(kmax_dim, T.max_rank);
+      if (m == 0 || n == 0) {
+        if (rank == 0) {
+          for (int j = tid; j < n; j += CT) T.perm[j] = j;
+          if (tid == 0) { T.out[0] = 0; T.out[1] = 1; }
+        }
+        return;
+      }
+      // own columns: j = rank + CL * jl
+      for (int jl = warp; jl < nloc; jl += NW) {
+        const int j = rank + CL * jl;
+        if (j >= n) break;
+        const double* c = Y + (size_t)j * ld;
+        double s = 0;
+        for (int i = lane; i < m; i += 32) {
+          const double x = __ldcg(c + i);
+          s += x * x;
+        }
+        s = warp_sum(s);
+        if (lane == 0) { nrm2[jl] = s; last[jl] = s; }
+      }
+      if (rank == 0)
+        for (int j = tid; j < n; j += CT) T.perm[j] = j;
+      if (tid == 0) { s_r11 = 0; s_cert = 0; }
+      __syncthreads();
+      int k = 0;
+      while (true) {
+        // 1. local pivot candidate among own columns j >= k
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int jl = tid; jl < nloc; jl += CT) {
+          const int j = rank + CL * jl;
+          if (j >= k && j < n && nrm2[jl] > bv) { bv = nrm2[jl]; bi = j; }
+        }
+        warp_argmax(bv, bi);
+        if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+          double b = rv[0];
+          int p = ri[0];
+          for (int w = 1; w < NW; w++)
+            if (rv[w] > b || (rv[w] == b && ri[w] < p)) { b = rv[w]; p = ri[w]; }
+          pub.bv = b;
+          pub.bi = p;
+        }
+        cl.sync();
+        // 2. global decision (identical in every CTA)
+        if (tid == 0) {
+          double b = -1.0;
+          int p = 0x7fffffff;
+          for (int r = 0; r < CL; r++) {
+            const ClPub* q = cl.map_shared_rank(&pub, r);
+            if (q->bv > b || (q->bv == b && q->bi < p)) { b = q->bv; p = q->bi; }
+          }
+          const double pv = b > 0.0 ? sqrt(b) : 0.0;
+          int stop = 0;
+          if (k == 0) {
+            s_r11 = pv;
+            if (pv == 0.0 || pv <= abs_tol) { stop = 1; s_cert = 1; }
+          } else if (pv <= eps * s_r11 || pv <= abs_tol) {
+            stop = 1;
+            s_cert = 1;
+          }
+          if (!stop && k == kmax) {
+            stop = 1;
+            s_cert = (k == kmax_dim);
+          }
+          s_p = p;
+          s_stop = stop;
+        }
+        __syncthreads();
+        if (s_stop) break;
+        const int p = s_p;
+        const int ok = k % CL;
+        double* ck = Y + (size_t)k * ld;
+        if (rank == ok) {
+          if (p != k) {
+            double* cp = Y + (size_t)p * ld;
+            for (int i = tid; i < m; i += CT) {
+              const double t = __ldcg(ck + i);
+              __stcg(ck + i, __ldcg(cp + i));
+              __stcg(cp + i, t);
+            }
+            if (tid == 0) {
+              double* nk = cl.map_shared_rank(nrm2, ok) + k / CL;
+              double* np = cl.map_shared_rank(nrm2, p % CL) + p / CL;
+              double* lk = cl.map_shared_rank(last, ok) + k / CL;
+              double* lp = cl.map_shared_rank(last, p % CL) + p / CL;
+              double t = *nk; *nk = *np; *np = t;
+              t = *lk; *lk = *lp; *lp = t;
+              const int q = T.perm[k]; T.perm[k] = T.perm[p]; T.perm[p] = q;
+            }
+            __syncthreads();
+          }
+          // 3. Householder reflector of column k (rrqr.hpp:85-103)
+          double s = 0;
+          for (int i = k + 1 + tid; i < m; i += CT) {
+            const double x = __ldcg(ck + i);
+            s += x * x;
+          }
+          s = warp_sum(s);
+          if (lane == 0) rv[warp] = s;
+          __syncthreads();
+          if (tid == 0) {
+            double xs = 0;
+            for (int w = 0; w < NW; w++) xs += rv[w];
+            const double xn = sqrt(xs);
+            const double alpha = __ldcg(ck + k);
+            double tk = 0, sc = 0;
+            if (xn != 0.0 || fabs(alpha) != 0.0) {
+              double beta = hypot(fabs(alpha), xn);
+              if (alpha > 0.0) beta = -beta;
+              if (beta != 0.0) {
+                tk = (beta - alpha) / beta;
+                sc = 1.0 / (alpha - beta);
+                __stcg(ck + k, beta);
+              }
+            }
+            pub.tau = tk;
+            rv[0] = sc;
+          }
+          __syncthreads();
+          const double sc = rv[0];
+          if (pub.tau != 0.0)
+            for (int i = k + 1 + tid; i < m; i += CT) __stcg(ck + i, __ldcg(ck + i) * sc);
+        }
+        cl.sync();
+        // 4. apply the reflector to own trailing columns, downdate norms
+        if (tid == 0) s_tau = cl.map_shared_rank(&pub, ok)->tau;
+        for (int i = k + 1 + tid; i < m; i += CT) v[i] = __ldcg(ck + i);
+        __syncthreads();
+        const double tk = s_tau;
+        int jl0 = (k + 1 - rank + CL - 1) / CL;
+        if (jl0 < 0) jl0 = 0;
+        for (int jl = jl0 + warp; jl < nloc; jl += NW) {
+          const int j = rank + CL * jl;
+          if (j >= n) break;
+          double* cj = Y + (size_t)j * ld;
+          if (tk != 0.0) {
+            double w = 0;
+            for (int i = k + 1 + lane; i < m; i += 32) w += v[i] * __ldcg(cj + i);
+            w = warp_sum(w) + __ldcg(cj + k);
+            w *= tk;
+            if (lane == 0) __stcg(cj + k, __ldcg(cj + k) - w);
+            for (int i = k + 1 + lane; i < m; i += 32) __stcg(cj + i, __ldcg(cj + i) - w * v[i]);
+          }
+          __syncwarp();
+          const double rk = __ldcg(cj + k);
+          double nj = nrm2[jl] - rk * rk;
+          if (nj < 0.0) nj = 0.0;
+          if (nj < 0.1 * last[jl]) {
+            double q = 0;
+            for (int i = k + 1 + lane; i < m; i += 32) {
+              const double x = __ldcg(cj + i);
+              q += x * x;
+            }
+            q = warp_sum(q);
+            if (lane == 0) { nrm2[jl] = q; last[jl] = q; }
+          } else if (lane == 0) {
+            nrm2[jl] = nj;
+          }
+        }
+        __syncthreads();
+        k++;
+        if (k == kmax_dim) {
+          if (tid == 0) s_cert = 1;
+          break;
+        }
+      }
+      cl.sync();  // keep peers' shared memory alive until every CTA is done
+      if (rank == 0 && tid == 0) { T.out[0] = k; T.out[1] = s_cert; }
+    }
+
     void set_attr() {
       static bool done = false;
       if (done) return;
       HSSMF_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       220 * 1024));
+      HSSMF_CUDA(cudaFuncSetAttribute(cpqr_cluster_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      HSSMF_CUDA(cudaFuncSetAttribute(cpqr_cluster_kernel,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       HSSMF_CUDA(cudaFuncSetAttribute(id_solve_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       done = true;
@@ -211,9 +428,34 @@ namespace hssmf_b200 {
                 double abs_tol, cudaStream_t s) {
     if (!ntask) return;
     set_attr();
-    const size_t smem = (size_t)max_n * 20 + (size_t)max_m * 8 + 64;
-    if (smem > 220 * 1024) throw CudaError("cpqr: task too large for shared memory");
-    cpqr_kernel<<<ntask, CT, smem, s>>>(tasks, eps, abs_tol);
+    // cluster width: enough CTAs that each owns ~32 columns, at most 16
+    int CL = 1;
+    while (CL < 16 && (long long)max_n * max_m > (long long)CL * 32 * 512) CL *= 2;
+    const char* env = getenv("HSSMF_CPQR_CLUSTER");
+    if (env) CL = std::max(1, std::min(16, atoi(env)));
+    if (CL == 1) {
+      const size_t smem = (size_t)max_n * 20 + (size_t)max_m * 8 + 64;
+      if (smem > 220 * 1024) throw CudaError("cpqr: task too large for shared memory");
+      cpqr_kernel<<<ntask, CT, smem, s>>>(tasks, eps, abs_tol);
+      HSSMF_LAUNCH_CHECK();
+      return;
+    }
+    const int nloc = (max_n + CL - 1) / CL;
+    const size_t smem = (size_t)nloc * 16 + (size_t)max_m * 8 + 64;
+    if (smem > 200 * 1024) throw CudaError("cpqr: task too large for shared memory");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntask * CL);
+    cfg.blockDim = dim3(CT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HSSMF_CUDA(cudaLaunchKernelEx(&cfg, cpqr_cluster_kernel, tasks, eps, abs_tol, CL));
     HSSMF_LAUNCH_CHECK();
   }
 

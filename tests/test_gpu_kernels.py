@@ -87,6 +87,22 @@ def test_id_matches_reference(oracle, m, n, rank):
             assert np.linalg.norm(y[:, J] @ full - y) <= 1e3 * max(eps, 1e-12) * np.linalg.norm(y) + 1e-6
 
 
+@pytest.mark.parametrize("cl", ["1", "2", "4", "8", "16"])
+def test_id_cluster_cpqr_matches_reference(oracle, monkeypatch, cl):
+    # the multi-CTA (thread-block cluster) CPQR must reproduce the reference's
+    # pivots, ranks, certification and coefficients
+    monkeypatch.setenv("HSSMF_CPQR_CLUSTER", cl)
+    rng = np.random.default_rng(5)
+    m, n, rank = 260, 500, 90
+    y = (rng.standard_normal((m, rank)) * np.logspace(0, -9, rank)) @ rng.standard_normal((rank, n))
+    for eps, mr in [(1e-6, -1), (1e-12, -1), (1e-6, 20)]:
+        p, k, cert, x = A.dev_interpolative_decomposition(y, eps, mr, 0.0)
+        wp, wk, wcert, wx = oracle.interpolative_decomposition(y, eps, mr, 0.0)
+        assert (k, cert) == (wk, wcert)
+        assert np.array_equal(p[:k], wp[:k])
+        assert np.allclose(x, wx, rtol=1e-6, atol=1e-8 * np.abs(wx).max())
+
+
 def test_id_zero_and_empty():
     p, k, cert, _ = A.dev_interpolative_decomposition(np.zeros((8, 5)), 1e-6)
     assert k == 0 and cert and list(p) == [0, 1, 2, 3, 4]
