@@ -1,0 +1,45 @@
+// Interpolative decomposition through the Gram matrix (blocked, pivoted
+// Cholesky) -- a BLAS3 restatement of the reference's tolerance-truncated
+// column-pivoted Householder QR (rrqr_tolerance, rrqr.hpp:32-151).
+//
+// For Y (d x n) the CPQR pivot at step k is the column of largest residual
+// norm after projecting out the k chosen columns; those residual norms are
+// exactly the diagonal of the Schur complement of the Gram matrix G = Y^T Y
+// after k steps of symmetric pivoted Cholesky, and R = L^T. Stop tests,
+// tie-breaking (lowest current position), the rank cap and certification
+// follow the reference verbatim; only the arithmetic route differs. G is
+// accumulated incrementally across adaptive rounds (new sample columns only),
+// so a round costs one rank-dd update plus the factorization, instead of a
+// level-2 sweep over d x n per elimination step.
+//
+// Accuracy: R (hence the ID coefficients) carries kappa(R11)^2 u relative
+// error; the engine uses this route only when eps >= 1e-5 (kappa(R11) <~
+// 1/eps), where that is below 1e-6 relative. Smaller tolerances use the
+// Householder CPQR (cpqr.cuh).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace hssmf_b200 {
+
+  struct GramTask {
+    double* G;       // n x n working Gram matrix (ld n), destroyed
+    double* L;       // n x kcap Cholesky columns by original index (ld n), zeroed
+    double* dg;      // n residual norms^2
+    int* flag;       // n pivoted flags (zeroed)
+    int* orig_at;    // n: original column at each CPQR position (the ID perm)
+    int* pos_of;     // n: inverse of orig_at
+    int* state;      // [k, stopped, certified]
+    double* r11;     // first pivot norm
+    int n, kmax_dim, kmax, kcap;
+  };
+
+  // runs the factorization of all tasks; returns per task (rank, certified)
+  // (one host sync per panel of nb steps to retire finished tasks)
+  void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
+                         cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
+                         double* flops = nullptr);
+
+}  // namespace hssmf_b200

@@ -11,6 +11,7 @@
 #include "front.cuh"
 #include "gemm.cuh"
 #include "hss_kernels.cuh"
+#include "gram_id.cuh"
 #include "rng.cuh"
 
 namespace hssmf_b200 {
@@ -129,6 +130,8 @@ namespace hssmf_b200 {
     long long ldD = 0;
     DBuf<double> B12, B21;
     Grow slr, slc, sr, sc, rr, rc;
+    DBuf<double> G0r, G0c;  // Gram matrices of the local samples (Gram ID route)
+    int gram_cols = 0;      // sample columns folded into G0r/G0c
     DBuf<double> dr, dc;
     // ULV
     DBuf<double> G;
@@ -160,6 +163,7 @@ namespace hssmf_b200 {
     DBuf<double> scale, one;
     int d = 0, rounds = 0;
     double flops = 0;
+    bool gram = false;  // ID route: Gram / pivoted Cholesky (eps >= 1e-5) or Householder
     // top factorization
     bool partial = false;
     DBuf<double> Z;
@@ -253,6 +257,11 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaMemcpyAsync(one.p, &h1, sizeof(double), cudaMemcpyHostToDevice, s));
       d = std::min(o.d0, o.max_rank + o.p);
       rounds = 0;
+      gram = o.eps >= 1e-5;
+      if (const char* e = getenv("HSSMF_ID_ALGO")) {
+        if (!strcmp(e, "householder")) gram = false;
+        if (!strcmp(e, "gram")) gram = true;
+      }
       if (m == 0) {
         nodes[root].state = DONE;
         return;
@@ -469,18 +478,103 @@ namespace hssmf_b200 {
       index_copy_run(cp, s);
       gg.run(s);
       flops += gg.flops;
+      if (!gram) return;
+      // G0 += S_new S_new^T  (only the appended sample columns)
+      std::vector<GemmProblem> gp;
+      for (int n : act) {
+        auto& N = nodes[n];
+        const int mt = N.mt, cb0 = N.gram_cols, nc = d - cb0;
+        if (nc <= 0 || !mt) continue;
+        if (!N.G0r.p) {
+          N.G0r.alloc((size_t)mt * mt, s);
+          N.G0c.alloc((size_t)mt * mt, s);
+          N.G0r.zero();
+          N.G0c.zero();
+        }
+        gp.push_back({N.slr.col(cb0), N.slr.col(cb0), N.G0r.p, mt, mt, nc, mt, mt, mt});
+        gp.push_back({N.slc.col(cb0), N.slc.col(cb0), N.G0c.p, mt, mt, nc, mt, mt, mt});
+        N.gram_cols = d;
+      }
+      flops += gemm_flops(gp);
+      gemm_run_host(gp, 'N', 'T', 1.0, 1.0, s);
     }
 
     // IDs of the local samples; certified nodes become Done
     // (compress_pass, hss_compress.hpp:250-297)
+    // Gram route (gram_id.cuh): residual norms / pivots from the pivoted
+    // Cholesky of the incrementally accumulated Gram matrices; R = L^T is
+    // scattered into position order for the common ID-coefficient solve
+    void gram_ids(const std::vector<int>& act, int cap_id, double abs_tol,
+                  std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
+                  std::vector<DBuf<int>>& perm, DBuf<int>& outs, std::vector<CpqrTask>& tasks,
+                  std::vector<int>& ho) {
+      const int na = (int)act.size(), nt = 2 * na;
+      std::vector<DBuf<double>> Gw(nt), L(nt), dg(nt);
+      std::vector<DBuf<int>> flag(nt), pos(nt);
+      DBuf<int> st;
+      DBuf<double> r11;
+      st.alloc(3 * nt, s);
+      r11.alloc(nt, s);
+      std::vector<GramTask> gt(nt);
+      for (int q = 0; q < na; q++) {
+        auto& N = nodes[act[q]];
+        const int mt = N.mt;
+        for (int side = 0; side < 2; side++) {
+          const int t = 2 * q + side;
+          const DBuf<double>& G0 = side ? N.G0c : N.G0r;
+          const int kdim = std::min(d, mt), kmax = std::min(kdim, std::max(cap_id, 0));
+          const int kcap = ((kmax + 31) / 32) * 32 + 32;
+          Gw[t].alloc((size_t)mt * mt + 1, s);
+          if (mt)
+            HSSMF_CUDA(cudaMemcpyAsync(Gw[t].p, G0.p, (size_t)mt * mt * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s));
+          L[t].alloc((size_t)mt * kcap + 1, s);
+          L[t].zero();
+          dg[t].alloc(mt + 1, s);
+          flag[t].alloc(mt + 1, s);
+          pos[t].alloc(mt + 1, s);
+          perm[t].alloc(mt + 1, s);
+          gt[t] = {Gw[t].p, L[t].p, dg[t].p, flag[t].p, perm[t].p, pos[t].p, st.p + 3 * t,
+                   r11.p + t, mt, kdim, kmax, kcap};
+        }
+      }
+      std::vector<int> rk, ce;
+      {
+        Ph ph_(this, 3);
+        gram_cholesky_run(gt, o.eps, abs_tol, s, rk, ce, &flops);
+      }
+      ho.assign(2 * nt, 0);
+      std::vector<CopyDesc> rc;
+      for (int t = 0; t < nt; t++) {
+        ho[2 * t] = rk[t];
+        ho[2 * t + 1] = ce[t];
+        const int mt = gt[t].n, k = rk[t];
+        Y[t].alloc((size_t)std::max(k, 1) * mt + 1, s);
+        X[t].alloc((size_t)k * std::max(mt - k, 0) + 1, s);
+        if (k) rc.push_back(cd(L[t].p, mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
+                               nullptr, 0, k, mt));
+        tasks[t] = {Y[t].p, k, mt, std::max(k, 1), std::max(cap_id, 0), perm[t].p, X[t].p,
+                    outs.p + 2 * t};
+      }
+      index_copy_run(rc, s);
+      HSSMF_CUDA(cudaMemcpyAsync(outs.p, ho.data(), ho.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      HSSMF_CUDA(cudaStreamSynchronize(s));
+    }
+
     void id_batch(const std::vector<int>& act, int cap_id, double abs_tol, int& fail) {
       const int na = (int)act.size();
       std::vector<DBuf<double>> Y(2 * na), X(2 * na);
       std::vector<DBuf<int>> perm(2 * na);
       DBuf<int> outs;
       outs.alloc(4 * na, s);
-      std::vector<CopyDesc> tr;
       std::vector<CpqrTask> tasks(2 * na);
+      std::vector<int> ho(4 * na);
+      if (gram) {
+        gram_ids(act, cap_id, abs_tol, Y, X, perm, outs, tasks, ho);
+        id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho);
+        return;
+      }
+      std::vector<CopyDesc> tr;
       int max_n = 0;
       for (int q = 0; q < na; q++) {
         auto& N = nodes[act[q]];
@@ -507,8 +601,6 @@ namespace hssmf_b200 {
         Ph ph_(this, 3);
         cpqr_run(dt.p, (int)tasks.size(), d, max_n, o.eps, abs_tol, s);
       }
-      Ph ph4(this, 4);
-      std::vector<int> ho(4 * na);
       HSSMF_CUDA(cudaMemcpyAsync(ho.data(), outs.p, ho.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
       HSSMF_CUDA(cudaStreamSynchronize(s));
       for (int q = 0; q < 2 * na; q++) {
@@ -516,6 +608,16 @@ namespace hssmf_b200 {
         flops += 2.0 * d * mt;
         for (int j = 0; j < k; j++) flops += 4.0 * (d - j) * (mt - j);
       }
+      id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho);
+    }
+
+    void id_finalize(const std::vector<int>& act, int cap_id, int& fail,
+                     std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
+                     std::vector<DBuf<int>>& perm, std::vector<CpqrTask>& tasks,
+                     std::vector<int>& ho) {
+      Ph ph4(this, 4);
+      const int na = (int)act.size();
+      (void)Y;
       std::vector<int> okq;
       std::vector<CpqrTask> solve_tasks;
       int max_rank_ok = 0, max_cols = 0;
@@ -636,6 +738,8 @@ namespace hssmf_b200 {
         auto& N = nodes[act[q]];
         N.slr.release();
         N.slc.release();
+        N.G0r.free();
+        N.G0c.free();
         N.state = DONE;
       }
     }
