@@ -30,6 +30,7 @@ namespace hssmf_b200 {
         if (__ldg(prefix + mid) <= tile) lo = mid; else hi = mid - 1;
       }
       const GemmProblem P = probs[lo];
+      if (P.skip && __ldcg(P.skip)) return;
       const int tiles_m = (P.m + BM - 1) / BM;
       const int t = tile - __ldg(prefix + lo);
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;

@@ -19,6 +19,7 @@ namespace hssmf_b200 {
     double* C;
     int m, n, k;
     int lda, ldb, ldc;
+    const int* skip = nullptr;  // optional device flag: problem is a no-op when *skip != 0
   };
 
   // device-resident batch: descriptors + tile prefix (prefix[p] = first tile

@@ -11,7 +11,7 @@ namespace hssmf_b200 {
 
   namespace {
     namespace cg = cooperative_groups;
-    constexpr int GT = 256, GW = GT / 32, NB = 32;
+    constexpr int GT = 256, GW = GT / 32, NB = kGramNB;
 
     struct Cand {
       double v;
@@ -188,12 +188,14 @@ namespace hssmf_b200 {
     int CL = 1;
     while (CL < 16 && max_n > CL * 256) CL *= 2;
     GramTask* d = nullptr;
-    int* st = nullptr;
     HSSMF_CUDA(cudaMallocAsync((void**)&d, nt * sizeof(GramTask), s));
     HSSMF_CUDA(cudaMemcpyAsync(d, tasks.data(), nt * sizeof(GramTask), cudaMemcpyHostToDevice, s));
     std::vector<int> hst(3 * nt);
-    std::vector<char> active(nt, 1);
-    for (int k0 = 0;; k0 += NB) {
+    int kmax = 0;
+    for (const auto& t : tasks) kmax = std::max(kmax, t.kmax);
+    // all panels are queued without host round trips: a finished task's
+    // panel kernel returns at once and its trailing GEMM is skipped on device
+    for (int k0 = 0; k0 <= kmax; k0 += NB) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(nt * CL);
       cfg.blockDim = dim3(GT);
@@ -208,31 +210,28 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel_kernel, (const GramTask*)d, k0, NB, eps,
                                     abs_tol, CL, k0 == 0 ? 1 : 0));
       HSSMF_LAUNCH_CHECK();
-      for (int t = 0; t < nt; t++)
-        HSSMF_CUDA(cudaMemcpyAsync(&hst[3 * t], tasks[t].state, 3 * sizeof(int),
-                                   cudaMemcpyDeviceToHost, s));
-      HSSMF_CUDA(cudaStreamSynchronize(s));
-      // trailing (SYRK-like) update of the Gram matrices still running
+      if (k0 + NB > kmax) break;
       std::vector<GemmProblem> p;
       for (int t = 0; t < nt; t++) {
-        if (hst[3 * t + 1]) {
-          active[t] = 0;
-          continue;
-        }
         const auto& T = tasks[t];
-        p.push_back({T.L + (size_t)k0 * T.n, T.L + (size_t)k0 * T.n, T.G, T.n, T.n, NB, T.n, T.n,
-                     T.n});
+        if (k0 > T.kmax) continue;
+        GemmProblem g{T.L + (size_t)k0 * T.n, T.L + (size_t)k0 * T.n, T.G, T.n, T.n, NB, T.n,
+                      T.n, T.n};
+        g.skip = T.state + 1;
+        p.push_back(g);
       }
-      if (p.empty()) break;
       if (flops) *flops += gemm_flops(p);
       gemm_run_host(p, 'N', 'T', -1.0, 1.0, s);
     }
+    for (int t = 0; t < nt; t++)
+      HSSMF_CUDA(cudaMemcpyAsync(&hst[3 * t], tasks[t].state, 3 * sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    HSSMF_CUDA(cudaStreamSynchronize(s));
     for (int t = 0; t < nt; t++) {
       rank[t] = hst[3 * t];
       cert[t] = hst[3 * t + 2];
     }
     HSSMF_CUDA(cudaFreeAsync(d, s));
-    (void)st;
   }
 
 }  // namespace hssmf_b200

@@ -24,6 +24,8 @@
 
 namespace hssmf_b200 {
 
+  constexpr int kGramNB = 64;  // panel width (steps between trailing updates)
+
   struct GramTask {
     double* G;       // n x n working Gram matrix (ld n), destroyed
     double* L;       // n x kcap Cholesky columns by original index (ld n), zeroed

@@ -523,7 +523,7 @@ namespace hssmf_b200 {
           const int t = 2 * q + side;
           const DBuf<double>& G0 = side ? N.G0c : N.G0r;
           const int kdim = std::min(d, mt), kmax = std::min(kdim, std::max(cap_id, 0));
-          const int kcap = ((kmax + 31) / 32) * 32 + 32;
+          const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
           Gw[t].alloc((size_t)mt * mt + 1, s);
           if (mt)
             HSSMF_CUDA(cudaMemcpyAsync(Gw[t].p, G0.p, (size_t)mt * mt * sizeof(double),
