@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DEFAULT_CONFIG = "c5_mf"
+DEFAULT_CONFIG = "c5"
 
 
 def dense_flops(ns, nu):
@@ -133,14 +133,42 @@ def measured_peaks(torch, dev):
 
 
 # ------------------------------------------------------ reference sample ---
-def subtree_sample(op, target_flops):
-    """pick the leftmost subtree whose dense-front flops approach target_flops
+def front_model_flops(op, cfg):
+    """per-front cost by the reference's own estimate (multifrontal.hpp:391-396:
+    dense 2ns^3/3 + 2ns^2 nu + 2 ns nu^2, HSS 4 m^2 d + 8 m r^2), with the HSS
+    fronts' (rank, d_final) from tests/golden/<workload>_front_model.npz (a
+    committed record of a full run) when the workload has HSS fronts"""
+    t = op.t
+    ns = (t.sep_end - t.sep_begin).astype(np.int64)
+    nu = np.diff(t.upd_ptr).astype(np.int64)
+    fl = dense_flops(ns, nu)
+    path = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_front_model.npz")
+    if os.path.exists(path):
+        g = np.load(path)
+        if len(g["rank"]) == len(fl):
+            h = g["type"] == 1
+            m = (ns + nu).astype(np.float64)
+            fl = np.where(h, 4 * m ** 2 * g["d_final"] + 8 * m * g["rank"].astype(np.float64) ** 2,
+                          fl)
+    return fl
+
+
+def subtree_sample(op, target_flops, cfg=None):
+    """pick the leftmost subtree whose modelled cost approaches target_flops
     and build its principal submatrix + relabelled tree (a self-contained
     subproblem of the same workload); returns (pieces, sample_flops, desc)"""
     t = op.t
     ns = (t.sep_end - t.sep_begin).astype(np.int64)
     nu = np.diff(t.upd_ptr).astype(np.int64)
+    model = None
     fl = dense_flops(ns, nu)
+    if cfg is not None:
+        path = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_front_model.npz")
+        if os.path.exists(path):
+            g = np.load(path)
+            if len(g["rank"]) == len(fl):
+                model = {k: g[k] for k in ("type", "rank", "d_final")}
+                fl = front_model_flops(op, cfg)
     nn = t.size()
     sub = fl.copy()
     lo = np.arange(nn)
@@ -186,9 +214,16 @@ def subtree_sample(op, target_flops):
                   upd_ptr=up, upd_ind=np.concatenate(upd) if upd else np.zeros(0, np.int32))
     sns = (pieces["sep_end"] - pieces["sep_begin"]).astype(np.int64)
     snu = np.diff(up).astype(np.int64)
-    sfl = float(dense_flops(sns, snu).sum())
+    sfl_f = dense_flops(sns, snu)
+    if model is not None:  # HSS fronts of the sample at their own (truncated) size
+        h = model["type"][ids] == 1
+        sm = (sns + snu).astype(np.float64)
+        sfl_f = np.where(h, 4 * sm ** 2 * model["d_final"][ids] +
+                         8 * sm * model["rank"][ids].astype(np.float64) ** 2, sfl_f)
+    sfl = float(sfl_f.sum())
     desc = (f"subtree of front {s} (level {t.level[s]}, {len(ids)} fronts, n={end - start}) "
-            f"= {sfl / fl.sum():.4f} of the workload's dense-front flops")
+            f"= {sfl / fl.sum():.4f} of the workload by the reference's per-front cost model "
+            f"(multifrontal.hpp:391-396)")
     return pieces, sfl, float(fl.sum()), desc
 
 
@@ -221,7 +256,7 @@ def reference_arm(args, cfg, op):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops)
+    pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
     thr = cpu_threads()
     for _ in range(args.warmup):
         run_reference_sample(cfg, pieces, thr)
@@ -255,7 +290,7 @@ def config_json(cfg, op, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
@@ -394,7 +429,7 @@ def main():
         try:
             from oracle import ref
             if ref.available():
-                pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops)
+                pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
                 thr = cpu_threads()
                 t = run_reference_sample(cfg, pieces, thr)
                 line["cpu_baseline"] = {"value": t * tfl / sfl, "unit": "s", "cores": thr,

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--save-model", default=None,
+                    help="write per-front (type, rank, d_final) for bench.py's CPU extrapolation")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     out = {"config": a.config}
@@ -70,6 +72,12 @@ def main():
                device_gb=m.device_bytes() / 1e9)
     if a.profile:
         out["kernels"] = m.kernel_stats()
+    if a.save_model:
+        dfin = np.zeros(len(m.type), np.int32)
+        for i in np.nonzero(m.type == 1)[0]:
+            dfin[i] = m.front_hss(int(i))[3]
+        np.savez_compressed(a.save_model, type=m.type, rank=m.rank, d_final=dfin,
+                            level=m.level, dim=m.dim)
     gp = os.path.join(ROOT, "tests", "golden", f"ref_{a.config}.npz")
     if os.path.exists(gp):
         g = np.load(gp)
