@@ -18,8 +18,8 @@
 using namespace hssmf_b200;
 
 namespace hssmf_b200 {
-  long long& launch_counter() {
-    static long long c = 0;
+  std::atomic<long long>& launch_counter() {
+    static std::atomic<long long> c{0};
     return c;
   }
 }  // namespace hssmf_b200
@@ -81,7 +81,7 @@ namespace {
 
 extern "C" {
 
-long long hssmf_launch_count(void) { return launch_counter(); }
+long long hssmf_launch_count(void) { return launch_counter().load(); }
 
 const char* hssmf_version(void) { return "hssmf_b200 0.1 (sm_100a)"; }
 

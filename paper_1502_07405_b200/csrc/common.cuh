@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -23,7 +24,7 @@ namespace hssmf_b200 {
 
   // host-side count of kernel launches issued by this library (bench.py
   // reports it as gpu_launches)
-  long long& launch_counter();
+  std::atomic<long long>& launch_counter();
 #define HSSMF_LAUNCH_CHECK()                 \
   do {                                       \
     ++::hssmf_b200::launch_counter();        \

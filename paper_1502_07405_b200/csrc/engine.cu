@@ -11,8 +11,11 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <thread>
 
 #include "common.cuh"
 #include "front.cuh"
@@ -183,7 +186,18 @@ namespace hssmf_b200 {
       if (scratch.bytes < n * sizeof(int)) scratch.alloc(std::max<size_t>(n * sizeof(int), 4096));
       return scratch.as<int>();
     }
-    void factor_hss_front(int i, int level);
+    struct HssResult {
+      std::unique_ptr<HssMatrixDev> hss;
+      bool fallback = false;
+      FrontDev front{};
+      DevMem keep, piv;
+      int singular_col = -1;
+      std::string msg, error;
+    };
+    std::vector<cudaStream_t> hstreams;  // concurrent HSS fronts of one level
+    double* assemble_hss_front(int i);
+    HssResult compress_hss_front(int i, double* F, cudaStream_t st);
+    void factor_hss_level(const std::vector<int>& lst);
   };
 
   Engine::Engine(int device) : d_(new Impl), device_(device) {
@@ -197,11 +211,23 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
     unsigned long long thr = ~0ull;
     HSSMF_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+    int nw = 8;
+    if (const char* e = getenv("HSSMF_HSS_STREAMS")) nw = std::max(1, atoi(e));
+    for (int w = 0; w < nw; w++) {
+      cudaStream_t st;
+      HSSMF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      d_->hstreams.push_back(st);
+    }
   }
 
   Engine::~Engine() {
     cudaSetDevice(device_);
+    auto hs = d_->hstreams;
     d_.reset();
+    for (auto st : hs) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
     if (stream_) cudaStreamDestroy(stream_);
   }
 
@@ -461,16 +487,15 @@ namespace hssmf_b200 {
     factored_ = false;
   }
 
-  // one HSS front (factor_front_hss, multifrontal.hpp:348-377) with the
-  // rank-guard fallback of factor_front (multifrontal.hpp:414-421)
-  void Engine::Impl::factor_hss_front(int i, int level) {
+  // dense assembly of HSS front i in HBM (assemble_dense semantics,
+  // multifrontal.hpp:141-170) on the engine stream; returns the m x m front
+  double* Engine::Impl::assemble_hss_front(int i) {
     const auto& fn = t.nodes[i];
     auto& h = hf[i];
     const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
     double* F = nullptr;
     HSSMF_CUDA(cudaMallocAsync((void**)&F, (size_t)m * m * sizeof(double) + 8, s));
     HSSMF_CUDA(cudaMemsetAsync(F, 0, (size_t)m * m * sizeof(double), s));
-    // dense assembly of the front in HBM: temporary descriptor over F
     FrontDev view = h;
     view.P = F;
     view.U = F + (size_t)ns * m;
@@ -482,19 +507,31 @@ namespace hssmf_b200 {
     hf[i] = view;
     upload_front(i);
     std::vector<int> one_id{i};
-    std::vector<long long> cp0{0, fn.child0 >= 0 ? t.nodes[fn.child0].nu() : 0};
-    std::vector<long long> cp1{0, fn.child1 >= 0 ? t.nodes[fn.child1].nu() : 0};
+    std::vector<long long> cp{0, fn.child0 >= 0 ? t.nodes[fn.child0].nu() : 0, 0,
+                              fn.child1 >= 0 ? t.nodes[fn.child1].nu() : 0};
     HSSMF_CUDA(cudaMemcpyAsync(scr, one_id.data(), sizeof(int), cudaMemcpyHostToDevice, s));
     long long* dcp = nullptr;
     HSSMF_CUDA(cudaMallocAsync((void**)&dcp, 4 * sizeof(long long), s));
-    HSSMF_CUDA(cudaMemcpyAsync(dcp, cp0.data(), 2 * sizeof(long long), cudaMemcpyHostToDevice, s));
-    HSSMF_CUDA(cudaMemcpyAsync(dcp + 2, cp1.data(), 2 * sizeof(long long), cudaMemcpyHostToDevice, s));
+    HSSMF_CUDA(cudaMemcpyAsync(dcp, cp.data(), 4 * sizeof(long long), cudaMemcpyHostToDevice, s));
     const FrontDev* Fd = d_fronts.as<FrontDev>();
     DenseKernels::assemble_sparse(Fd, scr, 1, d_ptr.as<int>(), d_ind.as<int>(), d_val.as<double>(), s);
-    DenseKernels::extend_add(Fd, scr, 1, 0, dcp, cp0[1], s);
-    DenseKernels::extend_add(Fd, scr, 1, 1, dcp + 2, cp1[1], s);
+    DenseKernels::extend_add(Fd, scr, 1, 0, dcp, cp[1], s);
+    DenseKernels::extend_add(Fd, scr, 1, 1, dcp + 2, cp[3], s);
     HSSMF_CUDA(cudaFreeAsync(dcp, s));
+    HSSMF_CUDA(cudaStreamSynchronize(s));
+    hf[i] = hf0[i];
+    upload_front(i);
+    return F;
+  }
 
+  // compression + ULV + densified update of an assembled HSS front on its own
+  // stream (factor_front_hss, multifrontal.hpp:348-377). Runs on a worker
+  // thread; the rank-guard fallback (multifrontal.hpp:414-421) factors the
+  // assembled front densely in place.
+  Engine::Impl::HssResult Engine::Impl::compress_hss_front(int i, double* F, cudaStream_t st) {
+    HssResult res;
+    const auto& fn = t.nodes[i];
+    const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
     auto tree = front_cluster_tree(ns, nu, opt.leaf);
     std::vector<long long> seeds(m);
     for (int l = 0; l < m; l++) seeds[l] = l < ns ? fn.sep_begin + l : fn.upd[l - ns];
@@ -504,7 +541,7 @@ namespace hssmf_b200 {
     ho.dd = opt.dd;
     ho.p = opt.p;
     ho.max_rank = std::min(opt.resolved_max_rank(t.n), m);
-    auto H = std::make_unique<HssMatrixDev>(s);
+    auto H = std::make_unique<HssMatrixDev>(st);
     bool fallback = false;
     try {
       H->compress(F, m, tree, seeds, ho);
@@ -513,51 +550,97 @@ namespace hssmf_b200 {
     } catch (const HssRankError&) {
       fallback = true;
     } catch (const HssSingular& e) {
-      HSSMF_CUDA(cudaFreeAsync(F, s));
-      hf[i] = hf0[i];
-      upload_front(i);
-      throw SolverFailure(3, i, e.column,
-                          "front " + std::to_string(i) + ": " + e.what());
+      HSSMF_CUDA(cudaFreeAsync(F, st));
+      res.singular_col = e.column;
+      res.msg = e.what();
+      return res;
     }
     if (!fallback) {
       H->drop_dense();
-      HSSMF_CUDA(cudaFreeAsync(F, s));
-      hf[i] = hf0[i];
-      hf[i].hss = 1;
-      upload_front(i);
-      hss[i] = std::move(H);
-      return;
+      HSSMF_CUDA(cudaFreeAsync(F, st));
+      HSSMF_CUDA(cudaStreamSynchronize(st));
+      res.hss = std::move(H);
+      return res;
     }
-    // rank guard tripped: densify this front (factor_front_dense on the
-    // assembled front); F becomes the front's persistent storage
     H.reset();
-    DevMem keep;
-    keep.p = F;  // adopt (freed with the engine's fallback list)
-    keep.bytes = (size_t)m * m * sizeof(double);
-    DevMem piv;
-    piv.alloc(2 * (size_t)ns * sizeof(int) + 8);
-    FrontDev f = view;
+    res.keep.p = F;
+    res.keep.bytes = (size_t)m * m * sizeof(double);
+    res.piv.alloc(2 * (size_t)ns * sizeof(int) + 8);
+    FrontDev f = hf0[i];
+    f.P = F;
+    f.U = F + (size_t)ns * m;
+    f.C = F + ns + (size_t)ns * m;
+    f.ldu = m;
+    f.ldc = m;
     f.hss = 0;
-    f.piv = piv.as<int>();
-    f.perm = piv.as<int>() + ns;
-    auto st = partial_lu_dynamic({f}, s);
-    if (st[0] >= 0)
-      throw SolverFailure(3, i, st[0],
-                          "front " + std::to_string(i) + ": exactly singular, zero pivot column " +
-                              std::to_string(st[0]));
-    // hand the Schur complement to the parent's transient slot (ld nu)
+    f.piv = res.piv.as<int>();
+    f.perm = res.piv.as<int>() + ns;
+    auto stt = partial_lu_dynamic({f}, st);
+    if (stt[0] >= 0) {
+      res.singular_col = stt[0];
+      res.msg = "exactly singular, zero pivot column " + std::to_string(stt[0]);
+      return res;
+    }
     if (nu)
       HSSMF_CUDA(cudaMemcpy2DAsync(hf0[i].C, (size_t)nu * sizeof(double), f.C,
                                    (size_t)m * sizeof(double), (size_t)nu * sizeof(double), nu,
-                                   cudaMemcpyDeviceToDevice, s));
+                                   cudaMemcpyDeviceToDevice, st));
+    HSSMF_CUDA(cudaStreamSynchronize(st));
     f.C = hf0[i].C;
     f.ldc = nu;
-    hf[i] = f;
-    upload_front(i);
-    fallback_mem.push_back(std::move(keep));
-    fallback_mem.push_back(std::move(piv));
-    (void)level;
+    res.fallback = true;
+    res.front = f;
+    return res;
   }
+
+  // the HSS fronts of one tree level: serial assembly, concurrent compression
+  // on a pool of streams / host threads, serial bookkeeping
+  void Engine::Impl::factor_hss_level(const std::vector<int>& lst) {
+    if (lst.empty()) return;
+    std::vector<double*> F(lst.size());
+    for (size_t q = 0; q < lst.size(); q++) F[q] = assemble_hss_front(lst[q]);
+    const int nw = (int)std::min<size_t>(lst.size(), hstreams.size());
+    std::vector<HssResult> res(lst.size());
+    std::atomic<int> next{0};
+    int dev = 0;
+    HSSMF_CUDA(cudaGetDevice(&dev));
+    auto work = [&](int w) {
+      cudaSetDevice(dev);
+      for (int q = next++; q < (int)lst.size(); q = next++) {
+        try {
+          res[q] = compress_hss_front(lst[q], F[q], hstreams[w]);
+        } catch (const std::exception& e) {
+          res[q].error = e.what();
+        }
+      }
+    };
+    if (nw <= 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int w = 0; w < nw; w++) th.emplace_back(work, w);
+      for (auto& x : th) x.join();
+    }
+    for (size_t q = 0; q < lst.size(); q++) {
+      const int i = lst[q];
+      auto& r = res[q];
+      if (!r.error.empty()) throw CudaError("hss front " + std::to_string(i) + ": " + r.error);
+      if (r.singular_col >= 0)
+        throw SolverFailure(3, i, r.singular_col, "front " + std::to_string(i) + ": " + r.msg);
+      if (r.hss) {
+        r.hss->set_stream(s);
+        hss[i] = std::move(r.hss);
+        hf[i] = hf0[i];
+        hf[i].hss = 1;
+      } else {
+        hf[i] = r.front;
+        fallback_mem.push_back(std::move(r.keep));
+        fallback_mem.push_back(std::move(r.piv));
+      }
+      upload_front(i);
+    }
+  }
+
 
   void Engine::factor() {
     HSSMF_CUDA(cudaSetDevice(device_));
@@ -610,12 +693,12 @@ namespace hssmf_b200 {
         D.launch(K_GEMM_SCHUR, P.flops_schur, 0,
                  [&] { gemm_run(P.schur, 'N', 'N', -1.0, 1.0, stream_); });
       }
-      for (int i : P.hss) {
+      if (!P.hss.empty()) {
+        HSSMF_CUDA(cudaStreamSynchronize(stream_));
+        D.launch(K_HSS, 0, 0, [&] { D.factor_hss_level(P.hss); });
         double hfl = 0;
-        D.launch(K_HSS, 0, 0, [&] {
-          D.factor_hss_front(i, L);
-          if (D.hss[i]) hfl = D.hss[i]->flops();
-        });
+        for (int i : P.hss)
+          if (D.hss[i]) hfl += D.hss[i]->flops();
         if (profile_ && !D.evs.empty()) D.evs.back().flops = hfl;
       }
     }

@@ -1260,6 +1260,10 @@ namespace hssmf_b200 {
     d_->Sr.release();
     d_->Sc.release();
   }
+  void HssMatrixDev::set_stream(cudaStream_t s) {
+    d_->collect_phases();
+    d_->s = s;
+  }
   void HssMatrixDev::solve_full(double* x) { d_->solve_full(x); }
   void HssMatrixDev::partial_forward(const double* b1, double* bupd) { d_->partial_forward(b1, bupd); }
   void HssMatrixDev::partial_backward(double* x1, const double* x2) { d_->partial_backward(x1, x2); }

@@ -81,6 +81,8 @@ namespace hssmf_b200 {
     void ulv_partial(double* update, long long ldu);
     // release the reference to A (front storage about to be freed)
     void drop_dense();
+    // stream used by later solves (factorization ran on its own stream)
+    void set_stream(cudaStream_t s);
 
     // solves (single right-hand side, device vectors)
     void solve_full(double* x);  // in place, length m
