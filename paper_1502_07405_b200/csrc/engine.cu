@@ -34,6 +34,16 @@ namespace hssmf_b200 {
       DevMem() = default;
       DevMem(const DevMem&) = delete;
       DevMem(DevMem&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+      DevMem& operator=(DevMem&& o) noexcept {
+        if (this != &o) {
+          free();
+          p = o.p;
+          bytes = o.bytes;
+          o.p = nullptr;
+          o.bytes = 0;
+        }
+        return *this;
+      }
       void alloc(size_t b) {
         free();
         if (b) HSSMF_CUDA(cudaMalloc(&p, b));
