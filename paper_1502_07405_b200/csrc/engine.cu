@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -614,14 +616,22 @@ namespace hssmf_b200 {
     std::atomic<int> next{0};
     int dev = 0;
     HSSMF_CUDA(cudaGetDevice(&dev));
+    static const bool dbg = getenv("HSSMF_DEBUG") != nullptr;
+    auto now = [] {
+      return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t0 = now();
+    std::vector<double> tq(lst.size());
     auto work = [&](int w) {
       cudaSetDevice(dev);
       for (int q = next++; q < (int)lst.size(); q = next++) {
+        const double a = now();
         try {
           res[q] = compress_hss_front(lst[q], F[q], hstreams[w]);
         } catch (const std::exception& e) {
           res[q].error = e.what();
         }
+        tq[q] = now() - a;
       }
     };
     if (nw <= 1) {
@@ -630,6 +640,15 @@ namespace hssmf_b200 {
       std::vector<std::thread> th;
       for (int w = 0; w < nw; w++) th.emplace_back(work, w);
       for (auto& x : th) x.join();
+    }
+    if (dbg) {
+      fprintf(stderr, "[hssmf] level: %zu HSS fronts, wall %.3f s\n", lst.size(), now() - t0);
+      for (size_t q = 0; q < lst.size(); q++) {
+        const auto& fn = t.nodes[lst[q]];
+        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s  rounds=%d d=%d rank=%d\n",
+                lst[q], fn.m(), fn.ns(), tq[q], res[q].hss ? res[q].hss->rounds() : -1,
+                res[q].hss ? res[q].hss->d_final() : -1, res[q].hss ? res[q].hss->hss_rank() : -1);
+      }
     }
     for (size_t q = 0; q < lst.size(); q++) {
       const int i = lst[q];
