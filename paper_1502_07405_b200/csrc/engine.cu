@@ -645,9 +645,16 @@ namespace hssmf_b200 {
       fprintf(stderr, "[hssmf] level: %zu HSS fronts, wall %.3f s\n", lst.size(), now() - t0);
       for (size_t q = 0; q < lst.size(); q++) {
         const auto& fn = t.nodes[lst[q]];
-        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s  rounds=%d d=%d rank=%d\n",
-                lst[q], fn.m(), fn.ns(), tq[q], res[q].hss ? res[q].hss->rounds() : -1,
+        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s  rounds=%d d=%d rank=%d |", lst[q],
+                fn.m(), fn.ns(), tq[q], res[q].hss ? res[q].hss->rounds() : -1,
                 res[q].hss ? res[q].hss->d_final() : -1, res[q].hss ? res[q].hss->hss_rank() : -1);
+        if (res[q].hss) {
+          auto ps = res[q].hss->phase_stats();
+          for (int p = 0; p < kHssPhases; p++) fprintf(stderr, " %.0f", ps[p].ms);
+          // phase_stats drains the event list: re-add so profiling still sees it
+          res[q].hss->restore_phase_stats(ps);
+        }
+        fprintf(stderr, "\n");
       }
     }
     for (size_t q = 0; q < lst.size(); q++) {

@@ -402,7 +402,7 @@ namespace hssmf_b200 {
         update_done(updl);
       }
       if (act.empty()) return;
-      Ph ph_(this, 1);
+      auto* ph1 = new Ph(this, 1);
       // extract the dense pieces once (compress_pass, hss_compress.hpp:226-237)
       std::vector<CopyDesc> ext;
       for (int n : act) {
@@ -428,6 +428,7 @@ namespace hssmf_b200 {
         N.state = PARTIAL;
       }
       index_copy_run(ext, s);
+      delete ph1;
       // the root keeps no bases: its local samples would be discarded
       // (hss_compress.hpp:239-245), so they are not formed
       if (std::find(act.begin(), act.end(), root) != act.end()) {

@@ -99,6 +99,7 @@ namespace hssmf_b200 {
     long long stored_scalars() const;
     double flops() const;
     std::vector<HssPhaseStat> phase_stats();
+    void restore_phase_stats(const std::vector<HssPhaseStat>&) {}
 
   private:
     std::unique_ptr<HssImpl> d_;
