@@ -241,7 +241,10 @@ def run_reference_sample(cfg, pieces, threads):
     F = ref.Factors(o, eps=cfg.eps, ls=cfg.ls, leaf=cfg.leaf, d0=cfg.d0, dd=cfg.dd, p=cfg.p,
                     min_hss=cfg.min_hss, mode=mode)
     F.solve(b)
-    return time.perf_counter() - t0
+    t = time.perf_counter() - t0
+    # the reference's own per-front cost model of what it actually did on the
+    # sample (FrontStat.flops, multifrontal.hpp:432-445)
+    return t, float(F.flops.astype(np.float64).sum()), int(F.hss_fronts)
 
 
 def cpu_threads():
@@ -260,8 +263,10 @@ def reference_arm(args, cfg, op):
     thr = cpu_threads()
     for _ in range(args.warmup):
         run_reference_sample(cfg, pieces, thr)
-    ts = [run_reference_sample(cfg, pieces, thr) for _ in range(args.steps)]
-    t = float(np.mean(ts))
+    runs = [run_reference_sample(cfg, pieces, thr) for _ in range(args.steps)]
+    t = float(np.mean([r[0] for r in runs]))
+    sfl = runs[0][1]
+    desc += f", {runs[0][2]} HSS fronts in the sample"
     scaled = t * tfl / sfl
     line = {
         "metric": METRIC, "value": scaled, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
@@ -386,6 +391,9 @@ def main():
     d2h = int(xh.nbytes)
 
     # per-kernel-class profile pass (events around each launch)
+    # HSS fronts of a level normally run concurrently on several streams; the
+    # profiled step runs them one at a time so per-class device times add up
+    os.environ["HSSMF_HSS_STREAMS"] = "1"
     m = P.mf_factor(op.a, op.t, opts, device=local)
     m.set_profile(True)
     m.reset_kernel_stats()
@@ -393,6 +401,9 @@ def main():
     m.solve_device(x_dev.data_ptr(), n, 1)
     ks = m.kernel_stats()
     m.set_profile(False)
+    os.environ.pop("HSSMF_HSS_STREAMS", None)
+    # hss_front_total wraps the hss_* phases: keep the leaves of the breakdown
+    ks = [k for k in ks if k["name"] != "hss_front_total"]
     tot_ms = sum(k["ms"] for k in ks) or 1.0
     top = max(ks, key=lambda k: k["ms"])
     if top["flops"] > 0:
@@ -431,11 +442,12 @@ def main():
             if ref.available():
                 pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
                 thr = cpu_threads()
-                t = run_reference_sample(cfg, pieces, thr)
+                t, sfl, nh = run_reference_sample(cfg, pieces, thr)
                 line["cpu_baseline"] = {"value": t * tfl / sfl, "unit": "s", "cores": thr,
                                         "kind": "reference",
-                                        "sample": desc + f"; measured {t:.3f} s, scaled x"
-                                                         f"{tfl / sfl:.1f} by flops"}
+                                        "sample": desc + f", {nh} HSS fronts in the sample; "
+                                                         f"measured {t:.3f} s, scaled x"
+                                                         f"{tfl / sfl:.1f} by the cost model"}
         except Exception as e:  # reported, never fatal for the GPU arm
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

@@ -611,7 +611,9 @@ namespace hssmf_b200 {
     if (lst.empty()) return;
     std::vector<double*> F(lst.size());
     for (size_t q = 0; q < lst.size(); q++) F[q] = assemble_hss_front(lst[q]);
-    const int nw = (int)std::min<size_t>(lst.size(), hstreams.size());
+    size_t width = hstreams.size();
+    if (const char* e = getenv("HSSMF_HSS_STREAMS")) width = std::max(1, atoi(e));
+    const int nw = (int)std::min<size_t>(lst.size(), std::min(width, hstreams.size()));
     std::vector<HssResult> res(lst.size());
     std::atomic<int> next{0};
     int dev = 0;
