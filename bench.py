@@ -154,22 +154,30 @@ def front_model_flops(op, cfg):
 
 
 def subtree_sample(op, target_flops, cfg=None):
-    """pick the leftmost subtree whose modelled cost approaches target_flops
-    and build its principal submatrix + relabelled tree (a self-contained
-    subproblem of the same workload); returns (pieces, sample_flops, desc)"""
+    """A bounded, self-contained piece of the same workload for the CPU
+    reference: the subtree of one front s plus a synthetic root front whose
+    separator is upd(s), over the principal submatrix on those indices. Every
+    front of the subtree then has exactly the (ns, nu) it has in the full run
+    (so HSS fronts stay HSS). s = the first HSS front of the deepest HSS level
+    when the workload has HSS fronts (front model present), else the first
+    subtree along child0 under target_flops of dense-front cost.
+    Returns (pieces, total_model_flops, description)."""
     t = op.t
     ns = (t.sep_end - t.sep_begin).astype(np.int64)
     nu = np.diff(t.upd_ptr).astype(np.int64)
-    model = None
     fl = dense_flops(ns, nu)
+    nn = t.size()
+    s = None
     if cfg is not None:
         path = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_front_model.npz")
         if os.path.exists(path):
             g = np.load(path)
             if len(g["rank"]) == len(fl):
-                model = {k: g[k] for k in ("type", "rank", "d_final")}
                 fl = front_model_flops(op, cfg)
-    nn = t.size()
+                h = np.nonzero(g["type"] == 1)[0]
+                if len(h):
+                    deepest = t.level[h].max()
+                    s = int(h[t.level[h] == deepest].min())
     sub = fl.copy()
     lo = np.arange(nn)
     for i in range(nn):  # postorder: children first
@@ -177,54 +185,63 @@ def subtree_sample(op, target_flops, cfg=None):
             if c >= 0:
                 sub[i] += sub[c]
                 lo[i] = min(lo[i], lo[c])
-    # walk down from the root along child0 until the subtree fits the target
-    s = t.root_id()
-    while sub[s] > target_flops and t.child0[s] >= 0:
-        s = t.child0[s]
+    if s is None:
+        s = t.root_id()
+        while sub[s] > target_flops and t.child0[s] >= 0:
+            s = t.child0[s]
     ids = np.arange(lo[s], s + 1)
     start = int(t.sep_begin[lo[s]])
     end = int(t.sep_end[s])
+    U = t.upd(s).astype(np.int64)
+    nin = end - start
+    n_s = nin + len(U)
+    gmap = {}
+    for k, g_ in enumerate(U):
+        gmap[int(g_)] = nin + k
+    def loc(v):
+        v = np.asarray(v, np.int64)
+        out = np.where((v >= start) & (v < end), v - start, -1)
+        if len(U):
+            pos = np.searchsorted(U, v)
+            hit = (pos < len(U)) & (U[np.minimum(pos, len(U) - 1)] == v)
+            out = np.where(hit, nin + pos, out)
+        return out
     ptr, ind, val = op.a.arrays()
+    rows = list(range(start, end)) + [int(x) for x in U]
     rows_ptr = [0]
     sind, sval = [], []
-    for r in range(start, end):
+    for r in rows:
         cols = ind[ptr[r]:ptr[r + 1]]
-        keep = (cols >= start) & (cols < end)
-        sind.append(cols[keep] - start)
+        lc = loc(cols)
+        keep = lc >= 0
+        sind.append(lc[keep])
         sval.append(val[ptr[r]:ptr[r + 1]][keep])
         rows_ptr.append(rows_ptr[-1] + int(keep.sum()))
     sptr = np.array(rows_ptr, np.int32)
     sind = np.concatenate(sind).astype(np.int32)
     sval = np.concatenate(sval)
     off = lo[s]
+    m_ids = len(ids)
     remap = lambda v: np.where(v >= 0, v - off, -1).astype(np.int32)  # noqa: E731
     par = remap(t.parent[ids])
-    par[-1] = -1
-    upd = []
-    for i in ids:
-        u = t.upd(i)
-        upd.append((u[u < end] - start).astype(np.int32))
-    up = np.zeros(len(ids) + 1, np.int32)
+    par[-1] = m_ids + 1  # the synthetic root; an empty leaf is its second child
+    upd = [loc(t.upd(i)).astype(np.int32) for i in ids] + [np.zeros(0, np.int32)] * 2
+    up = np.zeros(m_ids + 3, np.int32)
     for q, u in enumerate(upd):
         up[q + 1] = up[q] + len(u)
-    pieces = dict(n=end - start, ptr=sptr, ind=sind, val=sval,
-                  sep_begin=(t.sep_begin[ids] - start).astype(np.int32),
-                  sep_end=(t.sep_end[ids] - start).astype(np.int32),
-                  child0=remap(t.child0[ids]), child1=remap(t.child1[ids]), parent=par,
-                  upd_ptr=up, upd_ind=np.concatenate(upd) if upd else np.zeros(0, np.int32))
-    sns = (pieces["sep_end"] - pieces["sep_begin"]).astype(np.int64)
-    snu = np.diff(up).astype(np.int64)
-    sfl_f = dense_flops(sns, snu)
-    if model is not None:  # HSS fronts of the sample at their own (truncated) size
-        h = model["type"][ids] == 1
-        sm = (sns + snu).astype(np.float64)
-        sfl_f = np.where(h, 4 * sm ** 2 * model["d_final"][ids] +
-                         8 * sm * model["rank"][ids].astype(np.float64) ** 2, sfl_f)
-    sfl = float(sfl_f.sum())
-    desc = (f"subtree of front {s} (level {t.level[s]}, {len(ids)} fronts, n={end - start}) "
-            f"= {sfl / fl.sum():.4f} of the workload by the reference's per-front cost model "
-            f"(multifrontal.hpp:391-396)")
-    return pieces, sfl, float(fl.sum()), desc
+    pieces = dict(n=n_s, ptr=sptr, ind=sind, val=sval,
+                  sep_begin=np.concatenate([t.sep_begin[ids] - start, [nin, nin]]).astype(np.int32),
+                  sep_end=np.concatenate([t.sep_end[ids] - start, [nin, n_s]]).astype(np.int32),
+                  child0=np.concatenate([remap(t.child0[ids]), [-1, m_ids - 1]]).astype(np.int32),
+                  child1=np.concatenate([remap(t.child1[ids]), [-1, m_ids]]).astype(np.int32),
+                  parent=np.concatenate([par, [m_ids + 1, -1]]).astype(np.int32),
+                  upd_ptr=up, upd_ind=np.concatenate(upd))
+    desc = (f"subtree of front {s} (level {t.level[s]}, {m_ids} fronts, n={nin}) + a dense "
+            f"root over its {len(U)} update indices")
+    if s == t.root_id():
+        desc = "the whole workload"
+        return pieces, None, desc
+    return pieces, float(fl.sum()), desc
 
 
 def run_reference_sample(cfg, pieces, threads):
@@ -259,7 +276,7 @@ def reference_arm(args, cfg, op):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
+    pieces, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
     thr = cpu_threads()
     for _ in range(args.warmup):
         run_reference_sample(cfg, pieces, thr)
@@ -267,6 +284,8 @@ def reference_arm(args, cfg, op):
     t = float(np.mean([r[0] for r in runs]))
     sfl = runs[0][1]
     desc += f", {runs[0][2]} HSS fronts in the sample"
+    if tfl is None:
+        tfl = sfl
     scaled = t * tfl / sfl
     line = {
         "metric": METRIC, "value": scaled, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
@@ -440,9 +459,11 @@ def main():
         try:
             from oracle import ref
             if ref.available():
-                pieces, sfl, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
+                pieces, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
                 thr = cpu_threads()
                 t, sfl, nh = run_reference_sample(cfg, pieces, thr)
+                if tfl is None:
+                    tfl = sfl
                 line["cpu_baseline"] = {"value": t * tfl / sfl, "unit": "s", "cores": thr,
                                         "kind": "reference",
                                         "sample": desc + f", {nh} HSS fronts in the sample; "
