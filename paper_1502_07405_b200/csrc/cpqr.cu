@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include "gemm.cuh"
+
 namespace hssmf_b200 {
 
   namespace {
@@ -468,6 +470,91 @@ namespace hssmf_b200 {
     dim3 grid(ceil_div(max_cols, cpc), ntask);
     id_solve_kernel<<<grid, 256, (size_t)cpc * max_rank * 8, s>>>(tasks, cpc);
     HSSMF_LAUNCH_CHECK();
+  }
+
+  namespace {
+    constexpr int TB = 64, TC = 128;
+
+    struct TriStep {
+      const double* R;   // R1 block origin: R + i0 + i0*ldr
+      int ldr;
+      double* X;         // X rows [i0, i0+bs), ld ldx
+      int ldx, bs, ncols;
+    };
+
+    // X[i0:i0+bs, :] <- R1[i0:i0+bs, i0:i0+bs]^-1 X[i0:i0+bs, :] (upper, non-unit)
+    __global__ void __launch_bounds__(TC) tri_block_kernel(const TriStep* __restrict__ st) {
+      const TriStep S = st[blockIdx.y];
+      __shared__ double Rb[TB][TB + 1];
+      for (int e = threadIdx.x; e < S.bs * S.bs; e += TC) {
+        const int r = e % S.bs, c = e / S.bs;
+        Rb[r][c] = S.R[r + (size_t)c * S.ldr];
+      }
+      __syncthreads();
+      const int c = blockIdx.x * TC + threadIdx.x;
+      if (c >= S.ncols) return;
+      double* col = S.X + (size_t)c * S.ldx;
+      double x[TB];
+#pragma unroll
+      for (int r = 0; r < TB; r++) x[r] = r < S.bs ? col[r] : 0.0;
+#pragma unroll
+      for (int i = TB - 1; i >= 0; i--) {
+        if (i < S.bs) {
+          double s = x[i];
+#pragma unroll
+          for (int l = i + 1; l < TB; l++)
+            if (l < S.bs) s -= Rb[i][l] * x[l];
+          x[i] = s / Rb[i][i];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < TB; r++)
+        if (r < S.bs) col[r] = x[r];
+    }
+  }  // namespace
+
+  void id_solve_blocked(const std::vector<CpqrTask>& tasks, const std::vector<int>& ranks,
+                        cudaStream_t s, double* flops) {
+    // X = R2 (copies), then blocks from the bottom
+    int maxb = 0;
+    for (size_t t = 0; t < tasks.size(); t++) {
+      const int k = ranks[t], nc = tasks[t].n - k;
+      if (k <= 0 || nc <= 0) continue;
+      HSSMF_CUDA(cudaMemcpy2DAsync(tasks[t].X, (size_t)k * sizeof(double),
+                                   tasks[t].Y + (size_t)k * tasks[t].ldy,
+                                   (size_t)tasks[t].ldy * sizeof(double), (size_t)k * sizeof(double),
+                                   nc, cudaMemcpyDeviceToDevice, s));
+      maxb = std::max(maxb, (k + TB - 1) / TB);
+    }
+    TriStep* d = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&d, std::max<size_t>(tasks.size(), 1) * sizeof(TriStep), s));
+    for (int j = 0; j < maxb; j++) {
+      std::vector<TriStep> steps;
+      std::vector<GemmProblem> up;
+      int maxc = 0;
+      for (size_t t = 0; t < tasks.size(); t++) {
+        const auto& T = tasks[t];
+        const int k = ranks[t], nc = T.n - k;
+        if (k <= 0 || nc <= 0) continue;
+        const int i1 = k - j * TB;
+        if (i1 <= 0) continue;
+        const int i0 = std::max(0, i1 - TB), bs = i1 - i0;
+        steps.push_back({T.Y + i0 + (size_t)i0 * T.ldy, T.ldy, T.X + i0, k, bs, nc});
+        maxc = std::max(maxc, nc);
+        if (i0 > 0) {  // X[0:i0, :] -= R1[0:i0, i0:i1] X[i0:i1, :]
+          up.push_back({T.Y + (size_t)i0 * T.ldy, T.X + i0, T.X, i0, nc, bs, T.ldy, k, k});
+          if (flops) *flops += 2.0 * i0 * nc * bs;
+        }
+        if (flops) *flops += (double)bs * bs * nc;
+      }
+      if (steps.empty()) continue;
+      HSSMF_CUDA(cudaMemcpyAsync(d, steps.data(), steps.size() * sizeof(TriStep),
+                                 cudaMemcpyHostToDevice, s));
+      tri_block_kernel<<<dim3(ceil_div(maxc, TC), (unsigned)steps.size()), TC, 0, s>>>(d);
+      HSSMF_LAUNCH_CHECK();
+      gemm_run_host(up, 'N', 'N', -1.0, 1.0, s);
+    }
+    HSSMF_CUDA(cudaFreeAsync(d, s));
   }
 
   void cpqr_id_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,

@@ -5,6 +5,8 @@
 // second, column-tiled kernel once the ranks are known.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace hssmf_b200 {
@@ -24,6 +26,13 @@ namespace hssmf_b200 {
                 double abs_tol, cudaStream_t s);
   void id_solve_run(const CpqrTask* tasks, int ntask, int max_rank, int max_cols,
                     cudaStream_t s);
+  // ID coefficients for tasks with known ranks (host copies), blocked by 64:
+  // X = R2; for each 64-row block from the bottom, a triangular solve of the
+  // block (CTA per 128 columns) and a DMMA GEMM update of the rows above
+  // (reference trsm, kernels.hpp:205-244, with the same recursion base)
+  void id_solve_blocked(const std::vector<CpqrTask>& tasks, const std::vector<int>& ranks,
+                        cudaStream_t s, double* flops = nullptr);
+
   // convenience: both phases with an internal rank readback
   void cpqr_id_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,
                    double abs_tol, cudaStream_t s);

@@ -34,6 +34,7 @@ namespace hssmf_b200 {
       const int tiles_m = (P.m + BM - 1) / BM;
       const int t = tile - __ldg(prefix + lo);
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+      if (P.lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
       const int K = P.k;
 
       const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -20,6 +20,7 @@ namespace hssmf_b200 {
     int m, n, k;
     int lda, ldb, ldc;
     const int* skip = nullptr;  // optional device flag: problem is a no-op when *skip != 0
+    int lower = 0;              // only the lower triangle of C is needed (SYRK-like)
   };
 
   // device-resident batch: descriptors + tile prefix (prefix[p] = first tile

@@ -172,7 +172,8 @@ namespace hssmf_b200 {
             T.L[gi + (size_t)j * n] = ljj;
             continue;
           }
-          double s = gcol[gi];
+          // lower triangle of G only (the trailing updates skip the upper one)
+          double s = gi >= pj ? gcol[gi] : T.G[pj + (size_t)gi * n];
           const double* lr = Lp + (size_t)i * nb;
           for (int q = 0; q < jj; q++) s -= lr[q] * prow[q];
           const double lo = s / ljj;
@@ -270,9 +271,10 @@ namespace hssmf_b200 {
         GemmProblem g{T.L + (size_t)k0 * T.n, T.L + (size_t)k0 * T.n, T.G, T.n, T.n, nb, T.n,
                       T.n, T.n};
         g.skip = T.state + 1;
+        g.lower = 1;
         p.push_back(g);
       }
-      if (flops) *flops += gemm_flops(p);
+      if (flops) *flops += 0.5 * gemm_flops(p);
       gemm_run_host(p, 'N', 'T', -1.0, 1.0, s);
     }
     for (int t = 0; t < nt; t++)

@@ -492,8 +492,11 @@ namespace hssmf_b200 {
           N.G0r.zero();
           N.G0c.zero();
         }
-        gp.push_back({N.slr.col(cb0), N.slr.col(cb0), N.G0r.p, mt, mt, nc, mt, mt, mt});
-        gp.push_back({N.slc.col(cb0), N.slc.col(cb0), N.G0c.p, mt, mt, nc, mt, mt, mt});
+        GemmProblem gr{N.slr.col(cb0), N.slr.col(cb0), N.G0r.p, mt, mt, nc, mt, mt, mt};
+        GemmProblem gc{N.slc.col(cb0), N.slc.col(cb0), N.G0c.p, mt, mt, nc, mt, mt, mt};
+        gr.lower = gc.lower = 1;  // the Gram route reads the lower triangle only
+        gp.push_back(gr);
+        gp.push_back(gc);
         N.gram_cols = d;
       }
       flops += gemm_flops(gp);
@@ -620,7 +623,8 @@ namespace hssmf_b200 {
       const int na = (int)act.size();
       (void)Y;
       std::vector<int> okq;
-      std::vector<CpqrTask> solve_tasks;
+      std::vector<CpqrTask> solve_tasks, big_tasks;
+      std::vector<int> big_ranks;
       int max_rank_ok = 0, max_cols = 0;
       for (int q = 0; q < na; q++) {
         const int kr = ho[4 * q], cr = ho[4 * q + 1], kc = ho[4 * q + 2], cc = ho[4 * q + 3];
@@ -632,6 +636,11 @@ namespace hssmf_b200 {
         for (int side = 0; side < 2; side++) {
           const int t = 2 * q + side, k = ho[2 * t];
           if (k > 0 && tasks[t].n > k) {
+            if (k > 128) {  // GEMM-blocked triangular solve for large ranks
+              big_tasks.push_back(tasks[t]);
+              big_ranks.push_back(k);
+              continue;
+            }
             solve_tasks.push_back(tasks[t]);
             max_rank_ok = std::max(max_rank_ok, k);
             max_cols = std::max(max_cols, tasks[t].n - k);
@@ -640,6 +649,7 @@ namespace hssmf_b200 {
         }
       }
       if (okq.empty()) return;
+      if (!big_tasks.empty()) id_solve_blocked(big_tasks, big_ranks, s, &flops);
       if (!solve_tasks.empty()) {
         DBuf<CpqrTask> ds;
         ds.alloc(solve_tasks.size(), s);
