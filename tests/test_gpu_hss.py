@@ -242,3 +242,18 @@ def test_c1_hss_off_vs_golden():
     g = np.load(os.path.join(GOLD, "ref_c1_mf.npz"))
     op, m, b, x, res = run_mf("p2d", 256, 64, mode="mf")
     assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [64, 80])
+def test_p3d_with_config5_options_vs_reference(k):
+    # BASELINE config 5 options (HSS >= 4000, eps 1e-4, leaf 256) on smaller
+    # grids the reference finishes in minutes (tools/run_custom.py --ref):
+    # every HSS-front rank and the residual must match
+    import json
+    g = json.load(open(os.path.join(GOLD, f"ref_p3d{k}_c5opts.json")))["ref"]
+    so = dict(ls=64, min_hss=4000, eps=1e-4, leaf=256)
+    op, m, b, x, res = run_mf("p3d", k, 32, **so)
+    ranks = [int(m.rank[i]) for i in np.nonzero(m.type == 1)[0]]
+    assert len(ranks) == g["hss"]
+    assert ranks_close(ranks, g["ranks"])
+    assert res <= 10 * g["relres"]
