@@ -1,5 +1,6 @@
 #include "kernels_test.hpp"
 
+#include <cstdlib>
 #include <stdexcept>
 #include <vector>
 
@@ -112,19 +113,26 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemset(A.p, 0, (size_t)m * k * 8));
     HSSMF_CUDA(cudaMemset(B.p, 0, (size_t)k * n * 8));
     HSSMF_CUDA(cudaMemset(C.p, 0, (size_t)m * n * 8));
-    std::vector<GemmProblem> p{{A.as<double>(), B.as<double>(), C.as<double>(), m, n, k, m, k, m}};
+    // HSSMF_BENCH_TRANS=TN|NT|TT selects the operand transposes (measurement only)
+    char ta = 'N', tb = 'N';
+    if (const char* e = getenv("HSSMF_BENCH_TRANS")) {
+      ta = e[0];
+      tb = e[1];
+    }
+    const int lda = ta == 'N' ? m : k, ldb = tb == 'N' ? k : n;
+    std::vector<GemmProblem> p{{A.as<double>(), B.as<double>(), C.as<double>(), m, n, k, lda, ldb, m}};
     auto pre = gemm_tile_prefix(p);
     Buf D(sizeof(GemmProblem) + pre.size() * 4);
     HSSMF_CUDA(cudaMemcpy(D.p, p.data(), sizeof(GemmProblem), cudaMemcpyHostToDevice));
     HSSMF_CUDA(cudaMemcpy((char*)D.p + sizeof(GemmProblem), pre.data(), pre.size() * 4, cudaMemcpyHostToDevice));
     GemmBatchDev b{D.as<GemmProblem>(), (const int*)((char*)D.p + sizeof(GemmProblem)), 1, pre.back()};
-    gemm_run(b, 'N', 'N', 1.0, 1.0, 0);
+    gemm_run(b, ta, tb, 1.0, 1.0, 0);
     HSSMF_CUDA(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     HSSMF_CUDA(cudaEventCreate(&e0));
     HSSMF_CUDA(cudaEventCreate(&e1));
     HSSMF_CUDA(cudaEventRecord(e0, 0));
-    for (int i = 0; i < iters; i++) gemm_run(b, 'N', 'N', 1.0, 1.0, 0);
+    for (int i = 0; i < iters; i++) gemm_run(b, ta, tb, 1.0, 1.0, 0);
     HSSMF_CUDA(cudaEventRecord(e1, 0));
     HSSMF_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
