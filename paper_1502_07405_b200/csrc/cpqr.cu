@@ -284,14 +284,18 @@ namespace hssmf_b200 {
           pub.bi = p;
         }
         cl.sync();
-        // 2. global decision (identical in every CTA)
-        if (tid == 0) {
-          double b = -1.0;
-          int p = 0x7fffffff;
-          for (int r = 0; r < CL; r++) {
-            const ClPub* q = cl.map_shared_rank(&pub, r);
-            if (q->bv > b || (q->bv == b && q->bi < p)) { b = q->bv; p = q->bi; }
+        // 2. global decision (identical in every CTA); one lane per peer CTA
+        double b = -1.0;
+        int p = 0x7fffffff;
+        if (tid < 32) {
+          if (tid < CL) {
+            const ClPub* q = cl.map_shared_rank(&pub, tid);
+            b = q->bv;
+            p = q->bi;
           }
+          warp_argmax(b, p);
+        }
+        if (tid == 0) {
           const double pv = b > 0.0 ? sqrt(b) : 0.0;
           int stop = 0;
           if (k == 0) {

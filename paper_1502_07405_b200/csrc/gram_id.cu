@@ -113,13 +113,18 @@ namespace hssmf_b200 {
       cl.sync();
       for (int jj = 0; jj < nb && !stopped; jj++, j++) {
         const int buf = jj & 1;
-        // decision for step j (identical in every CTA, rrqr.hpp:62-77)
-        if (tid == 0) {
+        // decision for step j (identical in every CTA, rrqr.hpp:62-77): one
+        // lane per peer CTA fetches its candidate over DSMEM, warp reduction
+        if (tid < 32) {
           Cand c{-1.0, INT_MAX, -1};
-          for (int r = 0; r < CL; r++) {
-            const Cand* q = cl.map_shared_rank(&pub[buf], r);
-            if (better(q->v, q->pos, c.v, c.pos)) c = *q;
+          if (tid < CL) c = *cl.map_shared_rank(&pub[buf], tid);
+          for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_down_sync(0xffffffffu, c.v, o);
+            const int p2 = __shfl_down_sync(0xffffffffu, c.pos, o);
+            const int i2 = __shfl_down_sync(0xffffffffu, c.idx, o);
+            if (better(v2, p2, c.v, c.pos)) c = {v2, p2, i2};
           }
+          if (tid == 0) {
           const double pv = c.v > 0.0 ? sqrt(c.v) : 0.0;
           int stop = 0, ct = 0;
           if (j == 0) {
@@ -137,6 +142,7 @@ namespace hssmf_b200 {
           s_cert = ct;
           s_pj = c.idx;
           s_ljj = pv;
+          }
         }
         __syncthreads();
         if (s_stop) {
