@@ -285,17 +285,19 @@ namespace hssmf_b200 {
         }
         cl.sync();
         // 2. global decision (identical in every CTA); one lane per peer CTA
-        double b = -1.0;
-        int p = 0x7fffffff;
+        double gb = -1.0;
+        int gp = 0x7fffffff;
         if (tid < 32) {
           if (tid < CL) {
             const ClPub* q = cl.map_shared_rank(&pub, tid);
-            b = q->bv;
-            p = q->bi;
+            gb = q->bv;
+            gp = q->bi;
           }
-          warp_argmax(b, p);
+          warp_argmax(gb, gp);
         }
         if (tid == 0) {
+          const double b = gb;
+          const int p = gp;
           const double pv = b > 0.0 ? sqrt(b) : 0.0;
           int stop = 0;
           if (k == 0) {
