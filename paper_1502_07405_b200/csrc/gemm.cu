@@ -6,6 +6,10 @@
 // owning problem is found by binary search over the tile prefix.
 #include "gemm.cuh"
 
+#include <cstring>
+
+#include "staging.cuh"
+
 namespace hssmf_b200 {
 
   namespace {
@@ -167,6 +171,17 @@ namespace hssmf_b200 {
     if (q.empty()) return;
     auto pre = gemm_tile_prefix(q);
     const size_t pb = q.size() * sizeof(GemmProblem), xb = pre.size() * sizeof(int);
+    if (Staging* st = current_staging(s)) {
+      std::vector<char> buf(pb + xb);
+      std::memcpy(buf.data(), q.data(), pb);
+      std::memcpy(buf.data() + pb, pre.data(), xb);
+      if (void* d = st->put(buf.data(), buf.size())) {
+        GemmBatchDev b{(const GemmProblem*)d, (const int*)((char*)d + pb), (int)q.size(),
+                       pre.back()};
+        gemm_run(b, ta, tb, alpha, beta, s);
+        return;
+      }
+    }
     void* d = nullptr;
     HSSMF_CUDA(cudaMallocAsync(&d, pb + xb, s));
     HSSMF_CUDA(cudaMemcpyAsync(d, q.data(), pb, cudaMemcpyHostToDevice, s));

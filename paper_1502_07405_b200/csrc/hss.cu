@@ -13,6 +13,7 @@
 #include "hss_kernels.cuh"
 #include "gram_id.cuh"
 #include "rng.cuh"
+#include "staging.cuh"
 
 namespace hssmf_b200 {
 
@@ -1250,10 +1251,17 @@ namespace hssmf_b200 {
 
   void HssMatrixDev::compress(const double* A, long long lda, const ClusterTree& tree,
                               const std::vector<long long>& seeds, const HssOpts& o) {
+    StagingScope sc(staging_for(d_->s));
     d_->compress(A, lda, tree, seeds, o);
   }
-  void HssMatrixDev::ulv_full() { d_->ulv_full(); }
-  void HssMatrixDev::ulv_partial(double* update, long long ldu) { d_->ulv_partial(update, ldu); }
+  void HssMatrixDev::ulv_full() {
+    StagingScope sc(staging_for(d_->s));
+    d_->ulv_full();
+  }
+  void HssMatrixDev::ulv_partial(double* update, long long ldu) {
+    StagingScope sc(staging_for(d_->s));
+    d_->ulv_partial(update, ldu);
+  }
   void HssMatrixDev::drop_dense() {
     d_->A = nullptr;
     for (auto& N : d_->nodes) {
@@ -1275,9 +1283,18 @@ namespace hssmf_b200 {
     d_->collect_phases();
     d_->s = s;
   }
-  void HssMatrixDev::solve_full(double* x) { d_->solve_full(x); }
-  void HssMatrixDev::partial_forward(const double* b1, double* bupd) { d_->partial_forward(b1, bupd); }
-  void HssMatrixDev::partial_backward(double* x1, const double* x2) { d_->partial_backward(x1, x2); }
+  void HssMatrixDev::solve_full(double* x) {
+    StagingScope sc(staging_for(d_->s));
+    d_->solve_full(x);
+  }
+  void HssMatrixDev::partial_forward(const double* b1, double* bupd) {
+    StagingScope sc(staging_for(d_->s));
+    d_->partial_forward(b1, bupd);
+  }
+  void HssMatrixDev::partial_backward(double* x1, const double* x2) {
+    StagingScope sc(staging_for(d_->s));
+    d_->partial_backward(x1, x2);
+  }
   int HssMatrixDev::rows() const { return d_->m; }
   int HssMatrixDev::rounds() const { return d_->rounds; }
   int HssMatrixDev::d_final() const { return d_->d; }

@@ -2,6 +2,8 @@
 
 #include <algorithm>
 
+#include "staging.cuh"
+
 namespace hssmf_b200 {
 
   namespace {
@@ -243,11 +245,24 @@ namespace hssmf_b200 {
       done = true;
     }
 
-    template<typename T> T* upload_async(const std::vector<T>& v, cudaStream_t s) {
+    // device copy of a host array: through the thread's staging ring when it
+    // serves this stream (no free needed), else a stream-ordered allocation
+    template<typename T> struct Up {
+      T* p;
+      bool owned;
+    };
+    template<typename T> Up<T> upload_async(const std::vector<T>& v, cudaStream_t s) {
+      if (Staging* st = current_staging(s))
+        if (!v.empty())
+          if (void* p = st->put(v.data(), v.size() * sizeof(T)))
+            return {static_cast<T*>(p), false};
       T* d = nullptr;
       HSSMF_CUDA(cudaMallocAsync((void**)&d, std::max<size_t>(v.size() * sizeof(T), 16), s));
       HSSMF_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
-      return d;
+      return {d, true};
+    }
+    template<typename T> void release_async(const Up<T>& u, cudaStream_t s) {
+      if (u.owned) HSSMF_CUDA(cudaFreeAsync(u.p, s));
     }
   }  // namespace
 
@@ -260,12 +275,12 @@ namespace hssmf_b200 {
     for (size_t i = 0; i < d.size(); i++)
       pre[i + 1] = pre[i] + ((d[i].diag ? (long long)d[i].nr : (long long)d[i].nr * d[i].nc) +
                              CPB - 1) / CPB;
-    auto* dd = upload_async(d, s);
-    auto* dp = upload_async(pre, s);
-    index_copy_kernel<<<(unsigned)pre.back(), 256, 0, s>>>(dd, dp, (int)d.size());
+    auto dd = upload_async(d, s);
+    auto dp = upload_async(pre, s);
+    index_copy_kernel<<<(unsigned)pre.back(), 256, 0, s>>>(dd.p, dp.p, (int)d.size());
     HSSMF_LAUNCH_CHECK();
-    HSSMF_CUDA(cudaFreeAsync(dd, s));
-    HSSMF_CUDA(cudaFreeAsync(dp, s));
+    release_async(dd, s);
+    release_async(dp, s);
   }
 
   void maxabs_run(const double* a, long long lda, int m, int n, double* out, cudaStream_t s) {
@@ -282,10 +297,10 @@ namespace hssmf_b200 {
     int mmax = 0;
     for (auto& n : nodes) mmax = std::max(mmax, n.m);
     if ((size_t)mmax * 16 > 200 * 1024) throw CudaError("ulv solve: node too large for smem");
-    auto* d = upload_async(nodes, s);
-    ulv_fwd_kernel<<<(unsigned)nodes.size(), UT, (size_t)mmax * 16, s>>>(d);
+    auto d = upload_async(nodes, s);
+    ulv_fwd_kernel<<<(unsigned)nodes.size(), UT, (size_t)mmax * 16, s>>>(d.p);
     HSSMF_LAUNCH_CHECK();
-    HSSMF_CUDA(cudaFreeAsync(d, s));
+    release_async(d, s);
   }
 
   void ulv_bwd_level(const std::vector<UlvSolveNode>& nodes, cudaStream_t s) {
@@ -294,10 +309,10 @@ namespace hssmf_b200 {
     int mmax = 0;
     for (auto& n : nodes) mmax = std::max(mmax, n.m);
     if ((size_t)mmax * 8 > 200 * 1024) throw CudaError("ulv solve: node too large for smem");
-    auto* d = upload_async(nodes, s);
-    ulv_bwd_kernel<<<(unsigned)nodes.size(), UT, (size_t)mmax * 8, s>>>(d);
+    auto d = upload_async(nodes, s);
+    ulv_bwd_kernel<<<(unsigned)nodes.size(), UT, (size_t)mmax * 8, s>>>(d.p);
     HSSMF_LAUNCH_CHECK();
-    HSSMF_CUDA(cudaFreeAsync(d, s));
+    release_async(d, s);
   }
 
   void lu_solve_vec(const double* lu, int ld, const int* perm, int n, double* x, cudaStream_t s) {

@@ -1,0 +1,67 @@
+#include "staging.cuh"
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+namespace hssmf_b200 {
+
+  namespace {
+    thread_local Staging* g_cur = nullptr;
+  }
+
+  Staging::Staging(cudaStream_t s, size_t chunk_bytes, int chunks)
+      : s_(s), chunk_(chunk_bytes), nchunks_(chunks), ev_(chunks), armed_(chunks, 0) {
+    HSSMF_CUDA(cudaMallocHost((void**)&h_, chunk_ * nchunks_));
+    HSSMF_CUDA(cudaMalloc((void**)&d_, chunk_ * nchunks_));
+    for (auto& e : ev_) HSSMF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+
+  Staging::~Staging() {
+    cudaStreamSynchronize(s_);
+    for (auto& e : ev_) cudaEventDestroy(e);
+    cudaFreeHost(h_);
+    cudaFree(d_);
+  }
+
+  void* Staging::put(const void* src, size_t n) {
+    const size_t a = (n + 255) & ~size_t(255);
+    if (a > chunk_) return nullptr;
+    if (head_ + a > chunk_) {
+      // leave the current chunk: mark it busy until the stream passes this point
+      HSSMF_CUDA(cudaEventRecord(ev_[cur_], s_));
+      armed_[cur_] = 1;
+      cur_ = (cur_ + 1) % nchunks_;
+      head_ = 0;
+      if (armed_[cur_]) {
+        HSSMF_CUDA(cudaEventSynchronize(ev_[cur_]));
+        armed_[cur_] = 0;
+      }
+    }
+    char* h = h_ + (size_t)cur_ * chunk_ + head_;
+    char* d = d_ + (size_t)cur_ * chunk_ + head_;
+    std::memcpy(h, src, n);
+    HSSMF_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s_));
+    head_ += a;
+    return d;
+  }
+
+  Staging* staging_for(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, std::unique_ptr<Staging>>* reg =
+        new std::map<cudaStream_t, std::unique_ptr<Staging>>();  // never destroyed
+    std::lock_guard<std::mutex> lk(mu);
+    auto& p = (*reg)[s];
+    if (!p) p.reset(new Staging(s));
+    return p.get();
+  }
+
+  Staging* current_staging(cudaStream_t s) {
+    return (g_cur && g_cur->stream() == s) ? g_cur : nullptr;
+  }
+
+  StagingScope::StagingScope(Staging* st) : prev(g_cur) { g_cur = st; }
+  StagingScope::~StagingScope() { g_cur = prev; }
+
+}  // namespace hssmf_b200

@@ -1,0 +1,49 @@
+// Pinned host -> device staging ring for small per-launch descriptor arrays.
+//
+// The dynamic (HSS) phases upload a few hundred bytes of descriptors before
+// almost every launch. A ring of pinned chunks makes each upload one truly
+// asynchronous cudaMemcpyAsync, with no per-launch device allocation; a chunk
+// is reused only after an event recorded behind its last consumer has
+// completed. A Staging is bound to one stream and made current for the
+// calling thread with StagingScope; gemm_run_host / index_copy_run / the ULV
+// solve launchers use it when the stream matches.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace hssmf_b200 {
+
+  class Staging {
+   public:
+    explicit Staging(cudaStream_t s, size_t chunk_bytes = 256 << 10, int chunks = 32);
+    ~Staging();
+    Staging(const Staging&) = delete;
+    Staging& operator=(const Staging&) = delete;
+    cudaStream_t stream() const { return s_; }
+    // device copy of n host bytes, stream-ordered; nullptr if n exceeds a chunk
+    void* put(const void* src, size_t n);
+
+   private:
+    cudaStream_t s_;
+    size_t chunk_;
+    int nchunks_, cur_ = 0;
+    size_t head_ = 0;
+    char* h_ = nullptr;
+    char* d_ = nullptr;
+    std::vector<cudaEvent_t> ev_;
+    std::vector<char> armed_;
+  };
+
+  // process-wide ring per stream (created on first use)
+  Staging* staging_for(cudaStream_t s);
+  // thread-local current staging ring
+  Staging* current_staging(cudaStream_t s);
+  struct StagingScope {
+    Staging* prev;
+    explicit StagingScope(Staging* st);
+    ~StagingScope();
+  };
+
+}  // namespace hssmf_b200
