@@ -244,6 +244,33 @@ def test_c1_hss_off_vs_golden():
     assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-10
 
 
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_baseline_config_vs_golden(name):
+    # BASELINE configs 3 (P3D 64^3, eps 1e-4) and 4 (convection-diffusion
+    # 96^3, eps 1e-5): front types, per-front and per-node ranks within +-10%,
+    # residual <= 10x the reference's (tests/golden/ref_<name>.npz)
+    from paper_1502_07405_b200.problems import CONFIGS
+    cfg = CONFIGS[name]
+    g = np.load(os.path.join(GOLD, f"ref_{name}.npz"))
+    if cfg.kind == "cd3d":
+        op = P.ordered_problem(P.generate_convdiff3d(cfg.k, 0.1), cfg.nd_leaf)
+    else:
+        op = P.ordered_grid(cfg.kind, cfg.k, cfg.nd_leaf)
+    ptr, ind, val = op.a.arrays()
+    b = csr_matvec(ptr, ind, val, x_true(op.a.size(), 1))
+    m = P.mf_factor(op.a, op.t, cfg.solver_options())
+    x = P.mf_solve_new(m, b)
+    res = np.linalg.norm(op.a.matvec(x) - b) / np.linalg.norm(b)
+    assert np.array_equal(m.type, g["type"])
+    hs = g["hss_ids"]
+    assert ranks_close(m.rank[hs], g["rank"][hs])
+    for q, i in enumerate(hs):
+        u = m.front_hss(int(i))[0]
+        ru = g["node_u"][g["node_ptr"][q]:g["node_ptr"][q + 1]]
+        assert ranks_close(u[:-1], ru[:-1]), i
+    assert res <= 10 * float(g["relres"])
+
+
 @pytest.mark.parametrize("k", [64, 80])
 def test_p3d_with_config5_options_vs_reference(k):
     # BASELINE config 5 options (HSS >= 4000, eps 1e-4, leaf 256) on smaller
