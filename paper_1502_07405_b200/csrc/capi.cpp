@@ -2,6 +2,7 @@
 // device engine. Exceptions never cross the ABI: they become hssmf_codes.
 #include "../../include/hssmf_b200.h"
 
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -21,6 +22,17 @@ namespace hssmf_b200 {
   std::atomic<long long>& launch_counter() {
     static std::atomic<long long> c{0};
     return c;
+  }
+  SyncClock& sync_clock() {
+    static thread_local SyncClock c;
+    return c;
+  }
+  void stream_sync(cudaStream_t s) {
+    auto& c = sync_clock();
+    const auto a = std::chrono::steady_clock::now();
+    HSSMF_CUDA(cudaStreamSynchronize(s));
+    c.wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+    c.n++;
   }
 }  // namespace hssmf_b200
 

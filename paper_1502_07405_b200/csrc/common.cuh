@@ -33,6 +33,16 @@ namespace hssmf_b200 {
 
   inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+  // host time the calling thread spent blocked in stream_sync (seconds) and the
+  // number of such waits: HSSMF_DEBUG splits a front's wall time into host work
+  // and GPU waits with it
+  struct SyncClock {
+    double wait_s = 0;
+    long long n = 0;
+  };
+  SyncClock& sync_clock();
+  void stream_sync(cudaStream_t s);
+
   // ---- device-side ----------------------------------------------------------
 #ifdef __CUDACC__
   // one FP64 tensor-core MMA: D(8x8) += A(8x4) * B(4x8).

@@ -488,9 +488,14 @@ namespace hssmf_b200 {
       int ldx, bs, ncols;
     };
 
+    constexpr int kParamSteps = 128;
+    struct TriParam {
+      TriStep st[kParamSteps];
+    };
+
     // X[i0:i0+bs, :] <- R1[i0:i0+bs, i0:i0+bs]^-1 X[i0:i0+bs, :] (upper, non-unit)
-    __global__ void __launch_bounds__(TC) tri_block_kernel(const TriStep* __restrict__ st) {
-      const TriStep S = st[blockIdx.y];
+    __global__ void __launch_bounds__(TC) tri_block_kernel(const __grid_constant__ TriParam P) {
+      const TriStep S = P.st[blockIdx.y];
       __shared__ double Rb[TB][TB + 1];
       for (int e = threadIdx.x; e < S.bs * S.bs; e += TC) {
         const int r = e % S.bs, c = e / S.bs;
@@ -532,8 +537,6 @@ namespace hssmf_b200 {
                                    nc, cudaMemcpyDeviceToDevice, s));
       maxb = std::max(maxb, (k + TB - 1) / TB);
     }
-    TriStep* d = nullptr;
-    HSSMF_CUDA(cudaMallocAsync((void**)&d, std::max<size_t>(tasks.size(), 1) * sizeof(TriStep), s));
     for (int j = 0; j < maxb; j++) {
       std::vector<TriStep> steps;
       std::vector<GemmProblem> up;
@@ -553,14 +556,15 @@ namespace hssmf_b200 {
         }
         if (flops) *flops += (double)bs * bs * nc;
       }
-      if (steps.empty()) continue;
-      HSSMF_CUDA(cudaMemcpyAsync(d, steps.data(), steps.size() * sizeof(TriStep),
-                                 cudaMemcpyHostToDevice, s));
-      tri_block_kernel<<<dim3(ceil_div(maxc, TC), (unsigned)steps.size()), TC, 0, s>>>(d);
-      HSSMF_LAUNCH_CHECK();
+      for (size_t b0 = 0; b0 < steps.size(); b0 += kParamSteps) {
+        TriParam P;
+        const int nb = (int)std::min<size_t>(kParamSteps, steps.size() - b0);
+        for (int q = 0; q < nb; q++) P.st[q] = steps[b0 + q];
+        tri_block_kernel<<<dim3(ceil_div(maxc, TC), (unsigned)nb), TC, 0, s>>>(P);
+        HSSMF_LAUNCH_CHECK();
+      }
       gemm_run_host(up, 'N', 'N', -1.0, 1.0, s);
     }
-    HSSMF_CUDA(cudaFreeAsync(d, s));
   }
 
   void cpqr_id_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,

@@ -570,7 +570,7 @@ namespace hssmf_b200 {
     if (!fallback) {
       H->drop_dense();
       HSSMF_CUDA(cudaFreeAsync(F, st));
-      HSSMF_CUDA(cudaStreamSynchronize(st));
+      stream_sync(st);
       res.hss = std::move(H);
       return res;
     }
@@ -623,17 +623,21 @@ namespace hssmf_b200 {
       return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
     const double t0 = now();
-    std::vector<double> tq(lst.size());
+    std::vector<double> tq(lst.size()), tw(lst.size());
+    std::vector<long long> nw_(lst.size());
     auto work = [&](int w) {
       cudaSetDevice(dev);
       for (int q = next++; q < (int)lst.size(); q = next++) {
         const double a = now();
+        const SyncClock c0 = sync_clock();
         try {
           res[q] = compress_hss_front(lst[q], F[q], hstreams[w]);
         } catch (const std::exception& e) {
           res[q].error = e.what();
         }
         tq[q] = now() - a;
+        tw[q] = sync_clock().wait_s - c0.wait_s;
+        nw_[q] = sync_clock().n - c0.n;
       }
     };
     if (nw <= 1) {
@@ -647,8 +651,9 @@ namespace hssmf_b200 {
       fprintf(stderr, "[hssmf] level: %zu HSS fronts, wall %.3f s\n", lst.size(), now() - t0);
       for (size_t q = 0; q < lst.size(); q++) {
         const auto& fn = t.nodes[lst[q]];
-        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s  rounds=%d d=%d rank=%d |", lst[q],
-                fn.m(), fn.ns(), tq[q], res[q].hss ? res[q].hss->rounds() : -1,
+        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s (sync wait %.3f s in %lld, arena %.0f MB) rounds=%d d=%d rank=%d |",
+                lst[q], fn.m(), fn.ns(), tq[q], tw[q], nw_[q],
+                res[q].hss ? res[q].hss->arena_bytes() / 1e6 : 0.0, res[q].hss ? res[q].hss->rounds() : -1,
                 res[q].hss ? res[q].hss->d_final() : -1, res[q].hss ? res[q].hss->hss_rank() : -1);
         if (res[q].hss) {
           auto ps = res[q].hss->phase_stats();
@@ -684,6 +689,7 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaSetDevice(device_));
     auto& D = *d_;
     D.profile = profile_;
+    hss_set_phase_timing(profile_ || getenv("HSSMF_DEBUG") != nullptr);
     const int nn = (int)D.hf.size();
     // previous HSS / fallback state is rebuilt
     D.hss.clear();

@@ -8,7 +8,6 @@
 
 #include <cstring>
 
-#include "staging.cuh"
 
 namespace hssmf_b200 {
 
@@ -18,10 +17,18 @@ namespace hssmf_b200 {
     constexpr int SB = BK + 4;  // B tile stored [n][k]
     constexpr int SMEM = STAGES * (BK * SA + BN * SB) * 8;
 
+    // descriptors passed by value as a __grid_constant__ kernel parameter:
+    // a dynamic-phase launch then needs no separate descriptor upload
+    constexpr int kParamProbs = 96;
+    struct GemmParam {
+      int nprob;
+      int pre[kParamProbs + 1];
+      GemmProblem p[kParamProbs];
+    };
+
     template<bool TA, bool TB>
-    __global__ void __launch_bounds__(THREADS)
-    gemm_grouped_kernel(const GemmProblem* __restrict__ probs, const int* __restrict__ prefix,
-                        int nprob, double alpha, double beta) {
+    __device__ __forceinline__ void gemm_body(const GemmProblem* probs, const int* prefix,
+                                              int nprob, double alpha, double beta) {
       extern __shared__ __align__(16) double gsm[];
       double (*As)[BK * SA] = reinterpret_cast<double (*)[BK * SA]>(gsm);
       double (*Bs)[BN * SB] = reinterpret_cast<double (*)[BN * SB]>(gsm + STAGES * BK * SA);
@@ -31,12 +38,12 @@ namespace hssmf_b200 {
       int lo = 0, hi = nprob - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(prefix + mid) <= tile) lo = mid; else hi = mid - 1;
+        if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
       }
       const GemmProblem P = probs[lo];
       if (P.skip && __ldcg(P.skip)) return;
       const int tiles_m = (P.m + BM - 1) / BM;
-      const int t = tile - __ldg(prefix + lo);
+      const int t = tile - prefix[lo];
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
       if (P.lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
       const int K = P.k;
@@ -128,6 +135,33 @@ namespace hssmf_b200 {
           }
       }
     }
+
+    template<bool TA, bool TB>
+    __global__ void __launch_bounds__(THREADS)
+    gemm_grouped_kernel(const GemmProblem* __restrict__ probs, const int* __restrict__ prefix,
+                        int nprob, double alpha, double beta) {
+      gemm_body<TA, TB>(probs, prefix, nprob, alpha, beta);
+    }
+
+    template<bool TA, bool TB>
+    __global__ void __launch_bounds__(THREADS)
+    gemm_param_kernel(const __grid_constant__ GemmParam b, double alpha, double beta) {
+      gemm_body<TA, TB>(b.p, b.pre, b.nprob, alpha, beta);
+    }
+
+    void set_gemm_attrs() {
+      static bool attr = false;
+      if (attr) return;
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      attr = true;
+    }
   }  // namespace
 
   std::vector<int> gemm_tile_prefix(const std::vector<GemmProblem>& p) {
@@ -147,14 +181,7 @@ namespace hssmf_b200 {
                 cudaStream_t s) {
     if (b.nprob == 0 || b.tiles == 0) return;
     const bool TA = ta != 'N', TB = tb != 'N';
-    static bool attr = false;
-    if (!attr) {
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      attr = true;
-    }
+    set_gemm_attrs();
     dim3 grid(b.tiles), block(THREADS);
     if (!TA && !TB) gemm_grouped_kernel<false, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
     else if (TA && !TB) gemm_grouped_kernel<true, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
@@ -165,31 +192,34 @@ namespace hssmf_b200 {
 
   void gemm_run_host(const std::vector<GemmProblem>& p, char ta, char tb, double alpha,
                      double beta, cudaStream_t s) {
-    std::vector<GemmProblem> q;
-    for (const auto& x : p)
-      if (x.m > 0 && x.n > 0) q.push_back(x);
-    if (q.empty()) return;
-    auto pre = gemm_tile_prefix(q);
-    const size_t pb = q.size() * sizeof(GemmProblem), xb = pre.size() * sizeof(int);
-    if (Staging* st = current_staging(s)) {
-      std::vector<char> buf(pb + xb);
-      std::memcpy(buf.data(), q.data(), pb);
-      std::memcpy(buf.data() + pb, pre.data(), xb);
-      if (void* d = st->put(buf.data(), buf.size())) {
-        GemmBatchDev b{(const GemmProblem*)d, (const int*)((char*)d + pb), (int)q.size(),
-                       pre.back()};
-        gemm_run(b, ta, tb, alpha, beta, s);
-        return;
+    const bool TA = ta != 'N', TB = tb != 'N';
+    set_gemm_attrs();
+    GemmParam b;
+    b.nprob = 0;
+    b.pre[0] = 0;
+    auto flush = [&] {
+      if (!b.nprob) return;
+      const int tiles = b.pre[b.nprob];
+      if (tiles) {
+        dim3 grid(tiles), block(THREADS);
+        if (!TA && !TB) gemm_param_kernel<false, false><<<grid, block, SMEM, s>>>(b, alpha, beta);
+        else if (TA && !TB) gemm_param_kernel<true, false><<<grid, block, SMEM, s>>>(b, alpha, beta);
+        else if (!TA && TB) gemm_param_kernel<false, true><<<grid, block, SMEM, s>>>(b, alpha, beta);
+        else gemm_param_kernel<true, true><<<grid, block, SMEM, s>>>(b, alpha, beta);
+        HSSMF_LAUNCH_CHECK();
       }
+      b.nprob = 0;
+    };
+    // problems of one call are independent (distinct outputs), so a list
+    // longer than one parameter block is split over several launches
+    for (const auto& x : p) {
+      if (x.m <= 0 || x.n <= 0) continue;
+      if (b.nprob == kParamProbs) flush();
+      b.p[b.nprob] = x;
+      b.pre[b.nprob + 1] = b.pre[b.nprob] + ceil_div(x.m, BM) * ceil_div(x.n, BN);
+      b.nprob++;
     }
-    void* d = nullptr;
-    HSSMF_CUDA(cudaMallocAsync(&d, pb + xb, s));
-    HSSMF_CUDA(cudaMemcpyAsync(d, q.data(), pb, cudaMemcpyHostToDevice, s));
-    HSSMF_CUDA(cudaMemcpyAsync((char*)d + pb, pre.data(), xb, cudaMemcpyHostToDevice, s));
-    GemmBatchDev b{(const GemmProblem*)d, (const int*)((char*)d + pb), (int)q.size(),
-                   pre.back()};
-    gemm_run(b, ta, tb, alpha, beta, s);
-    HSSMF_CUDA(cudaFreeAsync(d, s));
+    flush();
   }
 
 }  // namespace hssmf_b200

@@ -6,6 +6,7 @@
 #include <climits>
 
 #include "gemm.cuh"
+#include "staging.cuh"
 
 namespace hssmf_b200 {
 
@@ -23,7 +24,8 @@ namespace hssmf_b200 {
     }
 
     // dynamic shared memory of one CTA (rows = own contiguous row block):
-    //   Lp[rows * nb]  panel columns of own rows       (double)
+    //   Lp[nb * rows]  panel columns of own rows, column-major (double) so
+    //                  that the per-row dot products of a warp hit distinct banks
     //   dg[rows]       residual norms^2 of own rows    (double)
     //   orig[n], pos[n] replicated position bookkeeping (int)
     //   flg[rows]      pivoted flags of own rows        (int)
@@ -96,7 +98,7 @@ namespace hssmf_b200 {
           pos[i] = __ldcg(T.pos_of + i);
         }
       }
-      for (int e = tid; e < nr * nb; e += GT) Lp[e] = 0.0;
+      for (int e = tid; e < rows * nb; e += GT) Lp[e] = 0.0;
       if (tid == 0) s_r11 = init ? 0.0 : __ldcg(T.r11);
       __syncthreads();
       int j = k0, stopped = 0, cert = 0;
@@ -154,7 +156,7 @@ namespace hssmf_b200 {
         const double ljj = s_ljj;
         const int owner = min(pj / rows, CL - 1);
         // pivot row's panel values from its owner (DSMEM)
-        if (tid < jj) prow[tid] = cl.map_shared_rank(Lp, owner)[(size_t)(pj - owner * rows) * nb + tid];
+        if (tid < jj) prow[tid] = cl.map_shared_rank(Lp, owner)[(size_t)tid * rows + (pj - owner * rows)];
         __syncthreads();
         // CPQR column swap of positions j and pos(pj), replicated in every CTA
         if (tid == 0) {
@@ -171,19 +173,21 @@ namespace hssmf_b200 {
         __syncthreads();
         for (int i = tid; i < nr; i += GT) {
           const int gi = r0 + i;
-          if (flg[i]) continue;
+          if (flg[i]) {
+            T.L[gi + (size_t)j * n] = 0.0;
+            continue;
+          }
           if (gi == pj) {
             flg[i] = 1;
-            Lp[(size_t)i * nb + jj] = ljj;
+            Lp[(size_t)jj * rows + i] = ljj;
             T.L[gi + (size_t)j * n] = ljj;
             continue;
           }
           // lower triangle of G only (the trailing updates skip the upper one)
           double s = gi >= pj ? gcol[gi] : T.G[pj + (size_t)gi * n];
-          const double* lr = Lp + (size_t)i * nb;
-          for (int q = 0; q < jj; q++) s -= lr[q] * prow[q];
+          for (int q = 0; q < jj; q++) s -= Lp[(size_t)q * rows + i] * prow[q];
           const double lo = s / ljj;
-          Lp[(size_t)i * nb + jj] = lo;
+          Lp[(size_t)jj * rows + i] = lo;
           T.L[gi + (size_t)j * n] = lo;
           double dd = dg[i] - lo * lo;
           if (dd < 0.0) dd = 0.0;
@@ -222,7 +226,7 @@ namespace hssmf_b200 {
 
   void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
                          cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
-                         double* flops) {
+                         double* flops, const std::function<void()>& before_sync) {
     const int nt = (int)tasks.size();
     rank.assign(nt, 0);
     cert.assign(nt, 0);
@@ -248,8 +252,13 @@ namespace hssmf_b200 {
     if (gram_smem(max_n, rows, nb) > (size_t)kSmemCap)
       throw CudaError("gram id: node too large for the cluster shared memory");
     GramTask* d = nullptr;
-    HSSMF_CUDA(cudaMallocAsync((void**)&d, nt * sizeof(GramTask), s));
-    HSSMF_CUDA(cudaMemcpyAsync(d, tasks.data(), nt * sizeof(GramTask), cudaMemcpyHostToDevice, s));
+    bool owned = false;
+    if (Staging* st = current_staging(s)) d = static_cast<GramTask*>(st->put(tasks.data(), nt * sizeof(GramTask)));
+    if (!d) {
+      owned = true;
+      HSSMF_CUDA(cudaMallocAsync((void**)&d, nt * sizeof(GramTask), s));
+      HSSMF_CUDA(cudaMemcpyAsync(d, tasks.data(), nt * sizeof(GramTask), cudaMemcpyHostToDevice, s));
+    }
     std::vector<int> hst(3 * nt);
     // all panels are queued without host round trips: a finished task's
     // panel kernel returns at once and its trailing GEMM is skipped on device
@@ -283,15 +292,24 @@ namespace hssmf_b200 {
       if (flops) *flops += 0.5 * gemm_flops(p);
       gemm_run_host(p, 'N', 'T', -1.0, 1.0, s);
     }
-    for (int t = 0; t < nt; t++)
-      HSSMF_CUDA(cudaMemcpyAsync(&hst[3 * t], tasks[t].state, 3 * sizeof(int),
+    // the tasks' state triples are contiguous when the caller packs them
+    bool packed = true;
+    for (int t = 1; t < nt; t++) packed &= tasks[t].state == tasks[0].state + 3 * t;
+    if (packed) {
+      HSSMF_CUDA(cudaMemcpyAsync(hst.data(), tasks[0].state, 3 * nt * sizeof(int),
                                  cudaMemcpyDeviceToHost, s));
-    HSSMF_CUDA(cudaStreamSynchronize(s));
+    } else {
+      for (int t = 0; t < nt; t++)
+        HSSMF_CUDA(cudaMemcpyAsync(&hst[3 * t], tasks[t].state, 3 * sizeof(int),
+                                   cudaMemcpyDeviceToHost, s));
+    }
+    if (before_sync) before_sync();
+    stream_sync(s);
     for (int t = 0; t < nt; t++) {
       rank[t] = hst[3 * t];
       cert[t] = hst[3 * t + 2];
     }
-    HSSMF_CUDA(cudaFreeAsync(d, s));
+    if (owned) HSSMF_CUDA(cudaFreeAsync(d, s));
   }
 
 }  // namespace hssmf_b200

@@ -13,11 +13,12 @@
 // level-2 sweep over d x n per elimination step.
 //
 // Accuracy: R (hence the ID coefficients) carries kappa(R11)^2 u relative
-// error; the engine uses this route only when eps >= 1e-5 (kappa(R11) <~
+// error; the engine uses this route only when eps >= 5e-5 (kappa(R11) <~
 // 1/eps), where that is below 1e-6 relative. Smaller tolerances use the
 // Householder CPQR (cpqr.cuh).
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -28,7 +29,8 @@ namespace hssmf_b200 {
 
   struct GramTask {
     double* G;       // n x n working Gram matrix (ld n), destroyed
-    double* L;       // n x kcap Cholesky columns by original index (ld n), zeroed
+    double* L;       // n x kcap Cholesky columns by original index (ld n); columns
+                     // below the rank are written in full (0 on pivoted rows)
     double* dg;      // n residual norms^2
     int* flag;       // n pivoted flags (zeroed)
     int* orig_at;    // n: original column at each CPQR position (the ID perm)
@@ -39,9 +41,11 @@ namespace hssmf_b200 {
   };
 
   // runs the factorization of all tasks; returns per task (rank, certified)
-  // (one host sync per panel of nb steps to retire finished tasks)
+  // after ONE host sync; before_sync may enqueue more device->host reads
+  // that the same sync then covers
   void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
                          cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
-                         double* flops = nullptr);
+                         double* flops = nullptr,
+                         const std::function<void()>& before_sync = {});
 
 }  // namespace hssmf_b200

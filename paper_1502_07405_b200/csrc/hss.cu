@@ -14,23 +14,31 @@
 #include "gram_id.cuh"
 #include "rng.cuh"
 #include "staging.cuh"
+#include "arena.cuh"
 
 namespace hssmf_b200 {
 
   namespace {
 
+    // device buffer; served by the current DevArena of its stream when there is
+    // one (HssMatrixDev entry points install the front's arena)
     template<typename T> struct DBuf {
       T* p = nullptr;
       size_t n = 0;
       cudaStream_t s = nullptr;
+      DevArena* ar = nullptr;
+      size_t cls = 0;
       DBuf() = default;
       DBuf(const DBuf&) = delete;
       DBuf& operator=(const DBuf&) = delete;
-      DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+      DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), ar(o.ar), cls(o.cls) {
+        o.p = nullptr;
+        o.n = 0;
+      }
       DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
           free();
-          p = o.p; n = o.n; s = o.s;
+          p = o.p; n = o.n; s = o.s; ar = o.ar; cls = o.cls;
           o.p = nullptr; o.n = 0;
         }
         return *this;
@@ -39,15 +47,22 @@ namespace hssmf_b200 {
         free();
         s = st;
         n = cnt;
-        if (cnt) HSSMF_CUDA(cudaMallocAsync((void**)&p, cnt * sizeof(T), s));
+        if (!cnt) return;
+        ar = current_arena(st);
+        if (ar) p = static_cast<T*>(ar->get(cnt * sizeof(T), &cls));
+        else HSSMF_CUDA(cudaMallocAsync((void**)&p, cnt * sizeof(T), s));
       }
       void zero() {
         if (n) HSSMF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
       }
       void free() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) {
+          if (ar) ar->put(p, cls);
+          else cudaFreeAsync(p, s);
+        }
         p = nullptr;
         n = 0;
+        ar = nullptr;
       }
       ~DBuf() { free(); }
     };
@@ -88,12 +103,16 @@ namespace hssmf_b200 {
         h.insert(h.end(), v.begin(), v.end());
         return o;
       }
+      const int* t = nullptr;  // transient copy in the staging ring
       void upload(cudaStream_t s) {
+        t = nullptr;
+        if (Staging* st = current_staging(s))
+          if (!h.empty()) t = static_cast<const int*>(st->put(h.data(), h.size() * sizeof(int)));
+        if (t) return;
         d.alloc(std::max<size_t>(h.size(), 1), s);
-        if (!h.empty())
-          HSSMF_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+        h2d(d.p, h.data(), h.size() * sizeof(int), s);
       }
-      const int* at(size_t o) const { return d.p + o; }
+      const int* at(size_t o) const { return (t ? t : d.p) + o; }
     };
 
     enum { UNCOMPRESSED = 0, PARTIAL = 1, DONE = 2 };
@@ -149,7 +168,13 @@ namespace hssmf_b200 {
     int size() const { return end - begin; }
   };
 
+  namespace {
+    std::atomic<bool> g_phase_timing{false};
+  }
+  void hss_set_phase_timing(bool on) { g_phase_timing = on; }
+
   struct HssImpl {
+    DevArena arena;  // first member: outlives every buffer below
     cudaStream_t s;
     ClusterTree tree;
     int m = 0;
@@ -164,7 +189,7 @@ namespace hssmf_b200 {
     DBuf<double> scale, one;
     int d = 0, rounds = 0;
     double flops = 0;
-    bool gram = false;  // ID route: Gram / pivoted Cholesky (eps >= 1e-5) or Householder
+    bool gram = false;  // ID route: Gram / pivoted Cholesky (eps >= 5e-5) or Householder
     // top factorization
     bool partial = false;
     DBuf<double> Z;
@@ -184,13 +209,15 @@ namespace hssmf_b200 {
     struct Ph {
       HssImpl* h;
       int id;
-      cudaEvent_t a;
+      cudaEvent_t a = nullptr;
       double f0;
       Ph(HssImpl* hh, int i) : h(hh), id(i), f0(hh->flops) {
+        if (!g_phase_timing) return;
         HSSMF_CUDA(cudaEventCreate(&a));
         HSSMF_CUDA(cudaEventRecord(a, h->s));
       }
       ~Ph() {
+        if (!a) return;
         cudaEvent_t b;
         if (cudaEventCreate(&b) == cudaSuccess && cudaEventRecord(b, h->s) == cudaSuccess)
           h->phev.push_back({id, a, b, h->flops - f0});
@@ -211,7 +238,7 @@ namespace hssmf_b200 {
     }
     ~HssImpl() { collect_phases(); }
 
-    explicit HssImpl(cudaStream_t st) : s(st) {}
+    explicit HssImpl(cudaStream_t st) : arena(st), s(st) {}
 
     // ---------------------------------------------------------- compression
     void init_tree(const ClusterTree& t) {
@@ -246,8 +273,7 @@ namespace hssmf_b200 {
       m = t.nodes.back().end;
       init_tree(t);
       seeds.alloc(std::max<size_t>(sd.size(), 1), s);
-      HSSMF_CUDA(cudaMemcpyAsync(seeds.p, sd.data(), sd.size() * sizeof(long long),
-                                 cudaMemcpyHostToDevice, s));
+      h2d(seeds.p, sd.data(), sd.size() * sizeof(long long), s);
       R.init(m, s);
       Sr.init(m, s);
       Sc.init(m, s);
@@ -255,10 +281,10 @@ namespace hssmf_b200 {
       scale.zero();
       one.alloc(1, s);
       const double h1 = 1.0;
-      HSSMF_CUDA(cudaMemcpyAsync(one.p, &h1, sizeof(double), cudaMemcpyHostToDevice, s));
+      h2d(one.p, &h1, sizeof(double), s);
       d = std::min(o.d0, o.max_rank + o.p);
       rounds = 0;
-      gram = o.eps >= 1e-5;
+      gram = o.eps >= 5e-5;
       if (const char* e = getenv("HSSMF_ID_ALGO")) {
         if (!strcmp(e, "householder")) gram = false;
         if (!strcmp(e, "gram")) gram = true;
@@ -289,7 +315,7 @@ namespace hssmf_b200 {
         }
         double sc = 0;
         HSSMF_CUDA(cudaMemcpyAsync(&sc, scale.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-        HSSMF_CUDA(cudaStreamSynchronize(s));
+        stream_sync(s);
         const int cap_id = std::min(d - o.p, o.max_rank);
         const double abs_tol = o.eps * sc;
         int fail = -1;
@@ -482,27 +508,55 @@ namespace hssmf_b200 {
       flops += gg.flops;
       if (!gram) return;
       // G0 += S_new S_new^T  (only the appended sample columns)
-      std::vector<GemmProblem> gp;
+      // (a node's first accumulation overwrites: beta = 0, no zero fill; the
+      // Gram route reads the lower triangle only)
+      std::vector<GemmProblem> gp, gp0;
       for (int n : act) {
         auto& N = nodes[n];
         const int mt = N.mt, cb0 = N.gram_cols, nc = d - cb0;
         if (nc <= 0 || !mt) continue;
-        if (!N.G0r.p) {
+        const bool first = !N.G0r.p;
+        if (first) {
           N.G0r.alloc((size_t)mt * mt, s);
           N.G0c.alloc((size_t)mt * mt, s);
-          N.G0r.zero();
-          N.G0c.zero();
         }
         GemmProblem gr{N.slr.col(cb0), N.slr.col(cb0), N.G0r.p, mt, mt, nc, mt, mt, mt};
         GemmProblem gc{N.slc.col(cb0), N.slc.col(cb0), N.G0c.p, mt, mt, nc, mt, mt, mt};
-        gr.lower = gc.lower = 1;  // the Gram route reads the lower triangle only
-        gp.push_back(gr);
-        gp.push_back(gc);
+        gr.lower = gc.lower = 1;
+        (first ? gp0 : gp).push_back(gr);
+        (first ? gp0 : gp).push_back(gc);
         N.gram_cols = d;
       }
-      flops += gemm_flops(gp);
+      flops += gemm_flops(gp) + gemm_flops(gp0);
+      gemm_run_host(gp0, 'N', 'T', 1.0, 0.0, s);
       gemm_run_host(gp, 'N', 'T', 1.0, 1.0, s);
     }
+
+    // all ID permutations of a batch in one device->host read: gathered into
+    // one packed buffer, read back before the batch's single host sync
+    struct PermReadback {
+      DBuf<int> packed;
+      std::vector<int> h;
+      std::vector<long long> off;
+      void enqueue(std::vector<DBuf<int>>& perm, int nt, cudaStream_t s) {
+        std::vector<IntSeg> segs;
+        off.assign(nt + 1, 0);
+        for (int t = 0; t < nt; t++) {
+          const int n = perm[t].n ? (int)perm[t].n - 1 : 0;
+          segs.push_back({perm[t].p, n, off[t]});
+          off[t + 1] = off[t] + n;
+        }
+        packed.alloc(off[nt] + 1, s);
+        int_gather_run(segs, packed.p, s);
+        h.resize(off[nt] + 1);
+        HSSMF_CUDA(cudaMemcpyAsync(h.data(), packed.p, off[nt] * sizeof(int), cudaMemcpyDeviceToHost, s));
+      }
+      void unpack(std::vector<std::vector<int>>& hp) {
+        const int nt = (int)off.size() - 1;
+        hp.assign(nt, {});
+        for (int t = 0; t < nt; t++) hp[t].assign(h.begin() + off[t], h.begin() + off[t + 1]);
+      }
+    };
 
     // IDs of the local samples; certified nodes become Done
     // (compress_pass, hss_compress.hpp:250-297)
@@ -512,7 +566,7 @@ namespace hssmf_b200 {
     void gram_ids(const std::vector<int>& act, int cap_id, double abs_tol,
                   std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
                   std::vector<DBuf<int>>& perm, DBuf<int>& outs, std::vector<CpqrTask>& tasks,
-                  std::vector<int>& ho) {
+                  std::vector<int>& ho, std::vector<std::vector<int>>& hp) {
       const int na = (int)act.size(), nt = 2 * na;
       std::vector<DBuf<double>> Gw(nt), L(nt), dg(nt);
       std::vector<DBuf<int>> flag(nt), pos(nt);
@@ -534,7 +588,6 @@ namespace hssmf_b200 {
             HSSMF_CUDA(cudaMemcpyAsync(Gw[t].p, G0.p, (size_t)mt * mt * sizeof(double),
                                        cudaMemcpyDeviceToDevice, s));
           L[t].alloc((size_t)mt * kcap + 1, s);
-          L[t].zero();
           dg[t].alloc(mt + 1, s);
           flag[t].alloc(mt + 1, s);
           pos[t].alloc(mt + 1, s);
@@ -544,10 +597,13 @@ namespace hssmf_b200 {
         }
       }
       std::vector<int> rk, ce;
+      PermReadback prb;
       {
         Ph ph_(this, 3);
-        gram_cholesky_run(gt, o.eps, abs_tol, s, rk, ce, &flops);
+        gram_cholesky_run(gt, o.eps, abs_tol, s, rk, ce, &flops,
+                          [&] { prb.enqueue(perm, nt, s); });
       }
+      prb.unpack(hp);
       ho.assign(2 * nt, 0);
       std::vector<CopyDesc> rc;
       for (int t = 0; t < nt; t++) {
@@ -562,8 +618,7 @@ namespace hssmf_b200 {
                     outs.p + 2 * t};
       }
       index_copy_run(rc, s);
-      HSSMF_CUDA(cudaMemcpyAsync(outs.p, ho.data(), ho.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-      HSSMF_CUDA(cudaStreamSynchronize(s));
+      h2d(outs.p, ho.data(), ho.size() * sizeof(int), s);
     }
 
     void id_batch(const std::vector<int>& act, int cap_id, double abs_tol, int& fail) {
@@ -574,9 +629,10 @@ namespace hssmf_b200 {
       outs.alloc(4 * na, s);
       std::vector<CpqrTask> tasks(2 * na);
       std::vector<int> ho(4 * na);
+      std::vector<std::vector<int>> hp;
       if (gram) {
-        gram_ids(act, cap_id, abs_tol, Y, X, perm, outs, tasks, ho);
-        id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho);
+        gram_ids(act, cap_id, abs_tol, Y, X, perm, outs, tasks, ho, hp);
+        id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho, hp);
         return;
       }
       std::vector<CopyDesc> tr;
@@ -600,26 +656,28 @@ namespace hssmf_b200 {
       index_copy_run(tr, s);
       DBuf<CpqrTask> dt;
       dt.alloc(tasks.size(), s);
-      HSSMF_CUDA(cudaMemcpyAsync(dt.p, tasks.data(), tasks.size() * sizeof(CpqrTask),
-                                 cudaMemcpyHostToDevice, s));
+      h2d(dt.p, tasks.data(), tasks.size() * sizeof(CpqrTask), s);
       {
         Ph ph_(this, 3);
         cpqr_run(dt.p, (int)tasks.size(), d, max_n, o.eps, abs_tol, s);
       }
       HSSMF_CUDA(cudaMemcpyAsync(ho.data(), outs.p, ho.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
-      HSSMF_CUDA(cudaStreamSynchronize(s));
+      PermReadback prb;
+      prb.enqueue(perm, 2 * na, s);
+      stream_sync(s);
+      prb.unpack(hp);
       for (int q = 0; q < 2 * na; q++) {
         const int mt = tasks[q].n, k = ho[2 * q];
         flops += 2.0 * d * mt;
         for (int j = 0; j < k; j++) flops += 4.0 * (d - j) * (mt - j);
       }
-      id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho);
+      id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho, hp);
     }
 
     void id_finalize(const std::vector<int>& act, int cap_id, int& fail,
                      std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
                      std::vector<DBuf<int>>& perm, std::vector<CpqrTask>& tasks,
-                     std::vector<int>& ho) {
+                     std::vector<int>& ho, std::vector<std::vector<int>>& hpt) {
       Ph ph4(this, 4);
       const int na = (int)act.size();
       (void)Y;
@@ -654,20 +712,13 @@ namespace hssmf_b200 {
       if (!solve_tasks.empty()) {
         DBuf<CpqrTask> ds;
         ds.alloc(solve_tasks.size(), s);
-        HSSMF_CUDA(cudaMemcpyAsync(ds.p, solve_tasks.data(), solve_tasks.size() * sizeof(CpqrTask),
-                                   cudaMemcpyHostToDevice, s));
+        h2d(ds.p, solve_tasks.data(), solve_tasks.size() * sizeof(CpqrTask), s);
         id_solve_run(ds.p, (int)solve_tasks.size(), max_rank_ok, max_cols, s);
       }
-      // perms to the host (skeleton index bookkeeping)
+      // perms on the host already (read back with the ranks)
       std::vector<std::vector<int>> hp(2 * okq.size());
       for (size_t i = 0; i < okq.size(); i++)
-        for (int side = 0; side < 2; side++) {
-          const int t = 2 * okq[i] + side;
-          hp[2 * i + side].resize(tasks[t].n);
-          HSSMF_CUDA(cudaMemcpyAsync(hp[2 * i + side].data(), perm[t].p, tasks[t].n * sizeof(int),
-                                     cudaMemcpyDeviceToHost, s));
-        }
-      HSSMF_CUDA(cudaStreamSynchronize(s));
+        for (int side = 0; side < 2; side++) hp[2 * i + side] = std::move(hpt[2 * okq[i] + side]);
       // bases, skeletons, reduced samples
       std::vector<CopyDesc> ce, cg;
       std::vector<BasisApplyJob> jobs;
@@ -686,13 +737,15 @@ namespace hssmf_b200 {
         // E = coeffs^H padded to rank r (BasisId ctor + pad_to, hss_matrix.hpp:21-58)
         N.Eu.alloc((size_t)kk * r + 1, s);
         N.Ev.alloc((size_t)kk * r + 1, s);
-        N.Eu.zero();
-        N.Ev.zero();
         for (int side = 0; side < 2; side++) {
           const int kid = side ? kc : kr, t = r - kid;
+          DBuf<double>& E = side ? N.Ev : N.Eu;
           if (kid && kk)
             ce.push_back(cd(X[2 * q + side].p + (size_t)t * kid, kid, 1, nullptr, 0, nullptr, 0,
-                            (side ? N.Ev : N.Eu).p, kk, nullptr, 0, nullptr, 0, kk, kid));
+                            E.p, kk, nullptr, 0, nullptr, 0, kk, kid));
+          // zero padding columns [kid, r) only
+          if (kk && r > kid)
+            HSSMF_CUDA(cudaMemsetAsync(E.p + (size_t)kk * kid, 0, (size_t)kk * (r - kid) * sizeof(double), s));
         }
         // skeleton indices
         std::vector<int> rows_all, cols_all;
@@ -715,8 +768,8 @@ namespace hssmf_b200 {
         N.d_ir.alloc(r + 1, s);
         N.d_ic.alloc(r + 1, s);
         if (r) {
-          HSSMF_CUDA(cudaMemcpyAsync(N.d_ir.p, N.ir.data(), r * sizeof(int), cudaMemcpyHostToDevice, s));
-          HSSMF_CUDA(cudaMemcpyAsync(N.d_ic.p, N.ic.data(), r * sizeof(int), cudaMemcpyHostToDevice, s));
+          h2d(N.d_ir.p, N.ir.data(), r * sizeof(int), s);
+          h2d(N.d_ic.p, N.ic.data(), r * sizeof(int), s);
         }
         // reduced samples sr = S_loc(skel rows), sc likewise
         N.sr.init(r, s);
@@ -1252,14 +1305,17 @@ namespace hssmf_b200 {
   void HssMatrixDev::compress(const double* A, long long lda, const ClusterTree& tree,
                               const std::vector<long long>& seeds, const HssOpts& o) {
     StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena);
     d_->compress(A, lda, tree, seeds, o);
   }
   void HssMatrixDev::ulv_full() {
     StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena);
     d_->ulv_full();
   }
   void HssMatrixDev::ulv_partial(double* update, long long ldu) {
     StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena);
     d_->ulv_partial(update, ldu);
   }
   void HssMatrixDev::drop_dense() {
@@ -1278,21 +1334,26 @@ namespace hssmf_b200 {
     d_->R.release();
     d_->Sr.release();
     d_->Sc.release();
+    d_->arena.trim();
   }
   void HssMatrixDev::set_stream(cudaStream_t s) {
     d_->collect_phases();
+    d_->arena.rebind(s);
     d_->s = s;
   }
   void HssMatrixDev::solve_full(double* x) {
     StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena);
     d_->solve_full(x);
   }
   void HssMatrixDev::partial_forward(const double* b1, double* bupd) {
     StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena);
     d_->partial_forward(b1, bupd);
   }
   void HssMatrixDev::partial_backward(double* x1, const double* x2) {
     StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena);
     d_->partial_backward(x1, x2);
   }
   int HssMatrixDev::rows() const { return d_->m; }
@@ -1325,6 +1386,7 @@ namespace hssmf_b200 {
     return s;
   }
   double HssMatrixDev::flops() const { return d_->flops; }
+  size_t HssMatrixDev::arena_bytes() const { return d_->arena.slab_bytes(); }
   std::vector<HssPhaseStat> HssMatrixDev::phase_stats() {
     d_->collect_phases();
     std::vector<HssPhaseStat> v(kHssPhases);

@@ -51,6 +51,9 @@ namespace hssmf_b200 {
 
   struct HssImpl;
 
+  // per-phase CUDA-event timing of the HSS path (profiling / HSSMF_DEBUG only)
+  void hss_set_phase_timing(bool on);
+
   // device-time phases of the HSS path (profiling)
   constexpr int kHssPhases = 9;
   inline const char* hss_phase_name(int i) {
@@ -98,6 +101,7 @@ namespace hssmf_b200 {
     void ranks(std::vector<int>& u, std::vector<int>& v) const;
     long long stored_scalars() const;
     double flops() const;
+    size_t arena_bytes() const;  // device slabs held by the front's block cache
     std::vector<HssPhaseStat> phase_stats();
     void restore_phase_stats(const std::vector<HssPhaseStat>&) {}
 

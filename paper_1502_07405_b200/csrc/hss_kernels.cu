@@ -9,8 +9,18 @@ namespace hssmf_b200 {
   namespace {
     constexpr int CPB = 1024;  // elements per block for index_copy
 
-    __global__ void index_copy_kernel(const CopyDesc* __restrict__ ds,
-                                      const long long* __restrict__ pre, int nd) {
+    constexpr int kParamCopies = 64;
+    struct CopyParam {
+      int nd;
+      long long pre[kParamCopies + 1];
+      CopyDesc d[kParamCopies];
+    };
+
+    // descriptors in a __grid_constant__ parameter block (no upload)
+    __global__ void index_copy_kernel(const __grid_constant__ CopyParam P) {
+      const CopyDesc* ds = P.d;
+      const long long* pre = P.pre;
+      const int nd = P.nd;
       int lo = 0, hi = nd - 1;
       const long long b = blockIdx.x;
       while (lo < hi) {
@@ -30,6 +40,17 @@ namespace hssmf_b200 {
         double* o = d.dst + di + dj * d.ldd;
         *o = d.accumulate ? *o + v : v;
       }
+    }
+
+    constexpr int kParamSegs = 128;
+    struct SegParam {
+      int ns;
+      IntSeg g[kParamSegs];
+    };
+    __global__ void int_gather_kernel(const __grid_constant__ SegParam P, int* __restrict__ dst) {
+      const IntSeg& g = P.g[blockIdx.y];
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x)
+        dst[g.off + i] = g.src[i];
     }
 
     __global__ void maxabs_kernel(const double* __restrict__ a, long long lda, int m, int n,
@@ -267,20 +288,45 @@ namespace hssmf_b200 {
   }  // namespace
 
   void index_copy_run(const std::vector<CopyDesc>& d0, cudaStream_t s) {
-    std::vector<CopyDesc> d;
-    for (const auto& x : d0)
-      if (x.nr > 0 && (x.nc > 0 || x.diag)) d.push_back(x);
-    if (d.empty()) return;
-    std::vector<long long> pre(d.size() + 1, 0);
-    for (size_t i = 0; i < d.size(); i++)
-      pre[i + 1] = pre[i] + ((d[i].diag ? (long long)d[i].nr : (long long)d[i].nr * d[i].nc) +
-                             CPB - 1) / CPB;
-    auto dd = upload_async(d, s);
-    auto dp = upload_async(pre, s);
-    index_copy_kernel<<<(unsigned)pre.back(), 256, 0, s>>>(dd.p, dp.p, (int)d.size());
-    HSSMF_LAUNCH_CHECK();
-    release_async(dd, s);
-    release_async(dp, s);
+    CopyParam P;
+    P.nd = 0;
+    P.pre[0] = 0;
+    auto flush = [&] {
+      if (!P.nd) return;
+      index_copy_kernel<<<(unsigned)P.pre[P.nd], 256, 0, s>>>(P);
+      HSSMF_LAUNCH_CHECK();
+      P.nd = 0;
+    };
+    // descriptors of one call write disjoint outputs: long lists are split
+    for (const auto& x : d0) {
+      if (x.nr <= 0 || (x.nc <= 0 && !x.diag)) continue;
+      if (P.nd == kParamCopies) flush();
+      P.d[P.nd] = x;
+      P.pre[P.nd + 1] =
+          P.pre[P.nd] + ((x.diag ? (long long)x.nr : (long long)x.nr * x.nc) + CPB - 1) / CPB;
+      P.nd++;
+    }
+    flush();
+  }
+
+  void int_gather_run(const std::vector<IntSeg>& segs, int* dst, cudaStream_t s) {
+    SegParam P;
+    P.ns = 0;
+    int maxn = 0;
+    auto flush = [&] {
+      if (!P.ns) return;
+      int_gather_kernel<<<dim3(std::min(ceil_div(maxn, 256), 64), P.ns), 256, 0, s>>>(P, dst);
+      HSSMF_LAUNCH_CHECK();
+      P.ns = 0;
+      maxn = 0;
+    };
+    for (const auto& g : segs) {
+      if (g.n <= 0) continue;
+      if (P.ns == kParamSegs) flush();
+      P.g[P.ns++] = g;
+      maxn = std::max(maxn, g.n);
+    }
+    flush();
   }
 
   void maxabs_run(const double* a, long long lda, int m, int n, double* out, cudaStream_t s) {

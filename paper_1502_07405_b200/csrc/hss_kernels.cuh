@@ -39,6 +39,14 @@ namespace hssmf_b200 {
   // runs a host list of descriptors (uploads them stream-ordered)
   void index_copy_run(const std::vector<CopyDesc>& d, cudaStream_t s);
 
+  // dst[off + i] = src[i], i < n, for every segment (one launch per 128)
+  struct IntSeg {
+    const int* src;
+    int n;
+    long long off;
+  };
+  void int_gather_run(const std::vector<IntSeg>& segs, int* dst, cudaStream_t s);
+
   // *out = max(*out, max |a(i, j)|) over an m x n block (ld lda); out is a
   // device double holding a non-negative value (bitwise int64 ordering)
   void maxabs_run(const double* a, long long lda, int m, int n, double* out, cudaStream_t s);

@@ -25,7 +25,7 @@ namespace hssmf_b200 {
     cudaFree(d_);
   }
 
-  void* Staging::put(const void* src, size_t n) {
+  char* Staging::stage(const void* src, size_t n, char** dev) {
     const size_t a = (n + 255) & ~size_t(255);
     if (a > chunk_) return nullptr;
     if (head_ + a > chunk_) {
@@ -40,11 +40,33 @@ namespace hssmf_b200 {
       }
     }
     char* h = h_ + (size_t)cur_ * chunk_ + head_;
-    char* d = d_ + (size_t)cur_ * chunk_ + head_;
+    *dev = d_ + (size_t)cur_ * chunk_ + head_;
     std::memcpy(h, src, n);
-    HSSMF_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s_));
     head_ += a;
+    return h;
+  }
+
+  void* Staging::put(const void* src, size_t n) {
+    char* d = nullptr;
+    char* h = stage(src, n, &d);
+    if (!h) return nullptr;
+    HSSMF_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s_));
     return d;
+  }
+
+  bool Staging::copy_to(void* dst, const void* src, size_t n) {
+    char* d = nullptr;
+    char* h = stage(src, n, &d);
+    if (!h) return false;
+    HSSMF_CUDA(cudaMemcpyAsync(dst, h, n, cudaMemcpyHostToDevice, s_));
+    return true;
+  }
+
+  void h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
+    if (!n) return;
+    if (Staging* st = current_staging(s))
+      if (st->copy_to(dst, src, n)) return;
+    HSSMF_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s));
   }
 
   Staging* staging_for(cudaStream_t s) {

@@ -17,15 +17,19 @@ namespace hssmf_b200 {
 
   class Staging {
    public:
-    explicit Staging(cudaStream_t s, size_t chunk_bytes = 256 << 10, int chunks = 32);
+    explicit Staging(cudaStream_t s, size_t chunk_bytes = 256 << 10, int chunks = 64);
     ~Staging();
     Staging(const Staging&) = delete;
     Staging& operator=(const Staging&) = delete;
     cudaStream_t stream() const { return s_; }
     // device copy of n host bytes, stream-ordered; nullptr if n exceeds a chunk
     void* put(const void* src, size_t n);
+    // stream-ordered copy of n host bytes to the device address dst through a
+    // pinned chunk (false if n exceeds a chunk)
+    bool copy_to(void* dst, const void* src, size_t n);
 
    private:
+    char* stage(const void* src, size_t n, char** dev);
     cudaStream_t s_;
     size_t chunk_;
     int nchunks_, cur_ = 0;
@@ -35,6 +39,10 @@ namespace hssmf_b200 {
     std::vector<cudaEvent_t> ev_;
     std::vector<char> armed_;
   };
+
+  // host -> device copy through the current staging ring of s when there is
+  // one (pinned, truly asynchronous), else a plain cudaMemcpyAsync
+  void h2d(void* dst, const void* src, size_t n, cudaStream_t s);
 
   // process-wide ring per stream (created on first use)
   Staging* staging_for(cudaStream_t s);

@@ -63,10 +63,14 @@ def hopts(**kw):
     return P.HssOptions(**kw)
 
 
-def ranks_close(mine, ref, rel=0.10, slack=2):
+def close_mask(mine, ref, rel=0.10, slack=2):
     mine = np.asarray(mine)
     ref = np.asarray(ref)
-    return np.all(np.abs(mine - ref) <= np.maximum(slack, rel * ref))
+    return np.abs(mine - ref) <= np.maximum(slack, rel * ref)
+
+
+def ranks_close(mine, ref, rel=0.10, slack=2):
+    return bool(np.all(close_mask(mine, ref, rel, slack)))
 
 
 def test_diagonal_rank_zero_and_exact_division():
@@ -267,11 +271,12 @@ def test_baseline_config_vs_golden(name):
     for q, i in enumerate(hs):
         u = m.front_hss(int(i))[0]
         ru = g["node_u"][g["node_ptr"][q]:g["node_ptr"][q + 1]]
-        assert ranks_close(u[:-1], ru[:-1]), i
+        bad = np.nonzero(~close_mask(u[:-1], ru[:-1]))[0]
+        assert bad.size == 0, (int(i), [(int(j), int(u[j]), int(ru[j])) for j in bad[:20]])
     assert res <= 10 * float(g["relres"])
 
 
-@pytest.mark.parametrize("k", [64, 80])
+@pytest.mark.parametrize("k", [64, 80, 96])
 def test_p3d_with_config5_options_vs_reference(k):
     # BASELINE config 5 options (HSS >= 4000, eps 1e-4, leaf 256) on smaller
     # grids the reference finishes in minutes (tools/run_custom.py --ref):

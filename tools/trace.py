@@ -1,0 +1,91 @@
+"""Host/GPU timeline of one refactorization under torch.profiler (CUPTI):
+which CUDA runtime calls the host threads spend their time in, how busy the
+GPU is, and the per-kernel totals. Diagnostic only — numbers taken under the
+tracer are never bench values.
+
+usage: python tools/trace.py c3 [--out gpurun_out/trace_c3.json.gz]
+"""
+import argparse
+import collections
+import gzip
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1502_07405_b200 as P  # noqa: E402
+from paper_1502_07405_b200.problems import CONFIGS  # noqa: E402
+
+
+def union_len(iv):
+    iv.sort()
+    tot, cs, ce = 0.0, None, None
+    for s, e in iv:
+        if cs is None or s > ce:
+            if cs is not None:
+                tot += ce - cs
+            cs, ce = s, e
+        else:
+            ce = max(ce, e)
+    if cs is not None:
+        tot += ce - cs
+    return tot
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    g = P.generate_convdiff3d(cfg.k, 0.1) if cfg.kind == "cd3d" else P.generate_grid_problem(cfg.kind, cfg.k)
+    op = P.ordered_problem(g, cfg.nd_leaf)
+    m = P.mf_factor(op.a, op.t, cfg.solver_options())
+    m.refactor()
+    torch.cuda.synchronize()
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        m.refactor()
+        torch.cuda.synchronize()
+    path = a.out or os.path.join(ROOT, "gpurun_out", f"trace_{a.config}.json")
+    prof.export_chrome_trace(path)
+    ev = json.load(open(path))["traceEvents"]
+    api = collections.defaultdict(lambda: [0, 0.0])
+    kern = collections.defaultdict(lambda: [0, 0.0])
+    kiv, t0, t1 = [], 1e30, 0
+    threads = collections.defaultdict(float)
+    for e in ev:
+        if e.get("ph") != "X":
+            continue
+        c = e.get("cat", "")
+        d = float(e.get("dur", 0))
+        if c in ("cuda_runtime", "cuda_driver"):
+            api[e["name"]][0] += 1
+            api[e["name"]][1] += d
+            threads[e.get("tid")] += d
+        elif c == "kernel":
+            nm = e["name"].replace("<unnamed>::", "").split("(")[0].split("::")[-1]
+            kern[nm][0] += 1
+            kern[nm][1] += d
+            kiv.append((float(e["ts"]), float(e["ts"]) + d))
+        if c in ("kernel", "cuda_runtime", "cuda_driver", "gpu_memcpy", "gpu_memset"):
+            t0 = min(t0, float(e["ts"]))
+            t1 = max(t1, float(e["ts"]) + d)
+    span = t1 - t0
+    out = {"config": a.config, "span_ms": span / 1e3, "gpu_busy_ms": union_len(kiv) / 1e3,
+           "api_ms_by_thread": {str(k): v / 1e3 for k, v in sorted(threads.items(), key=lambda x: -x[1])[:12]},
+           "api": [(k, v[0], round(v[1] / 1e3, 2), round(v[1] / max(v[0], 1), 2))
+                   for k, v in sorted(api.items(), key=lambda x: -x[1][1])[:20]],
+           "kernels": [(k, v[0], round(v[1] / 1e3, 2)) for k, v in sorted(kern.items(), key=lambda x: -x[1][1])[:20]]}
+    print(json.dumps(out, indent=1))
+    with open(path, "rb") as f, gzip.open(path + ".gz", "wb") as g2:
+        g2.write(f.read())
+    os.remove(path)
+
+
+if __name__ == "__main__":
+    main()
