@@ -170,6 +170,10 @@ int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st
 /* measurement: average device time (ms) of `iters` m x n x k DGEMMs (NN) on
  * the DMMA kernel, device-resident operands; used for the FP64 roofline */
 int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st);
+/* Timing of the Gram-route ID kernels (no reference counterpart; measurement
+   only): ntask tasks of an n x n Gram matrix of rank min(n, d). */
+int hssmf_bench_gram(int device, int n, int d, int ntask, int iters, double* ms, int* steps,
+                     hssmf_status* st);
 
 /* number of kernel launches this library has issued (process-wide) */
 long long hssmf_launch_count(void);

@@ -89,6 +89,8 @@ _SIGS = {
     "hssmf_dev_lu": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, i32p, C.POINTER(Status)]),
     "hssmf_bench_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_double), C.POINTER(Status)]),
+    "hssmf_bench_gram": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(Status)]),
 }
 
 

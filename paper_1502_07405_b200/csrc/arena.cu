@@ -4,19 +4,40 @@ namespace hssmf_b200 {
 
   namespace {
     thread_local DevArena* g_arena = nullptr;
-
-    // 4 classes per power of two, 256 B minimum
-    size_t size_class(size_t b) {
-      if (b <= 256) return 256;
-      size_t p = 256;
-      while (p * 2 < b) p *= 2;
-      const size_t q = p / 4;
-      return (b + q - 1) / q * q;
-    }
+    thread_local DevArena* g_keep = nullptr;
   }  // namespace
 
   DevArena::~DevArena() {
     for (auto& sl : slabs_) cudaFreeAsync(sl.base, s_);
+  }
+
+  int DevArena::order_of(size_t bytes) {
+    int o = 0;
+    while ((kMinBlock << o) < bytes) o++;
+    return o;
+  }
+
+  void DevArena::new_slab() {
+    Slab sl;
+    HSSMF_CUDA(cudaMallocAsync((void**)&sl.base, kSlabBytes, s_));
+    slabs_.push_back(sl);
+    insert_free(sl.base, kMaxOrder);
+  }
+
+  void DevArena::insert_free(char* p, int o) {
+    free_[o].insert(p);
+    free_order_[p] = o;
+  }
+
+  void DevArena::erase_free(char* p, int o) {
+    free_[o].erase(p);
+    free_order_.erase(p);
+  }
+
+  int DevArena::slab_of(const char* p) const {
+    for (size_t i = 0; i < slabs_.size(); i++)
+      if (p >= slabs_[i].base && p < slabs_[i].base + kSlabBytes) return (int)i;
+    return -1;
   }
 
   void* DevArena::get(size_t bytes, size_t* cls) {
@@ -26,78 +47,65 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaMallocAsync(&p, bytes, s_));
       return p;
     }
-    const size_t c = size_class(bytes);
-    *cls = c;
-    auto it = free_.find(c);
-    if (it != free_.end() && !it->second.empty()) {
-      void* p = it->second.back();
-      it->second.pop_back();
-      slabs_[owner_[p]].live++;
-      return p;
+    const int want = order_of(bytes);
+    int o = want;
+    while (o <= kMaxOrder && free_[o].empty()) o++;
+    if (o > kMaxOrder) {
+      new_slab();
+      o = kMaxOrder;
     }
-    if (slabs_.empty() || slabs_.back().used + c > slabs_.back().size) {
-      Slab sl;
-      sl.size = kSlabBytes;
-      HSSMF_CUDA(cudaMallocAsync((void**)&sl.base, sl.size, s_));
-      slabs_.push_back(sl);
+    char* p = *free_[o].begin();
+    erase_free(p, o);
+    // split down to the wanted order, the upper halves stay free
+    while (o > want) {
+      o--;
+      insert_free(p + (kMinBlock << o), o);
     }
-    Slab& sl = slabs_.back();
-    void* p = sl.base + sl.used;
-    sl.used += c;
-    sl.live++;
-    owner_[p] = (int)slabs_.size() - 1;
+    *cls = (size_t)want + 1;
+    slabs_[slab_of(p)].live++;
+    live_bytes_ += kMinBlock << want;
     return p;
   }
 
-  void DevArena::put(void* p, size_t cls) {
-    if (!p) return;
+  void DevArena::put(void* vp, size_t cls) {
+    if (!vp) return;
     if (cls == 0) {
-      cudaFreeAsync(p, s_);
+      cudaFreeAsync(vp, s_);
       return;
     }
-    slabs_[owner_[p]].live--;
-    free_[cls].push_back(p);
+    char* p = static_cast<char*>(vp);
+    int o = (int)cls - 1;
+    const int si = slab_of(p);
+    Slab& sl = slabs_[si];
+    sl.live--;
+    live_bytes_ -= kMinBlock << o;
+    // merge with free buddies
+    while (o < kMaxOrder) {
+      const size_t off = (size_t)(p - sl.base);
+      char* buddy = sl.base + (off ^ (kMinBlock << o));
+      auto it = free_order_.find(buddy);
+      if (it == free_order_.end() || it->second != o) break;
+      erase_free(buddy, o);
+      p = std::min(p, buddy);
+      o++;
+    }
+    insert_free(p, o);
   }
 
   void DevArena::trim() {
-    // slabs without a live block go back to the stream-ordered pool
-    bool any = false;
-    for (auto& sl : slabs_) any |= sl.live == 0;
-    if (!any) return;
-    std::vector<int> remap(slabs_.size(), -1);
     std::vector<Slab> keep;
-    for (size_t i = 0; i < slabs_.size(); i++) {
-      if (slabs_[i].live == 0) {
-        cudaFreeAsync(slabs_[i].base, s_);
+    for (auto& sl : slabs_) {
+      if (sl.live == 0) {
+        erase_free(sl.base, kMaxOrder);
+        cudaFreeAsync(sl.base, s_);
       } else {
-        remap[i] = (int)keep.size();
-        keep.push_back(slabs_[i]);
-      }
-    }
-    for (auto& kv : free_) {
-      std::vector<void*> v;
-      for (void* p : kv.second)
-        if (remap[owner_[p]] >= 0) v.push_back(p);
-      kv.second.swap(v);
-    }
-    for (auto it = owner_.begin(); it != owner_.end();) {
-      if (remap[it->second] < 0) {
-        it = owner_.erase(it);
-      } else {
-        it->second = remap[it->second];
-        ++it;
+        keep.push_back(sl);
       }
     }
     slabs_.swap(keep);
-    // a partially used last slab keeps taking new blocks; a fresh one starts
-    // after a retained one only when that is full
   }
 
-  size_t DevArena::slab_bytes() const {
-    size_t b = 0;
-    for (const auto& sl : slabs_) b += sl.size;
-    return b;
-  }
+  size_t DevArena::slab_bytes() const { return slabs_.size() * kSlabBytes; }
 
   void DevArena::rebind(cudaStream_t s) {
     if (s == s_) return;
@@ -108,7 +116,16 @@ namespace hssmf_b200 {
   DevArena* current_arena(cudaStream_t s) {
     return (g_arena && g_arena->stream() == s) ? g_arena : nullptr;
   }
-  ArenaScope::ArenaScope(DevArena* a) : prev(g_arena) { g_arena = a; }
-  ArenaScope::~ArenaScope() { g_arena = prev; }
+  DevArena* current_keep_arena(cudaStream_t s) {
+    return (g_keep && g_keep->stream() == s) ? g_keep : nullptr;
+  }
+  ArenaScope::ArenaScope(DevArena* a, DevArena* keep) : prev(g_arena), prev_keep(g_keep) {
+    g_arena = a;
+    g_keep = keep;
+  }
+  ArenaScope::~ArenaScope() {
+    g_arena = prev;
+    g_keep = prev_keep;
+  }
 
 }  // namespace hssmf_b200

@@ -4,14 +4,16 @@
 // allocations (per-node samples, bases, index lists, GEMM scratch). Served by
 // cudaMallocAsync / cudaFreeAsync each costs 10-20 us of host time and the
 // calls contend across the concurrent front threads, so the host, not the
-// GPU, bounded the HSS phases. A DevArena carves blocks from 32 MB slabs and recycles freed blocks by size class,
-// so the steady state makes no driver call. Reuse is stream-ordered: every
+// GPU, bounded the HSS phases. A DevArena carves power-of-two blocks from
+// 32 MB slabs with a binary buddy allocator (freed buddies merge back), so
+// the steady state makes no driver call. Reuse is stream-ordered: every
 // block of an arena is only touched by work on the arena's stream, so a block
 // returned to the cache may be handed to a later launch on the same stream at
 // once. Blocks above kArenaMaxBlock go straight to the stream-ordered pool;
 // trim() returns slabs without live blocks to it.
 #pragma once
 
+#include <set>
 #include <unordered_map>
 #include <vector>
 
@@ -21,8 +23,10 @@ namespace hssmf_b200 {
 
   class DevArena {
    public:
+    static constexpr size_t kMinBlock = 256;
+    static constexpr int kMaxOrder = 17;  // 256 B << 17 = 32 MB slabs
+    static constexpr size_t kSlabBytes = kMinBlock << kMaxOrder;
     static constexpr size_t kArenaMaxBlock = 4u << 20;
-    static constexpr size_t kSlabBytes = 32u << 20;
 
     explicit DevArena(cudaStream_t s) : s_(s) {}
     ~DevArena();
@@ -30,7 +34,7 @@ namespace hssmf_b200 {
     DevArena& operator=(const DevArena&) = delete;
 
     cudaStream_t stream() const { return s_; }
-    // block of >= bytes; *cls receives the size class (0: not cached)
+    // block of >= bytes; *cls receives the block's class (0: not from a slab)
     void* get(size_t bytes, size_t* cls);
     void put(void* p, size_t cls);
     // return slabs without live blocks to the stream-ordered pool
@@ -38,25 +42,36 @@ namespace hssmf_b200 {
     // move to another stream: the old one is drained first
     void rebind(cudaStream_t s);
     size_t slab_bytes() const;
+    size_t live_bytes() const { return live_bytes_; }
 
    private:
     struct Slab {
       char* base = nullptr;
-      size_t size = 0, used = 0;
       long long live = 0;
     };
+    static int order_of(size_t bytes);
+    void new_slab();
+    void insert_free(char* p, int o);
+    void erase_free(char* p, int o);
+    int slab_of(const char* p) const;
+
     cudaStream_t s_;
     std::vector<Slab> slabs_;
-    std::unordered_map<void*, int> owner_;  // block -> slab
-    std::unordered_map<size_t, std::vector<void*>> free_;
+    // binary buddy free lists (power-of-two blocks, merged on release)
+    std::set<char*> free_[kMaxOrder + 1];
+    std::unordered_map<char*, int> free_order_;
+    size_t live_bytes_ = 0;
   };
 
-  // thread-local current arena (set by ArenaScope); nullptr if none or if it
-  // is bound to another stream
+  // thread-local current arenas (set by ArenaScope): scratch blocks and blocks
+  // that outlive the compression (the factor data); nullptr if none or bound
+  // to another stream
   DevArena* current_arena(cudaStream_t s);
+  DevArena* current_keep_arena(cudaStream_t s);
   struct ArenaScope {
     DevArena* prev;
-    explicit ArenaScope(DevArena* a);
+    DevArena* prev_keep;
+    ArenaScope(DevArena* a, DevArena* keep);
     ~ArenaScope();
   };
 

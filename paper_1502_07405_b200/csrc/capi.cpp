@@ -15,6 +15,7 @@
 #include "hss_dense.hpp"
 #include "host/analysis.hpp"
 #include "kernels_test.hpp"
+#include "staging.cuh"
 
 using namespace hssmf_b200;
 
@@ -33,6 +34,7 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaStreamSynchronize(s));
     c.wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
     c.n++;
+    if (Staging* st = current_staging(s)) st->complete();
   }
 }  // namespace hssmf_b200
 
@@ -396,6 +398,11 @@ int hssmf_dev_id(int device, const double* y, int m, int n, double eps, int max_
 
 int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st) {
   return guard(st, [&] { *ms = bench_gemm(device, m, n, k, iters); });
+}
+
+int hssmf_bench_gram(int device, int n, int d, int ntask, int iters, double* ms, int* steps,
+                     hssmf_status* st) {
+  return guard(st, [&] { *ms = bench_gram(device, n, d, ntask, iters, steps); });
 }
 
 int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st) {

@@ -26,24 +26,26 @@ namespace hssmf_b200 {
       GemmProblem p[kParamProbs];
     };
 
-    template<bool TA, bool TB>
-    __device__ __forceinline__ void gemm_body(const GemmProblem* probs, const int* prefix,
-                                              int nprob, double alpha, double beta) {
-      extern __shared__ __align__(16) double gsm[];
-      double (*As)[BK * SA] = reinterpret_cast<double (*)[BK * SA]>(gsm);
-      double (*Bs)[BN * SB] = reinterpret_cast<double (*)[BN * SB]>(gsm + STAGES * BK * SA);
-
-      // locate problem
-      const int tile = blockIdx.x;
+    // problem owning this CTA's tile (binary search over the tile prefix)
+    __device__ __forceinline__ int find_problem(const int* prefix, int nprob, int tile) {
       int lo = 0, hi = nprob - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
       }
-      const GemmProblem P = probs[lo];
+      return lo;
+    }
+
+    // one 64 x 64 output tile t of problem P
+    template<bool TA, bool TB>
+    __device__ __forceinline__ void gemm_tile(const GemmProblem& P, int t, double alpha,
+                                              double beta) {
+      extern __shared__ __align__(16) double gsm[];
+      double (*As)[BK * SA] = reinterpret_cast<double (*)[BK * SA]>(gsm);
+      double (*Bs)[BN * SB] = reinterpret_cast<double (*)[BN * SB]>(gsm + STAGES * BK * SA);
+
       if (P.skip && __ldcg(P.skip)) return;
       const int tiles_m = (P.m + BM - 1) / BM;
-      const int t = tile - prefix[lo];
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
       if (P.lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
       const int K = P.k;
@@ -140,13 +142,23 @@ namespace hssmf_b200 {
     __global__ void __launch_bounds__(THREADS)
     gemm_grouped_kernel(const GemmProblem* __restrict__ probs, const int* __restrict__ prefix,
                         int nprob, double alpha, double beta) {
-      gemm_body<TA, TB>(probs, prefix, nprob, alpha, beta);
+      const int lo = find_problem(prefix, nprob, blockIdx.x);
+      const GemmProblem P = probs[lo];
+      gemm_tile<TA, TB>(P, blockIdx.x - prefix[lo], alpha, beta);
     }
 
-    template<bool TA, bool TB>
+    // mixed batch: every problem carries its own transposes and alpha / beta
     __global__ void __launch_bounds__(THREADS)
-    gemm_param_kernel(const __grid_constant__ GemmParam b, double alpha, double beta) {
-      gemm_body<TA, TB>(b.p, b.pre, b.nprob, alpha, beta);
+    gemm_param_kernel(const __grid_constant__ GemmParam b) {
+      const int lo = find_problem(b.pre, b.nprob, blockIdx.x);
+      const GemmProblem& P = b.p[lo];
+      const int t = blockIdx.x - b.pre[lo];
+      switch (P.trans) {
+        case 0: gemm_tile<false, false>(P, t, P.alpha, P.beta); break;
+        case 1: gemm_tile<true, false>(P, t, P.alpha, P.beta); break;
+        case 2: gemm_tile<false, true>(P, t, P.alpha, P.beta); break;
+        default: gemm_tile<true, true>(P, t, P.alpha, P.beta); break;
+      }
     }
 
     void set_gemm_attrs() {
@@ -156,10 +168,7 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       attr = true;
     }
   }  // namespace
@@ -192,7 +201,12 @@ namespace hssmf_b200 {
 
   void gemm_run_host(const std::vector<GemmProblem>& p, char ta, char tb, double alpha,
                      double beta, cudaStream_t s) {
-    const bool TA = ta != 'N', TB = tb != 'N';
+    std::vector<GemmProblem> q(p);
+    for (auto& x : q) gemm_set_op(x, ta, tb, alpha, beta);
+    gemm_run_mixed(q, s);
+  }
+
+  void gemm_run_mixed(const std::vector<GemmProblem>& p, cudaStream_t s) {
     set_gemm_attrs();
     GemmParam b;
     b.nprob = 0;
@@ -201,11 +215,7 @@ namespace hssmf_b200 {
       if (!b.nprob) return;
       const int tiles = b.pre[b.nprob];
       if (tiles) {
-        dim3 grid(tiles), block(THREADS);
-        if (!TA && !TB) gemm_param_kernel<false, false><<<grid, block, SMEM, s>>>(b, alpha, beta);
-        else if (TA && !TB) gemm_param_kernel<true, false><<<grid, block, SMEM, s>>>(b, alpha, beta);
-        else if (!TA && TB) gemm_param_kernel<false, true><<<grid, block, SMEM, s>>>(b, alpha, beta);
-        else gemm_param_kernel<true, true><<<grid, block, SMEM, s>>>(b, alpha, beta);
+        gemm_param_kernel<<<tiles, THREADS, SMEM, s>>>(b);
         HSSMF_LAUNCH_CHECK();
       }
       b.nprob = 0;

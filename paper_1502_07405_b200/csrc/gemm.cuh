@@ -21,7 +21,17 @@ namespace hssmf_b200 {
     int lda, ldb, ldc;
     const int* skip = nullptr;  // optional device flag: problem is a no-op when *skip != 0
     int lower = 0;              // only the lower triangle of C is needed (SYRK-like)
+    // per-problem operation (gemm_run_mixed): bit 0 = op(A) transposed,
+    // bit 1 = op(B) transposed; C = alpha op(A) op(B) + beta C
+    int trans = 0;
+    double alpha = 1.0, beta = 0.0;
   };
+
+  inline void gemm_set_op(GemmProblem& g, char ta, char tb, double alpha, double beta) {
+    g.trans = (ta != 'N' ? 1 : 0) | (tb != 'N' ? 2 : 0);
+    g.alpha = alpha;
+    g.beta = beta;
+  }
 
   // device-resident batch: descriptors + tile prefix (prefix[p] = first tile
   // of problem p, prefix[nprob] = total tiles)
@@ -42,10 +52,11 @@ namespace hssmf_b200 {
   void gemm_run(const GemmBatchDev& b, char ta, char tb, double alpha, double beta,
                 cudaStream_t s);
 
-  // one-off convenience: uploads descriptors synchronously into a temporary
-  // device buffer (tests / dynamic HSS phases), then launches
-  struct DevBuffer;
+  // dynamic batches (HSS phases, tests): the descriptors travel as kernel
+  // parameters, no upload. gemm_run_host applies one op to every problem;
+  // gemm_run_mixed takes each problem's own trans / alpha / beta.
   void gemm_run_host(const std::vector<GemmProblem>& p, char ta, char tb, double alpha,
                      double beta, cudaStream_t s);
+  void gemm_run_mixed(const std::vector<GemmProblem>& p, cudaStream_t s);
 
 }  // namespace hssmf_b200

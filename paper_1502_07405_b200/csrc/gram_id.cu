@@ -33,7 +33,10 @@ namespace hssmf_b200 {
       return (size_t)rows * nb * 8 + (size_t)rows * 8 + (size_t)n * 8 + (size_t)rows * 4 + 64;
     }
 
-    __device__ void block_cand(double bv, int bp, int bi, Cand* out, double* wv, int* wp, int* wi) {
+    // CTA-wide best candidate: warp shuffles, then every thread combines the
+    // per-warp winners itself (no serial step, no second barrier)
+    __device__ __forceinline__ Cand block_best(double bv, int bp, int bi, double* wv, int* wp,
+                                               int* wi) {
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       for (int o = 16; o > 0; o >>= 1) {
         const double v2 = __shfl_down_sync(0xffffffffu, bv, o);
@@ -43,20 +46,20 @@ namespace hssmf_b200 {
       }
       if (lane == 0) { wv[warp] = bv; wp[warp] = bp; wi[warp] = bi; }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        Cand c{wv[0], wp[0], wi[0]};
-        for (int w = 1; w < GW; w++)
-          if (better(wv[w], wp[w], c.v, c.pos)) c = {wv[w], wp[w], wi[w]};
-        *out = c;
-      }
+      Cand c{wv[0], wp[0], wi[0]};
+      for (int w = 1; w < GW; w++)
+        if (better(wv[w], wp[w], c.v, c.pos)) c = {wv[w], wp[w], wi[w]};
+      return c;
     }
 
     // nb steps of symmetric pivoted Cholesky on the Gram matrix, one
     // thread-block cluster per task. Rows are split in contiguous blocks over
     // the CTAs; each CTA keeps its rows' panel columns, residual norms and
     // flags plus a replicated copy of the position bookkeeping in shared
-    // memory, so one cluster barrier per elimination step suffices: the
-    // candidates for step j+1 are published together with column j.
+    // memory. Per elimination step there is ONE cluster barrier and ONE DSMEM
+    // round trip: every CTA publishes its best candidate together with that
+    // row's panel values, every CTA fetches all of them, and every thread
+    // takes the (identical) pivot decision itself.
     __global__ void __launch_bounds__(GT)
     gram_panel_kernel(const GramTask* __restrict__ tasks, int k0, int nb, double eps,
                       double abs_tol, int CL, int init) {
@@ -73,12 +76,12 @@ namespace hssmf_b200 {
       int* orig = reinterpret_cast<int*>(dg + rows);
       int* pos = orig + n;
       int* flg = pos + n;
-      __shared__ Cand pub[2];
+      __shared__ Cand pub[2];              // own candidate (double-buffered)
+      __shared__ double pubrow[2][kGramNB];  // its panel row
+      __shared__ Cand stc[16];             // all candidates of the cluster
+      __shared__ double strow[16][kGramNB];  // and their panel rows
       __shared__ double wv[GW];
       __shared__ int wp[GW], wi[GW];
-      __shared__ int s_stop, s_pj, s_cert;
-      __shared__ double s_ljj, s_r11;
-      __shared__ double prow[64];
 
       if (__ldcg(T.state + 1) && !init) return;  // finished in an earlier panel
       // load / initialise the state
@@ -99,7 +102,7 @@ namespace hssmf_b200 {
         }
       }
       for (int e = tid; e < rows * nb; e += GT) Lp[e] = 0.0;
-      if (tid == 0) s_r11 = init ? 0.0 : __ldcg(T.r11);
+      double r11 = init ? 0.0 : __ldcg(T.r11);
       __syncthreads();
       int j = k0, stopped = 0, cert = 0;
       if (n == 0 || T.kmax_dim == 0) {
@@ -110,29 +113,41 @@ namespace hssmf_b200 {
         int bp = INT_MAX, bi = -1;
         for (int i = tid; i < nr; i += GT)
           if (!flg[i] && better(dg[i], pos[r0 + i], bv, bp)) { bv = dg[i]; bp = pos[r0 + i]; bi = r0 + i; }
-        block_cand(bv, bp, bi, &pub[0], wv, wp, wi);
+        const Cand c = block_best(bv, bp, bi, wv, wp, wi);
+        if (tid == 0) pub[0] = c;
       }
       cl.sync();
       for (int jj = 0; jj < nb && !stopped; jj++, j++) {
         const int buf = jj & 1;
-        // decision for step j (identical in every CTA, rrqr.hpp:62-77): one
-        // lane per peer CTA fetches its candidate over DSMEM, warp reduction
-        if (tid < 32) {
-          Cand c{-1.0, INT_MAX, -1};
-          if (tid < CL) c = *cl.map_shared_rank(&pub[buf], tid);
-          for (int o = 16; o > 0; o >>= 1) {
-            const double v2 = __shfl_down_sync(0xffffffffu, c.v, o);
-            const int p2 = __shfl_down_sync(0xffffffffu, c.pos, o);
-            const int i2 = __shfl_down_sync(0xffffffffu, c.idx, o);
-            if (better(v2, p2, c.v, c.pos)) c = {v2, p2, i2};
-          }
-          if (tid == 0) {
-          const double pv = c.v > 0.0 ? sqrt(c.v) : 0.0;
+        // fetch every CTA's candidate and panel row (one DSMEM round trip)
+        if (tid < CL * 16) {
+          const int c = tid >> 4, l = tid & 15;
+          const double* rr = cl.map_shared_rank(&pubrow[buf][0], c);
+          // all remote loads in flight together, then the local stores
+          Cand cv;
+          if (l == 0) cv = *cl.map_shared_rank(&pub[buf], c);
+          double v[kGramNB / 16];
+#pragma unroll
+          for (int u = 0; u < kGramNB / 16; u++) v[u] = l + 16 * u < jj ? rr[l + 16 * u] : 0.0;
+          if (l == 0) stc[c] = cv;
+#pragma unroll
+          for (int u = 0; u < kGramNB / 16; u++)
+            if (l + 16 * u < jj) strow[c][l + 16 * u] = v[u];
+        }
+        __syncthreads();
+        // decision for step j, taken identically by every thread of every
+        // CTA (rrqr.hpp:62-77: largest residual norm, lowest position on ties)
+        int w = 0;
+        Cand best = stc[0];
+        for (int c = 1; c < CL; c++)
+          if (better(stc[c].v, stc[c].pos, best.v, best.pos)) { best = stc[c]; w = c; }
+        const double pv = best.v > 0.0 ? sqrt(best.v) : 0.0;
+        {
           int stop = 0, ct = 0;
           if (j == 0) {
-            s_r11 = pv;
+            r11 = pv;
             if (pv == 0.0 || pv <= abs_tol) { stop = 1; ct = 1; }
-          } else if (pv <= eps * s_r11 || pv <= abs_tol) {
+          } else if (pv <= eps * r11 || pv <= abs_tol) {
             stop = 1;
             ct = 1;
           }
@@ -140,37 +155,22 @@ namespace hssmf_b200 {
             stop = 1;
             ct = (j == T.kmax_dim);
           }
-          s_stop = stop;
-          s_cert = ct;
-          s_pj = c.idx;
-          s_ljj = pv;
+          if (stop) {
+            stopped = 1;
+            cert = ct;
+            break;
           }
         }
-        __syncthreads();
-        if (s_stop) {
-          stopped = 1;
-          cert = s_cert;
-          break;
-        }
-        const int pj = s_pj;
-        const double ljj = s_ljj;
-        const int owner = min(pj / rows, CL - 1);
-        // pivot row's panel values from its owner (DSMEM)
-        if (tid < jj) prow[tid] = cl.map_shared_rank(Lp, owner)[(size_t)tid * rows + (pj - owner * rows)];
-        __syncthreads();
-        // CPQR column swap of positions j and pos(pj), replicated in every CTA
-        if (tid == 0) {
-          const int pp = pos[pj], ok = orig[j];
-          orig[j] = pj;
-          orig[pp] = ok;
-          pos[pj] = j;
-          pos[ok] = pp;
-        }
+        const int pj = best.idx;
+        const double ljj = pv;
+        const double* prow = strow[w];
+        // CPQR column swap of positions j and pos(pj) (applied below by
+        // thread 0 once every thread has read the old values)
+        const int pp = pos[pj], ok = orig[j];
         // column j of L on own rows, residual norms downdated (clamped at 0)
         const double* gcol = T.G + (size_t)pj * n;
         double bv = -1.0;
         int bp = INT_MAX, bi = -1;
-        __syncthreads();
         for (int i = tid; i < nr; i += GT) {
           const int gi = r0 + i;
           if (flg[i]) {
@@ -184,15 +184,23 @@ namespace hssmf_b200 {
             continue;
           }
           // lower triangle of G only (the trailing updates skip the upper one)
-          double s = gi >= pj ? gcol[gi] : T.G[pj + (size_t)gi * n];
-          for (int q = 0; q < jj; q++) s -= Lp[(size_t)q * rows + i] * prow[q];
-          const double lo = s / ljj;
+          double sv = gi >= pj ? gcol[gi] : T.G[pj + (size_t)gi * n];
+          for (int q = 0; q < jj; q++) sv -= Lp[(size_t)q * rows + i] * prow[q];
+          const double lo = sv / ljj;
           Lp[(size_t)jj * rows + i] = lo;
           T.L[gi + (size_t)j * n] = lo;
           double dd = dg[i] - lo * lo;
           if (dd < 0.0) dd = 0.0;
           dg[i] = dd;
-          if (better(dd, pos[gi], bv, bp)) { bv = dd; bp = pos[gi]; bi = gi; }
+          const int pgi = gi == ok ? pp : pos[gi];
+          if (better(dd, pgi, bv, bp)) { bv = dd; bp = pgi; bi = gi; }
+        }
+        const Cand c = block_best(bv, bp, bi, wv, wp, wi);  // barrier inside
+        if (tid == 0) {
+          orig[j] = pj;
+          orig[pp] = ok;
+          pos[pj] = j;
+          pos[ok] = pp;
         }
         if (j + 1 == T.kmax_dim) {  // factorization exhausted exactly
           stopped = 1;
@@ -200,9 +208,12 @@ namespace hssmf_b200 {
           j++;
           break;
         }
-        block_cand(bv, bp, bi, &pub[buf ^ 1], wv, wp, wi);
+        // publish the candidate for step j + 1 with its panel row (q <= jj)
+        if (tid == 0) pub[buf ^ 1] = c;
+        if (c.idx >= 0 && tid <= jj) pubrow[buf ^ 1][tid] = Lp[(size_t)tid * rows + (c.idx - r0)];
         cl.sync();
       }
+      __syncthreads();
       // write back the state for the next panel / the host
       for (int i = tid; i < nr; i += GT) {
         __stcg(T.dg + r0 + i, dg[i]);
@@ -214,7 +225,7 @@ namespace hssmf_b200 {
           __stcg(T.pos_of + i, pos[i]);
         }
         if (tid == 0) {
-          if (k0 == 0) __stcg(T.r11, s_r11);
+          if (k0 == 0) __stcg(T.r11, r11);
           __stcg(T.state + 0, j);
           __stcg(T.state + 1, stopped);
           __stcg(T.state + 2, cert);
@@ -296,12 +307,10 @@ namespace hssmf_b200 {
     bool packed = true;
     for (int t = 1; t < nt; t++) packed &= tasks[t].state == tasks[0].state + 3 * t;
     if (packed) {
-      HSSMF_CUDA(cudaMemcpyAsync(hst.data(), tasks[0].state, 3 * nt * sizeof(int),
-                                 cudaMemcpyDeviceToHost, s));
+      d2h(hst.data(), tasks[0].state, 3 * nt * sizeof(int), s);
     } else {
       for (int t = 0; t < nt; t++)
-        HSSMF_CUDA(cudaMemcpyAsync(&hst[3 * t], tasks[t].state, 3 * sizeof(int),
-                                   cudaMemcpyDeviceToHost, s));
+        d2h(&hst[3 * t], tasks[t].state, 3 * sizeof(int), s);
     }
     if (before_sync) before_sync();
     stream_sync(s);

@@ -43,12 +43,19 @@ namespace hssmf_b200 {
         }
         return *this;
       }
-      void alloc(size_t cnt, cudaStream_t st) {
+      void alloc(size_t cnt, cudaStream_t st) { alloc_in(cnt, st, current_arena(st)); }
+      // block that outlives the compression (factor data): kept apart from the
+      // scratch blocks so that the scratch slabs can be released afterwards
+      void alloc_keep(size_t cnt, cudaStream_t st) {
+        DevArena* k = current_keep_arena(st);
+        alloc_in(cnt, st, k ? k : current_arena(st));
+      }
+      void alloc_in(size_t cnt, cudaStream_t st, DevArena* a) {
         free();
         s = st;
         n = cnt;
         if (!cnt) return;
-        ar = current_arena(st);
+        ar = a;
         if (ar) p = static_cast<T*>(ar->get(cnt * sizeof(T), &cls));
         else HSSMF_CUDA(cudaMallocAsync((void**)&p, cnt * sizeof(T), s));
       }
@@ -76,14 +83,24 @@ namespace hssmf_b200 {
         cols = cap = 0;
         b.s = s;
       }
-      void ensure(int c) {
+      // grow to >= c columns; the existing columns are copied now, or, with
+      // defer, by a descriptor appended to the caller's next index_copy batch
+      // (the old block is parked in grave until that launch is enqueued)
+      void ensure(int c, std::vector<CopyDesc>* defer = nullptr,
+                  std::vector<DBuf<double>>* grave = nullptr) {
         if (c <= cap) return;
         const int nc = std::max(c, cap + cap / 2);
         DBuf<double> nb;
         nb.alloc((size_t)rows * nc + 1, b.s);
-        if (cols && rows)
-          HSSMF_CUDA(cudaMemcpyAsync(nb.p, b.p, (size_t)rows * cols * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, b.s));
+        if (cols && rows) {
+          if (defer) {
+            defer->push_back(copy_block(b.p, rows, nb.p, rows, rows, cols));
+            grave->push_back(std::move(b));
+          } else {
+            HSSMF_CUDA(cudaMemcpyAsync(nb.p, b.p, (size_t)rows * cols * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, b.s));
+          }
+        }
         b = std::move(nb);
         cap = nc;
       }
@@ -122,10 +139,14 @@ namespace hssmf_b200 {
       double flops = 0;
       void run(cudaStream_t s) {
         flops += gemm_flops(nn) + gemm_flops(tn) + gemm_flops(nt) + gemm_flops(tn_plus);
-        gemm_run_host(nn, 'N', 'N', -1.0, 1.0, s);
-        gemm_run_host(tn, 'T', 'N', -1.0, 1.0, s);
-        gemm_run_host(nt, 'N', 'T', -1.0, 1.0, s);
-        gemm_run_host(tn_plus, 'T', 'N', 1.0, 1.0, s);
+        // one mixed launch for the four groups (distinct outputs)
+        std::vector<GemmProblem> all;
+        all.reserve(nn.size() + tn.size() + nt.size() + tn_plus.size());
+        for (auto g : nn) { gemm_set_op(g, 'N', 'N', -1.0, 1.0); all.push_back(g); }
+        for (auto g : tn) { gemm_set_op(g, 'T', 'N', -1.0, 1.0); all.push_back(g); }
+        for (auto g : nt) { gemm_set_op(g, 'N', 'T', -1.0, 1.0); all.push_back(g); }
+        for (auto g : tn_plus) { gemm_set_op(g, 'T', 'N', 1.0, 1.0); all.push_back(g); }
+        gemm_run_mixed(all, s);
         nn.clear(); tn.clear(); nt.clear(); tn_plus.clear();
       }
     };
@@ -174,7 +195,8 @@ namespace hssmf_b200 {
   void hss_set_phase_timing(bool on) { g_phase_timing = on; }
 
   struct HssImpl {
-    DevArena arena;  // first member: outlives every buffer below
+    DevArena arena;       // scratch blocks; first members: outlive every buffer below
+    DevArena keep_arena;  // factor data
     cudaStream_t s;
     ClusterTree tree;
     int m = 0;
@@ -238,7 +260,7 @@ namespace hssmf_b200 {
     }
     ~HssImpl() { collect_phases(); }
 
-    explicit HssImpl(cudaStream_t st) : arena(st), s(st) {}
+    explicit HssImpl(cudaStream_t st) : arena(st), keep_arena(st), s(st) {}
 
     // ---------------------------------------------------------- compression
     void init_tree(const ClusterTree& t) {
@@ -272,14 +294,14 @@ namespace hssmf_b200 {
       o = opts;
       m = t.nodes.back().end;
       init_tree(t);
-      seeds.alloc(std::max<size_t>(sd.size(), 1), s);
+      seeds.alloc_keep(std::max<size_t>(sd.size(), 1), s);
       h2d(seeds.p, sd.data(), sd.size() * sizeof(long long), s);
       R.init(m, s);
       Sr.init(m, s);
       Sc.init(m, s);
-      scale.alloc(1, s);
+      scale.alloc_keep(1, s);
       scale.zero();
-      one.alloc(1, s);
+      one.alloc_keep(1, s);
       const double h1 = 1.0;
       h2d(one.p, &h1, sizeof(double), s);
       d = std::min(o.d0, o.max_rank + o.p);
@@ -314,7 +336,7 @@ namespace hssmf_b200 {
           maxabs_run(Sc.col(dold), m, m, dn, scale.p, s);
         }
         double sc = 0;
-        HSSMF_CUDA(cudaMemcpyAsync(&sc, scale.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+        d2h(&sc, scale.p, sizeof(double), s);
         stream_sync(s);
         const int cap_id = std::min(d - o.p, o.max_rank);
         const double abs_tol = o.eps * sc;
@@ -443,8 +465,8 @@ namespace hssmf_b200 {
           auto& a = nodes[N.c0];
           auto& b = nodes[N.c1];
           N.mt = a.r + b.r;
-          N.B12.alloc((size_t)a.r * b.r + 1, s);
-          N.B21.alloc((size_t)b.r * a.r + 1, s);
+          N.B12.alloc_keep((size_t)a.r * b.r + 1, s);
+          N.B21.alloc_keep((size_t)b.r * a.r + 1, s);
           ext.push_back(cd(A, 1, lda, a.d_ir.p, 0, b.d_ic.p, 0, N.B12.p, a.r, nullptr, 0, nullptr,
                            0, a.r, b.r));
           ext.push_back(cd(A, 1, lda, b.d_ir.p, 0, a.d_ic.p, 0, N.B21.p, b.r, nullptr, 0, nullptr,
@@ -474,13 +496,14 @@ namespace hssmf_b200 {
     // (build_local_samples, hss_compress.hpp:101-144)
     void build_local_samples(const std::vector<int>& act) {
       std::vector<CopyDesc> cp;
+      std::vector<DBuf<double>> grave;
       GemmGroups gg;
       for (int n : act) {
         auto& N = nodes[n];
         const int cb = N.cols_built, nc = d - cb;
         if (nc <= 0) continue;
-        N.slr.ensure(d);
-        N.slc.ensure(d);
+        N.slr.ensure(d, &cp, &grave);
+        N.slc.ensure(d, &cp, &grave);
         const int mt = N.mt;
         if (N.leaf) {
           cp.push_back(copy_block(Sr.col(cb) + N.begin, m, N.slr.col(cb), mt, mt, nc));
@@ -528,8 +551,12 @@ namespace hssmf_b200 {
         N.gram_cols = d;
       }
       flops += gemm_flops(gp) + gemm_flops(gp0);
-      gemm_run_host(gp0, 'N', 'T', 1.0, 0.0, s);
-      gemm_run_host(gp, 'N', 'T', 1.0, 1.0, s);
+      for (auto& g : gp0) gemm_set_op(g, 'N', 'T', 1.0, 0.0);
+      for (auto g : gp) {
+        gemm_set_op(g, 'N', 'T', 1.0, 1.0);
+        gp0.push_back(g);
+      }
+      gemm_run_mixed(gp0, s);
     }
 
     // all ID permutations of a batch in one device->host read: gathered into
@@ -549,7 +576,7 @@ namespace hssmf_b200 {
         packed.alloc(off[nt] + 1, s);
         int_gather_run(segs, packed.p, s);
         h.resize(off[nt] + 1);
-        HSSMF_CUDA(cudaMemcpyAsync(h.data(), packed.p, off[nt] * sizeof(int), cudaMemcpyDeviceToHost, s));
+        d2h(h.data(), packed.p, off[nt] * sizeof(int), s);
       }
       void unpack(std::vector<std::vector<int>>& hp) {
         const int nt = (int)off.size() - 1;
@@ -575,6 +602,7 @@ namespace hssmf_b200 {
       st.alloc(3 * nt, s);
       r11.alloc(nt, s);
       std::vector<GramTask> gt(nt);
+      std::vector<CopyDesc> gcp;  // working copies of the accumulated Gram matrices
       for (int q = 0; q < na; q++) {
         auto& N = nodes[act[q]];
         const int mt = N.mt;
@@ -584,18 +612,17 @@ namespace hssmf_b200 {
           const int kdim = std::min(d, mt), kmax = std::min(kdim, std::max(cap_id, 0));
           const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
           Gw[t].alloc((size_t)mt * mt + 1, s);
-          if (mt)
-            HSSMF_CUDA(cudaMemcpyAsync(Gw[t].p, G0.p, (size_t)mt * mt * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s));
+          if (mt) gcp.push_back(copy_block(G0.p, mt, Gw[t].p, mt, mt, mt));
           L[t].alloc((size_t)mt * kcap + 1, s);
           dg[t].alloc(mt + 1, s);
           flag[t].alloc(mt + 1, s);
           pos[t].alloc(mt + 1, s);
-          perm[t].alloc(mt + 1, s);
+          perm[t].alloc_keep(mt + 1, s);
           gt[t] = {Gw[t].p, L[t].p, dg[t].p, flag[t].p, perm[t].p, pos[t].p, st.p + 3 * t,
                    r11.p + t, mt, kdim, kmax, kcap};
         }
       }
+      index_copy_run(gcp, s);
       std::vector<int> rk, ce;
       PermReadback prb;
       {
@@ -646,7 +673,7 @@ namespace hssmf_b200 {
           const Grow& src = side ? N.slc : N.slr;
           Y[t].alloc((size_t)d * mt + 1, s);
           X[t].alloc((size_t)std::min(d, mt) * mt + 1, s);
-          perm[t].alloc(mt + 1, s);
+          perm[t].alloc_keep(mt + 1, s);
           // Y = S_loc^T (d x mt)
           tr.push_back(cd(src.b.p, mt, 1, nullptr, 0, nullptr, 0, Y[t].p, d, nullptr, 0, nullptr, 0,
                           d, mt));
@@ -661,7 +688,7 @@ namespace hssmf_b200 {
         Ph ph_(this, 3);
         cpqr_run(dt.p, (int)tasks.size(), d, max_n, o.eps, abs_tol, s);
       }
-      HSSMF_CUDA(cudaMemcpyAsync(ho.data(), outs.p, ho.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+      d2h(ho.data(), outs.p, ho.size() * sizeof(int), s);
       PermReadback prb;
       prb.enqueue(perm, 2 * na, s);
       stream_sync(s);
@@ -735,8 +762,8 @@ namespace hssmf_b200 {
         N.d_vp = std::move(perm[2 * q + 1]);
         const int kk = mt - r;
         // E = coeffs^H padded to rank r (BasisId ctor + pad_to, hss_matrix.hpp:21-58)
-        N.Eu.alloc((size_t)kk * r + 1, s);
-        N.Ev.alloc((size_t)kk * r + 1, s);
+        N.Eu.alloc_keep((size_t)kk * r + 1, s);
+        N.Ev.alloc_keep((size_t)kk * r + 1, s);
         for (int side = 0; side < 2; side++) {
           const int kid = side ? kc : kr, t = r - kid;
           DBuf<double>& E = side ? N.Ev : N.Eu;
@@ -765,8 +792,8 @@ namespace hssmf_b200 {
           N.ir[j] = rows_all[N.up[j]];
           N.ic[j] = cols_all[N.vp[j]];
         }
-        N.d_ir.alloc(r + 1, s);
-        N.d_ic.alloc(r + 1, s);
+        N.d_ir.alloc_keep(r + 1, s);
+        N.d_ic.alloc_keep(r + 1, s);
         if (r) {
           h2d(N.d_ir.p, N.ir.data(), r * sizeof(int), s);
           h2d(N.d_ic.p, N.ic.data(), r * sizeof(int), s);
@@ -817,13 +844,13 @@ namespace hssmf_b200 {
       if (todo.empty()) return;
       std::vector<CopyDesc> c1, c3;
       GemmGroups gg;
-      std::vector<DBuf<double>> tr(todo.size()), tc(todo.size());
+      std::vector<DBuf<double>> tr(todo.size()), tc(todo.size()), grave;
       std::vector<BasisApplyJob> jobs;
       for (size_t q = 0; q < todo.size(); q++) {
         auto& N = nodes[todo[q]];
         const int cb = N.cols_built, nc = d - cb, r = N.r, mt = N.mt;
         for (Grow* g : {&N.sr, &N.sc, &N.rr, &N.rc}) {
-          g->ensure(d);
+          g->ensure(d, &c1, &grave);
           g->cols = d;
         }
         if (N.leaf) {
@@ -906,7 +933,7 @@ namespace hssmf_b200 {
                 pend[q].bn[bi][1] = (int)dcv.size();
               }
           }
-          N.G.alloc((size_t)mt * mt + 1, s);
+          N.G.alloc_keep((size_t)mt * mt + 1, s);
         }
         pool.upload(s);
         std::vector<CopyDesc> cps;
@@ -950,7 +977,7 @@ namespace hssmf_b200 {
             N.red_ld = mt;
             continue;
           }
-          N.lpiv.alloc(2 * k, s);
+          N.lpiv.alloc_keep(2 * k, s);
           FrontDev f{};
           f.ns = k;
           f.nu = N.r;
@@ -985,7 +1012,7 @@ namespace hssmf_b200 {
     // dense LU of Z (zn x zn) with ns leading columns eliminated
     void factor_top(int ns, int nus, int blame) {
       Ph ph_(this, 7);
-      Zpiv.alloc(2 * ns + 1, s);
+      Zpiv.alloc_keep(2 * ns + 1, s);
       FrontDev f{};
       f.ns = ns;
       f.nu = nus;
@@ -1009,7 +1036,7 @@ namespace hssmf_b200 {
       r0 = R0.r;
       r1 = R1.r;
       zn = r0 + r1;
-      Z.alloc((size_t)zn * zn + 1, s);
+      Z.alloc_keep((size_t)zn * zn + 1, s);
       Z.zero();
       const auto& N = nodes[root];
       std::vector<CopyDesc> c;
@@ -1025,7 +1052,7 @@ namespace hssmf_b200 {
       auto& Rt = nodes[root];
       if (Rt.leaf) {
         zn = m;
-        Z.alloc((size_t)m * m + 1, s);
+        Z.alloc_keep((size_t)m * m + 1, s);
         index_copy_run({copy_block(A, lda, Z.p, m, m, m)}, s);
         factor_top(m, 0, root);
         return;
@@ -1164,7 +1191,7 @@ namespace hssmf_b200 {
       if (sbuf.p) return;
       size_t tot = 2 * (size_t)m + 64;
       for (auto& N : nodes) tot += (size_t)N.k + 2 * N.r + 8;
-      sbuf.alloc(tot, s);
+      sbuf.alloc_keep(tot, s);
       double* p = sbuf.p;
       for (auto& N : nodes) {
         N.ws = p; p += N.k + 2;
@@ -1305,17 +1332,17 @@ namespace hssmf_b200 {
   void HssMatrixDev::compress(const double* A, long long lda, const ClusterTree& tree,
                               const std::vector<long long>& seeds, const HssOpts& o) {
     StagingScope sc(staging_for(d_->s));
-    ArenaScope as(&d_->arena);
+    ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->compress(A, lda, tree, seeds, o);
   }
   void HssMatrixDev::ulv_full() {
     StagingScope sc(staging_for(d_->s));
-    ArenaScope as(&d_->arena);
+    ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->ulv_full();
   }
   void HssMatrixDev::ulv_partial(double* update, long long ldu) {
     StagingScope sc(staging_for(d_->s));
-    ArenaScope as(&d_->arena);
+    ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->ulv_partial(update, ldu);
   }
   void HssMatrixDev::drop_dense() {
@@ -1339,21 +1366,22 @@ namespace hssmf_b200 {
   void HssMatrixDev::set_stream(cudaStream_t s) {
     d_->collect_phases();
     d_->arena.rebind(s);
+    d_->keep_arena.rebind(s);
     d_->s = s;
   }
   void HssMatrixDev::solve_full(double* x) {
     StagingScope sc(staging_for(d_->s));
-    ArenaScope as(&d_->arena);
+    ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->solve_full(x);
   }
   void HssMatrixDev::partial_forward(const double* b1, double* bupd) {
     StagingScope sc(staging_for(d_->s));
-    ArenaScope as(&d_->arena);
+    ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->partial_forward(b1, bupd);
   }
   void HssMatrixDev::partial_backward(double* x1, const double* x2) {
     StagingScope sc(staging_for(d_->s));
-    ArenaScope as(&d_->arena);
+    ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->partial_backward(x1, x2);
   }
   int HssMatrixDev::rows() const { return d_->m; }
@@ -1386,7 +1414,9 @@ namespace hssmf_b200 {
     return s;
   }
   double HssMatrixDev::flops() const { return d_->flops; }
-  size_t HssMatrixDev::arena_bytes() const { return d_->arena.slab_bytes(); }
+  size_t HssMatrixDev::arena_bytes() const {
+    return d_->arena.slab_bytes() + d_->keep_arena.slab_bytes();
+  }
   std::vector<HssPhaseStat> HssMatrixDev::phase_stats() {
     d_->collect_phases();
     std::vector<HssPhaseStat> v(kHssPhases);

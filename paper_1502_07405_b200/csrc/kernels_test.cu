@@ -8,6 +8,7 @@
 #include "engine.hpp"
 #include "front.cuh"
 #include "gemm.cuh"
+#include "gram_id.cuh"
 #include "rng.cuh"
 
 namespace hssmf_b200 {
@@ -139,6 +140,54 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    return ms / iters;
+  }
+
+  double bench_gram(int device, int n, int d, int ntask, int iters, int* steps) {
+    HSSMF_CUDA(cudaSetDevice(device));
+    // S: n x d pseudo-random (host LCG), G0 = S S^T (lower triangle)
+    std::vector<double> hs((size_t)n * d);
+    unsigned long long x = 88172645463325252ull;
+    for (auto& v : hs) {
+      x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+      v = (double)(x >> 11) / 9007199254740992.0 - 0.5;
+    }
+    Buf S(hs.size() * 8), G0((size_t)n * n * 8);
+    HSSMF_CUDA(cudaMemcpy(S.p, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice));
+    GemmProblem g{S.as<double>(), S.as<double>(), G0.as<double>(), n, n, d, n, n, n};
+    g.lower = 1;
+    gemm_run_host({g}, 'N', 'T', 1.0, 0.0, 0);
+    const int kdim = std::min(n, d), kmax = kdim;
+    const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
+    Buf Gw((size_t)n * n * 8 * ntask), L((size_t)n * kcap * 8 * ntask), dg((size_t)n * 8 * ntask),
+        fl((size_t)n * 4 * ntask), pos((size_t)n * 4 * ntask), perm((size_t)n * 4 * ntask),
+        st(12 * ntask), r11(8 * ntask);
+    std::vector<GramTask> tasks(ntask);
+    for (int t = 0; t < ntask; t++)
+      tasks[t] = {Gw.as<double>() + (size_t)t * n * n, L.as<double>() + (size_t)t * n * kcap,
+                  dg.as<double>() + (size_t)t * n, fl.as<int>() + (size_t)t * n,
+                  perm.as<int>() + (size_t)t * n, pos.as<int>() + (size_t)t * n,
+                  st.as<int>() + 3 * t, r11.as<double>() + t, n, kdim, kmax, kcap};
+    std::vector<int> rk, ce;
+    auto once = [&] {
+      for (int t = 0; t < ntask; t++)
+        HSSMF_CUDA(cudaMemcpyAsync(tasks[t].G, G0.p, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, 0));
+      gram_cholesky_run(tasks, 1e-14, 0.0, 0, rk, ce);
+    };
+    once();
+    HSSMF_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    HSSMF_CUDA(cudaEventCreate(&e0));
+    HSSMF_CUDA(cudaEventCreate(&e1));
+    HSSMF_CUDA(cudaEventRecord(e0, 0));
+    for (int i = 0; i < iters; i++) once();
+    HSSMF_CUDA(cudaEventRecord(e1, 0));
+    HSSMF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    HSSMF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *steps = rk.empty() ? 0 : rk[0];
     return ms / iters;
   }
 

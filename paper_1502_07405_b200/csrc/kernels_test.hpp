@@ -12,4 +12,7 @@ namespace hssmf_b200 {
                double abs_tol, int* perm, int* rank, int* certified, double* coeffs);
   void test_lu(int device, double* a, int m, int n, int* piv);
   double bench_gemm(int device, int m, int n, int k, int iters);
+  // pivoted-Cholesky ID kernel timing: ntask tasks of an n x n Gram matrix of
+  // rank min(n, d); returns ms per batch, *steps = pivots taken
+  double bench_gram(int device, int n, int d, int ntask, int iters, int* steps);
 }  // namespace hssmf_b200

@@ -1,5 +1,6 @@
 #include "staging.cuh"
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -23,6 +24,34 @@ namespace hssmf_b200 {
     for (auto& e : ev_) cudaEventDestroy(e);
     cudaFreeHost(h_);
     cudaFree(d_);
+    if (hr_) cudaFreeHost(hr_);
+  }
+
+  bool Staging::d2h(void* dst, const void* src, size_t n) {
+    const size_t a = (n + 255) & ~size_t(255);
+    if (hr_used_ + a > hr_cap_) {
+      if (!pend_.empty()) return false;
+      if (hr_) HSSMF_CUDA(cudaFreeHost(hr_));
+      hr_cap_ = std::max<size_t>(2 * hr_cap_, std::max<size_t>(a, 1 << 20));
+      HSSMF_CUDA(cudaMallocHost((void**)&hr_, hr_cap_));
+    }
+    HSSMF_CUDA(cudaMemcpyAsync(hr_ + hr_used_, src, n, cudaMemcpyDeviceToHost, s_));
+    pend_.push_back({dst, hr_used_, n});
+    hr_used_ += a;
+    return true;
+  }
+
+  void Staging::complete() {
+    for (const auto& p : pend_) std::memcpy(p.dst, hr_ + p.off, p.n);
+    pend_.clear();
+    hr_used_ = 0;
+  }
+
+  void d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
+    if (!n) return;
+    if (Staging* st = current_staging(s))
+      if (st->d2h(dst, src, n)) return;
+    HSSMF_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
   }
 
   char* Staging::stage(const void* src, size_t n, char** dev) {

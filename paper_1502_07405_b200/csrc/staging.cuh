@@ -27,6 +27,11 @@ namespace hssmf_b200 {
     // stream-ordered copy of n host bytes to the device address dst through a
     // pinned chunk (false if n exceeds a chunk)
     bool copy_to(void* dst, const void* src, size_t n);
+    // device -> host read of n bytes into dst, staged through pinned memory
+    // and delivered to dst by complete() (stream_sync calls it); false if the
+    // pinned buffer cannot take it now
+    bool d2h(void* dst, const void* src, size_t n);
+    void complete();
 
    private:
     char* stage(const void* src, size_t n, char** dev);
@@ -38,11 +43,23 @@ namespace hssmf_b200 {
     char* d_ = nullptr;
     std::vector<cudaEvent_t> ev_;
     std::vector<char> armed_;
+    // pinned landing area of the pending device -> host reads
+    struct Pending {
+      void* dst;
+      size_t off, n;
+    };
+    char* hr_ = nullptr;
+    size_t hr_cap_ = 0, hr_used_ = 0;
+    std::vector<Pending> pend_;
   };
 
   // host -> device copy through the current staging ring of s when there is
   // one (pinned, truly asynchronous), else a plain cudaMemcpyAsync
   void h2d(void* dst, const void* src, size_t n, cudaStream_t s);
+  // device -> host read that the next stream_sync(s) completes (a pageable
+  // cudaMemcpyAsync blocks inside the driver and serialises the other front
+  // threads' CUDA calls; a pinned one does not)
+  void d2h(void* dst, const void* src, size_t n, cudaStream_t s);
 
   // process-wide ring per stream (created on first use)
   Staging* staging_for(cudaStream_t s);

@@ -68,7 +68,8 @@ def main():
             api[e["name"]][1] += d
             threads[e.get("tid")] += d
         elif c == "kernel":
-            nm = e["name"].replace("<unnamed>::", "").split("(")[0].split("::")[-1]
+            nm = e["name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+            nm = nm.split("(")[0].split("<")[0].split("::")[-1]
             kern[nm][0] += 1
             kern[nm][1] += d
             kiv.append((float(e["ts"]), float(e["ts"]) + d))
@@ -76,7 +77,12 @@ def main():
             t0 = min(t0, float(e["ts"]))
             t1 = max(t1, float(e["ts"]) + d)
     span = t1 - t0
+    mc = collections.Counter()
+    for e in ev:
+        if e.get("ph") == "X" and e.get("cat") in ("gpu_memcpy", "gpu_memset"):
+            mc[e["name"]] += 1
     out = {"config": a.config, "span_ms": span / 1e3, "gpu_busy_ms": union_len(kiv) / 1e3,
+           "copies": dict(mc),
            "api_ms_by_thread": {str(k): v / 1e3 for k, v in sorted(threads.items(), key=lambda x: -x[1])[:12]},
            "api": [(k, v[0], round(v[1] / 1e3, 2), round(v[1] / max(v[0], 1), 2))
                    for k, v in sorted(api.items(), key=lambda x: -x[1][1])[:20]],
