@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "staging.cuh"
@@ -21,6 +22,43 @@ namespace hssmf_b200 {
     };
     __device__ __forceinline__ bool better(double v, int p, double bv, int bp) {
       return v > bv || (v == bv && p < bp);
+    }
+
+    // ---- cluster push messaging: st.async into the peers' shared memory,
+    // completion counted in bytes on the receiver's mbarrier (no cluster
+    // barrier, no remote loads on the per-step critical path)
+    __device__ __forceinline__ uint32_t smem_u32(const void* p) {
+      return (uint32_t)__cvta_generic_to_shared(p);
+    }
+    __device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+      uint32_t r;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+      return r;
+    }
+    __device__ __forceinline__ void st_async_b64(uint32_t ra, unsigned long long v, uint32_t rbar) {
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                   :: "r"(ra), "l"(v), "r"(rbar) : "memory");
+    }
+    __device__ __forceinline__ void st_async_v2(uint32_t ra, unsigned long long a,
+                                                unsigned long long b, uint32_t rbar) {
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+                   :: "r"(ra), "l"(a), "l"(b), "r"(rbar) : "memory");
+    }
+    __device__ __forceinline__ void mbar_init(uint32_t a, int count) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(count) : "memory");
+    }
+    __device__ __forceinline__ void mbar_arrive_expect(uint32_t a, uint32_t bytes) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(bytes)
+                   : "memory");
+    }
+    __device__ __forceinline__ void mbar_wait(uint32_t a, int parity) {
+      asm volatile(
+          "{\n"
+          ".reg .pred P1;\n"
+          "WAIT_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+          "@!P1 bra WAIT_%=;\n"
+          "}\n" :: "r"(a), "r"(parity) : "memory");
     }
 
     // dynamic shared memory of one CTA (rows = own contiguous row block):
@@ -76,10 +114,11 @@ namespace hssmf_b200 {
       int* orig = reinterpret_cast<int*>(dg + rows);
       int* pos = orig + n;
       int* flg = pos + n;
-      __shared__ Cand pub[2];              // own candidate (double-buffered)
-      __shared__ double pubrow[2][kGramNB];  // its panel row
-      __shared__ Cand stc[16];             // all candidates of the cluster
-      __shared__ double strow[16][kGramNB];  // and their panel rows
+      // every CTA's candidate and that row's panel values, pushed by the
+      // owners (double-buffered by step parity, one mbarrier per buffer)
+      __shared__ __align__(16) Cand stc[2][16];
+      __shared__ __align__(16) double strow[2][16][kGramNB];
+      __shared__ __align__(8) unsigned long long mbar[2];
       __shared__ double wv[GW];
       __shared__ int wp[GW], wi[GW];
 
@@ -103,8 +142,31 @@ namespace hssmf_b200 {
       }
       for (int e = tid; e < rows * nb; e += GT) Lp[e] = 0.0;
       double r11 = init ? 0.0 : __ldcg(T.r11);
+      if (tid == 0) {
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
       __syncthreads();
+      // push this CTA's candidate (and nv values of its panel row) for the
+      // step whose buffer is b into every peer, this CTA included
+      auto push = [&](int b, const Cand& c, int nv) {
+        if (tid >= CL * 16) return;
+        const int peer = tid >> 4, l = tid & 15;
+        const uint32_t rbar = mapa(smem_u32(&mbar[b]), peer);
+        if (l == 0)
+          st_async_v2(mapa(smem_u32(&stc[b][rank]), peer), (unsigned long long)__double_as_longlong(c.v),
+                      (unsigned long long)(unsigned)c.pos | ((unsigned long long)(unsigned)c.idx << 32),
+                      rbar);
+        const uint32_t rrow = mapa(smem_u32(&strow[b][rank][0]), peer);
+        const int ci = c.idx - r0;
+        for (int q = l; q < nv; q += 16)
+          st_async_b64(rrow + 8u * q,
+                       (unsigned long long)__double_as_longlong(c.idx >= 0 ? Lp[(size_t)q * rows + ci] : 0.0),
+                       rbar);
+      };
       int j = k0, stopped = 0, cert = 0;
+      Cand c0{-1.0, INT_MAX, -1};
       if (n == 0 || T.kmax_dim == 0) {
         stopped = 1;
         cert = 1;
@@ -113,34 +175,21 @@ namespace hssmf_b200 {
         int bp = INT_MAX, bi = -1;
         for (int i = tid; i < nr; i += GT)
           if (!flg[i] && better(dg[i], pos[r0 + i], bv, bp)) { bv = dg[i]; bp = pos[r0 + i]; bi = r0 + i; }
-        const Cand c = block_best(bv, bp, bi, wv, wp, wi);
-        if (tid == 0) pub[0] = c;
+        c0 = block_best(bv, bp, bi, wv, wp, wi);
       }
-      cl.sync();
+      cl.sync();  // every peer's mbarriers are initialised
+      if (!stopped) push(0, c0, 0);
       for (int jj = 0; jj < nb && !stopped; jj++, j++) {
         const int buf = jj & 1;
-        // fetch every CTA's candidate and panel row (one DSMEM round trip)
-        if (tid < CL * 16) {
-          const int c = tid >> 4, l = tid & 15;
-          const double* rr = cl.map_shared_rank(&pubrow[buf][0], c);
-          // all remote loads in flight together, then the local stores
-          Cand cv;
-          if (l == 0) cv = *cl.map_shared_rank(&pub[buf], c);
-          double v[kGramNB / 16];
-#pragma unroll
-          for (int u = 0; u < kGramNB / 16; u++) v[u] = l + 16 * u < jj ? rr[l + 16 * u] : 0.0;
-          if (l == 0) stc[c] = cv;
-#pragma unroll
-          for (int u = 0; u < kGramNB / 16; u++)
-            if (l + 16 * u < jj) strow[c][l + 16 * u] = v[u];
-        }
-        __syncthreads();
+        // wait for every CTA's candidate and panel row of this step
+        if (tid == 0) mbar_arrive_expect(smem_u32(&mbar[buf]), (uint32_t)(CL * (16 + 8 * jj)));
+        mbar_wait(smem_u32(&mbar[buf]), (jj >> 1) & 1);
         // decision for step j, taken identically by every thread of every
         // CTA (rrqr.hpp:62-77: largest residual norm, lowest position on ties)
         int w = 0;
-        Cand best = stc[0];
+        Cand best = stc[buf][0];
         for (int c = 1; c < CL; c++)
-          if (better(stc[c].v, stc[c].pos, best.v, best.pos)) { best = stc[c]; w = c; }
+          if (better(stc[buf][c].v, stc[buf][c].pos, best.v, best.pos)) { best = stc[buf][c]; w = c; }
         const double pv = best.v > 0.0 ? sqrt(best.v) : 0.0;
         {
           int stop = 0, ct = 0;
@@ -163,7 +212,7 @@ namespace hssmf_b200 {
         }
         const int pj = best.idx;
         const double ljj = pv;
-        const double* prow = strow[w];
+        const double* prow = strow[buf][w];
         // CPQR column swap of positions j and pos(pj) (applied below by
         // thread 0 once every thread has read the old values)
         const int pp = pos[pj], ok = orig[j];
@@ -173,22 +222,24 @@ namespace hssmf_b200 {
         int bp = INT_MAX, bi = -1;
         for (int i = tid; i < nr; i += GT) {
           const int gi = r0 + i;
-          if (flg[i]) {
-            T.L[gi + (size_t)j * n] = 0.0;
-            continue;
-          }
+          if (flg[i]) continue;  // Lp stays 0 on pivoted rows
           if (gi == pj) {
             flg[i] = 1;
             Lp[(size_t)jj * rows + i] = ljj;
-            T.L[gi + (size_t)j * n] = ljj;
             continue;
           }
-          // lower triangle of G only (the trailing updates skip the upper one)
-          double sv = gi >= pj ? gcol[gi] : T.G[pj + (size_t)gi * n];
-          for (int q = 0; q < jj; q++) sv -= Lp[(size_t)q * rows + i] * prow[q];
-          const double lo = sv / ljj;
+          // lower triangle of G only (the trailing updates skip the upper one);
+          // the panel product is summed while the G load is in flight
+          const double gv = gi >= pj ? gcol[gi] : T.G[pj + (size_t)gi * n];
+          double t0 = 0.0, t1 = 0.0;
+          int q = 0;
+          for (; q + 1 < jj; q += 2) {
+            t0 += Lp[(size_t)q * rows + i] * prow[q];
+            t1 += Lp[(size_t)(q + 1) * rows + i] * prow[q + 1];
+          }
+          if (q < jj) t0 += Lp[(size_t)q * rows + i] * prow[q];
+          const double lo = (gv - (t0 + t1)) / ljj;
           Lp[(size_t)jj * rows + i] = lo;
-          T.L[gi + (size_t)j * n] = lo;
           double dd = dg[i] - lo * lo;
           if (dd < 0.0) dd = 0.0;
           dg[i] = dd;
@@ -208,12 +259,20 @@ namespace hssmf_b200 {
           j++;
           break;
         }
-        // publish the candidate for step j + 1 with its panel row (q <= jj)
-        if (tid == 0) pub[buf ^ 1] = c;
-        if (c.idx >= 0 && tid <= jj) pubrow[buf ^ 1][tid] = Lp[(size_t)tid * rows + (c.idx - r0)];
-        cl.sync();
+        // push the candidate for step j + 1 with its panel row (q <= jj)
+        push(buf ^ 1, c, jj + 1);
       }
       __syncthreads();
+      // the panel's columns of L, written once from shared memory (no global
+      // stores inside the step loop, so the per-step cluster barrier's release
+      // fence has nothing to drain); pivoted rows hold 0
+      {
+        const int ncol = j - k0;
+        for (int e = tid; e < ncol * nr; e += GT) {
+          const int q = e / nr, i = e - q * nr;
+          T.L[(r0 + i) + (size_t)(k0 + q) * n] = Lp[(size_t)q * rows + i];
+        }
+      }
       // write back the state for the next panel / the host
       for (int i = tid; i < nr; i += GT) {
         __stcg(T.dg + r0 + i, dg[i]);
@@ -231,7 +290,7 @@ namespace hssmf_b200 {
           __stcg(T.state + 2, cert);
         }
       }
-      cl.sync();  // peers may still read this CTA's shared memory
+      cl.sync();  // no CTA leaves while a peer may still address its shared memory
     }
   }  // namespace
 
@@ -256,10 +315,17 @@ namespace hssmf_b200 {
       kmax = std::max(kmax, t.kmax);
     }
     int CL = 1;
-    while (CL < 16 && max_n > CL * 128) CL *= 2;
+    // cluster size: one row per thread up to 16 CTAs (HSSMF_GRAM_MAXCL caps it;
+    // measurement knob: wide clusters need co-resident SMs of one GPC)
+    static const int max_cl = [] {
+      const char* e = getenv("HSSMF_GRAM_MAXCL");
+      const int v = e ? atoi(e) : 16;
+      return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 16;
+    }();
+    while (CL < max_cl && max_n > CL * GT) CL *= 2;
     const int rows = (max_n + CL - 1) / CL;
     int nb = kGramNB;
-    while (nb > 8 && gram_smem(max_n, rows, nb) > (size_t)kSmemCap) nb /= 2;
+    while (nb > 8 && gram_smem(max_n, rows, nb) > (size_t)kSmemCap) nb -= 8;
     if (gram_smem(max_n, rows, nb) > (size_t)kSmemCap)
       throw CudaError("gram id: node too large for the cluster shared memory");
     GramTask* d = nullptr;
