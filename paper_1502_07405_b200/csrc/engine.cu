@@ -204,12 +204,14 @@ namespace hssmf_b200 {
       FrontDev front{};
       DevMem keep, piv;
       int singular_col = -1;
+      bool oom = false;  // device memory ran out while fronts ran concurrently
       std::string msg, error;
     };
     std::vector<cudaStream_t> hstreams;  // concurrent HSS fronts of one level
     double* assemble_hss_front(int i);
     HssResult compress_hss_front(int i, double* F, cudaStream_t st);
     void factor_hss_level(const std::vector<int>& lst);
+    size_t devmem_bytes() const;  // engine-owned cudaMalloc storage
   };
 
   Engine::Engine(int device) : d_(new Impl), device_(device) {
@@ -625,16 +627,40 @@ namespace hssmf_b200 {
     const double t0 = now();
     std::vector<double> tq(lst.size()), tw(lst.size());
     std::vector<long long> nw_(lst.size());
+    // admission: a front starts only while the device pool is below the
+    // budget, unless nothing else runs (the rest is caught by the retry below)
+    cudaMemPool_t pool;
+    HSSMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    size_t dfree = 0, dtotal = 0;
+    HSSMF_CUDA(cudaMemGetInfo(&dfree, &dtotal));
+    // the pool's live bytes plus the engine's own (cudaMalloc) storage
+    const size_t budget = (size_t)(0.6 * (double)dtotal), fixed = devmem_bytes();
+    std::atomic<int> running{0};
     auto work = [&](int w) {
       cudaSetDevice(dev);
       for (int q = next++; q < (int)lst.size(); q = next++) {
+        for (;;) {
+          size_t used = 0;
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+          if (running.load() == 0 || used + fixed < budget) break;
+          std::this_thread::sleep_for(std::chrono::milliseconds(2));
+        }
+        running++;
         const double a = now();
         const SyncClock c0 = sync_clock();
         try {
           res[q] = compress_hss_front(lst[q], F[q], hstreams[w]);
+        } catch (const CudaError& e) {
+          // the front's own buffers are released on unwinding; its assembled
+          // dense front F is read-only in the HSS path, so it is retried alone
+          // once the concurrent fronts are done
+          res[q] = HssResult{};
+          if (strstr(e.what(), "out of memory")) res[q].oom = true;
+          else res[q].error = e.what();
         } catch (const std::exception& e) {
           res[q].error = e.what();
         }
+        running--;
         tq[q] = now() - a;
         tw[q] = sync_clock().wait_s - c0.wait_s;
         nw_[q] = sync_clock().n - c0.n;
@@ -647,8 +673,27 @@ namespace hssmf_b200 {
       for (int w = 0; w < nw; w++) th.emplace_back(work, w);
       for (auto& x : th) x.join();
     }
+    for (size_t q = 0; q < lst.size(); q++) {
+      if (!res[q].oom) continue;
+      for (auto st : hstreams) stream_sync(st);
+      if (dbg) fprintf(stderr, "[hssmf]   front %d: out of memory concurrently, retried alone\n", lst[q]);
+      const double a = now();
+      try {
+        res[q] = compress_hss_front(lst[q], F[q], hstreams[0]);
+      } catch (const std::exception& e) {
+        res[q].error = e.what();
+      }
+      tq[q] = now() - a;
+    }
     if (dbg) {
-      fprintf(stderr, "[hssmf] level: %zu HSS fronts, wall %.3f s\n", lst.size(), now() - t0);
+      cudaMemPool_t mp;
+      size_t used = 0, high = 0;
+      if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+        cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used);
+        cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemHigh, &high);
+      }
+      fprintf(stderr, "[hssmf] level: %zu HSS fronts, wall %.3f s, pool used %.1f GB (high %.1f GB)\n",
+              lst.size(), now() - t0, used / 1e9, high / 1e9);
       for (size_t q = 0; q < lst.size(); q++) {
         const auto& fn = t.nodes[lst[q]];
         fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s (sync wait %.3f s in %lld, arena %.0f MB) rounds=%d d=%d rank=%d |",
@@ -933,12 +978,12 @@ namespace hssmf_b200 {
       k.ms = k.flops = k.bytes = 0;
     }
   }
-  size_t Engine::device_bytes() const {
-    const auto& D = *d_;
-    size_t s = D.persist.bytes + D.ipersist.bytes + D.trans[0].bytes + D.trans[1].bytes +
-               D.bupd.bytes + D.d_val.bytes + D.d_ind.bytes + D.d_ptr.bytes + D.d_gemm.bytes;
-    for (auto& m : D.fallback_mem) s += m.bytes;
-    return s;
+  size_t Engine::Impl::devmem_bytes() const {
+    size_t b = persist.bytes + ipersist.bytes + trans[0].bytes + trans[1].bytes + bupd.bytes +
+               d_val.bytes + d_ind.bytes + d_ptr.bytes + d_gemm.bytes;
+    for (auto& m : fallback_mem) b += m.bytes;
+    return b;
   }
+  size_t Engine::device_bytes() const { return d_->devmem_bytes(); }
 
 }  // namespace hssmf_b200

@@ -161,6 +161,19 @@ namespace hssmf_b200 {
       }
     }
 
+    // C = sum_s W_s + beta C over the split-K partial products (fixed order)
+    __global__ void splitk_reduce_kernel(const double* __restrict__ W, int S, int m, int n,
+                                         double beta, double* __restrict__ C, int ldc) {
+      const long long tot = (long long)m * n, stride = (long long)gridDim.x * blockDim.x;
+      for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += stride) {
+        double v = W[e];
+        for (int q = 1; q < S; q++) v += W[e + q * tot];
+        const int i = (int)(e % m), j = (int)(e / m);
+        double* c = C + i + (size_t)j * ldc;
+        *c = beta == 0.0 ? v : v + beta * *c;
+      }
+    }
+
     void set_gemm_attrs() {
       static bool attr = false;
       if (attr) return;
@@ -204,6 +217,61 @@ namespace hssmf_b200 {
     std::vector<GemmProblem> q(p);
     for (auto& x : q) gemm_set_op(x, ta, tb, alpha, beta);
     gemm_run_mixed(q, s);
+  }
+
+  int gemm_splitk_factor(int m, int n, int k) {
+    // resident CTAs: 4 per SM (smem / registers of the 64 x 64 tile kernel)
+    const long long slots = 148LL * 4;
+    const long long tiles = (long long)ceil_div(m, BM) * ceil_div(n, BN);
+    if (tiles >= 4 * slots || k < 2048) return 1;
+    int best = 1;
+    double best_eff = 0;
+    for (int S = 1; S <= 8 && k / S >= 512; S++) {
+      const long long c = tiles * S;
+      const double eff = (double)c / (double)(((c + slots - 1) / slots) * slots);
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        best = S;
+      }
+    }
+    return best;
+  }
+
+  void gemm_run_splitk(const GemmProblem& p0, char ta, char tb, double alpha, double beta,
+                       cudaStream_t s) {
+    if (p0.m <= 0 || p0.n <= 0) return;
+    const int S = gemm_splitk_factor(p0.m, p0.n, p0.k);
+    if (S <= 1) {
+      gemm_run_host({p0}, ta, tb, alpha, beta, s);
+      return;
+    }
+    // K slices rounded to the k-step; partial products into a workspace,
+    // then one deterministic reduction
+    const int kc = ceil_div(ceil_div(p0.k, S), BK) * BK;
+    const long long mn = (long long)p0.m * p0.n;
+    double* W = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&W, (size_t)mn * S * sizeof(double), s));
+    std::vector<GemmProblem> parts;
+    int used = 0;
+    for (int q = 0; q < S; q++) {
+      const int k0 = q * kc, k1 = std::min(p0.k, k0 + kc);
+      if (k1 <= k0) break;
+      GemmProblem g = p0;
+      g.A = ta == 'N' ? p0.A + (size_t)k0 * p0.lda : p0.A + k0;
+      g.B = tb == 'N' ? p0.B + k0 : p0.B + (size_t)k0 * p0.ldb;
+      g.k = k1 - k0;
+      g.C = W + q * mn;
+      g.ldc = p0.m;
+      g.lower = 0;
+      gemm_set_op(g, ta, tb, alpha, 0.0);
+      parts.push_back(g);
+      used++;
+    }
+    gemm_run_mixed(parts, s);
+    const int blocks = (int)std::min<long long>((mn + 255) / 256, 148LL * 16);
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(W, used, p0.m, p0.n, beta, p0.C, p0.ldc);
+    HSSMF_LAUNCH_CHECK();
+    HSSMF_CUDA(cudaFreeAsync(W, s));
   }
 
   void gemm_run_mixed(const std::vector<GemmProblem>& p, cudaStream_t s) {

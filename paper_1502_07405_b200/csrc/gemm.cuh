@@ -58,5 +58,11 @@ namespace hssmf_b200 {
   void gemm_run_host(const std::vector<GemmProblem>& p, char ta, char tb, double alpha,
                      double beta, cudaStream_t s);
   void gemm_run_mixed(const std::vector<GemmProblem>& p, cudaStream_t s);
+  // one large-K problem with few output tiles: split-K over extra CTAs to fill
+  // the resident-CTA waves, partial products reduced in a fixed order
+  // (deterministic); falls back to a plain launch when splitting does not pay
+  int gemm_splitk_factor(int m, int n, int k);
+  void gemm_run_splitk(const GemmProblem& p, char ta, char tb, double alpha, double beta,
+                       cudaStream_t s);
 
 }  // namespace hssmf_b200

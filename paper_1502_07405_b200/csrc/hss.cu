@@ -326,10 +326,10 @@ namespace hssmf_b200 {
           rng_fill(seeds.p, 0, m, dold, d, R.col(dold), m, s);
           // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
           // hss_compress.hpp:359-363)
-          std::vector<GemmProblem> p1{{A, R.col(dold), Sr.col(dold), m, dn, m, (int)lda, m, m}};
-          gemm_run_host(p1, 'N', 'N', 1.0, 0.0, s);
-          std::vector<GemmProblem> p2{{A, R.col(dold), Sc.col(dold), m, dn, m, (int)lda, m, m}};
-          gemm_run_host(p2, 'T', 'N', 1.0, 0.0, s);
+          gemm_run_splitk({A, R.col(dold), Sr.col(dold), m, dn, m, (int)lda, m, m}, 'N', 'N', 1.0,
+                          0.0, s);
+          gemm_run_splitk({A, R.col(dold), Sc.col(dold), m, dn, m, (int)lda, m, m}, 'T', 'N', 1.0,
+                          0.0, s);
           flops += 4.0 * m * m * dn;
           R.cols = Sr.cols = Sc.cols = d;
           maxabs_run(Sr.col(dold), m, m, dn, scale.p, s);

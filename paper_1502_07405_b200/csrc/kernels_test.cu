@@ -42,9 +42,10 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemcpy(A.p, a, na * 8, cudaMemcpyHostToDevice));
     HSSMF_CUDA(cudaMemcpy(B.p, b, nb * 8, cudaMemcpyHostToDevice));
     HSSMF_CUDA(cudaMemcpy(C.p, c, nc * 8, cudaMemcpyHostToDevice));
-    std::vector<GemmProblem> p{{A.as<double>(), B.as<double>(), C.as<double>(), m, n, k, lda,
-                                ldb, ldc}};
-    gemm_run_host(p, ta, tb, alpha, beta, 0);
+    // single problems go through the split-K path (a plain launch when
+    // splitting does not pay), which is how the HSS sampling products run
+    gemm_run_splitk({A.as<double>(), B.as<double>(), C.as<double>(), m, n, k, lda, ldb, ldc}, ta,
+                    tb, alpha, beta, 0);
     HSSMF_CUDA(cudaMemcpy(c, C.p, nc * 8, cudaMemcpyDeviceToHost));
   }
 

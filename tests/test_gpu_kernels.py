@@ -11,7 +11,9 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (64, 64, 16), (130, 67, 45),
-                                   (257, 129, 300)])
+                                   (257, 129, 300),
+                                   # split-K (few output tiles, long K): the HSS sampling shape
+                                   (700, 96, 5003), (200, 128, 2048)])
 def test_gemm_matches_fp64(ta, tb, m, n, k):
     rng = np.random.default_rng(m * 1000 + n * 10 + k)
     a = rng.standard_normal((m, k) if ta == "N" else (k, m))
