@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 
 #include "common.cuh"
@@ -208,7 +210,18 @@ namespace hssmf_b200 {
       std::string msg, error;
     };
     std::vector<cudaStream_t> hstreams;  // concurrent HSS fronts of one level
-    double* assemble_hss_front(int i);
+    double* assemble_hss_front(int i, cudaStream_t st);
+    void assemble_on(int i, const FrontDev& view, cudaStream_t st);
+    void upload_front_on(int i, cudaStream_t st) {
+      HSSMF_CUDA(cudaMemcpyAsync(d_fronts.as<FrontDev>() + i, &hf[i], sizeof(FrontDev),
+                                 cudaMemcpyHostToDevice, st));
+    }
+    // dependency-driven factorization of the fronts from the deepest HSS
+    // level up (see factor_region)
+    void factor_region(const std::vector<int>& R);
+    std::vector<double*> region_c;  // pool-allocated update blocks of region fronts
+    std::vector<int> region_singular;  // first zero-pivot column per region front
+    int region_level = -1;             // deepest level holding an HSS front
     HssResult compress_hss_front(int i, double* F, cudaStream_t st);
     void factor_hss_level(const std::vector<int>& lst);
     size_t devmem_bytes() const;  // engine-owned cudaMalloc storage
@@ -295,6 +308,16 @@ namespace hssmf_b200 {
       D.want_hss[i] = f.level < o.switch_level() && f.m() >= o.min_hss && f.ns() > 0;
     }
 
+    // fronts from the deepest HSS level up run dependency-driven
+    // (factor_region); HSSMF_REGION=0 keeps the level-synchronous schedule
+    D.region_level = -1;
+    static const bool use_region = [] {
+      const char* e = getenv("HSSMF_REGION");
+      return !(e && e[0] == '0');
+    }();
+    if (use_region)
+      for (int i = 0; i < nn; i++)
+        if (D.want_hss[i]) D.region_level = std::max(D.region_level, D.t.nodes[i].level);
     D.lv.assign(nlev, {});
     auto& lv = D.lv;
     for (int i = 0; i < nn; i++) lv[D.t.nodes[i].level].push_back(i);
@@ -336,7 +359,9 @@ namespace hssmf_b200 {
       P.b_count = boff - P.b_off;
       P.p_bytes = poff - P.p_off;
       P.c_bytes = coff;
-      cmax[L % 2] = std::max(cmax[L % 2], coff);
+      // region levels (above the deepest HSS level) allocate update blocks
+      // per front; the static arenas only serve the levels below
+      if (D.region_level < 0 || L >= D.region_level) cmax[L % 2] = std::max(cmax[L % 2], coff);
     }
     // dense-front id lists (static plan)
     for (int L = nlev - 1; L >= 0; L--) {
@@ -370,7 +395,9 @@ namespace hssmf_b200 {
       h.ldc = h.nu;
       h.P = D.want_hss[i] ? nullptr : D.persist.as<double>(p_at[i]);
       h.U = D.want_hss[i] ? nullptr : D.persist.as<double>(u_at[i]);
-      h.C = D.trans[f.level % 2].as<double>(c_at[i]);
+      const bool region = D.region_level >= 0 &&
+                          (f.level < D.region_level || (f.level == D.region_level && D.want_hss[i]));
+      h.C = region ? nullptr : D.trans[f.level % 2].as<double>(c_at[i]);
       h.piv = D.want_hss[i] ? nullptr : D.ipersist.as<int>() + piv_at[i];
       h.perm = h.piv ? h.piv + h.ns : nullptr;
       h.upd = D.d_upd.as<int>() + upd_off[i];
@@ -501,40 +528,47 @@ namespace hssmf_b200 {
     factored_ = false;
   }
 
-  // dense assembly of HSS front i in HBM (assemble_dense semantics,
-  // multifrontal.hpp:141-170) on the engine stream; returns the m x m front
-  double* Engine::Impl::assemble_hss_front(int i) {
+  // assembly of front i into the storage named by view (assemble_dense
+  // semantics, multifrontal.hpp:141-170: sparse entries, then child0, child1
+  // extend-add) on stream st; the caller has zeroed the target
+  void Engine::Impl::assemble_on(int i, const FrontDev& view, cudaStream_t st) {
     const auto& fn = t.nodes[i];
-    auto& h = hf[i];
+    hf[i] = view;
+    upload_front_on(i, st);
+    long long cp[4] = {0, fn.child0 >= 0 ? t.nodes[fn.child0].nu() : 0, 0,
+                       fn.child1 >= 0 ? t.nodes[fn.child1].nu() : 0};
+    char* d = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&d, 64, st));
+    int* did = reinterpret_cast<int*>(d + 32);
+    long long* dcp = reinterpret_cast<long long*>(d);
+    HSSMF_CUDA(cudaMemcpyAsync(dcp, cp, sizeof(cp), cudaMemcpyHostToDevice, st));
+    HSSMF_CUDA(cudaMemcpyAsync(did, &i, sizeof(int), cudaMemcpyHostToDevice, st));
+    const FrontDev* Fd = d_fronts.as<FrontDev>();
+    DenseKernels::assemble_sparse(Fd, did, 1, d_ptr.as<int>(), d_ind.as<int>(), d_val.as<double>(), st);
+    DenseKernels::extend_add(Fd, did, 1, 0, dcp, cp[1], st);
+    DenseKernels::extend_add(Fd, did, 1, 1, dcp + 2, cp[3], st);
+    HSSMF_CUDA(cudaFreeAsync(d, st));
+  }
+
+  // dense assembly of HSS front i in HBM on stream st; returns the m x m front
+  double* Engine::Impl::assemble_hss_front(int i, cudaStream_t st) {
+    const auto& fn = t.nodes[i];
     const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
     double* F = nullptr;
-    HSSMF_CUDA(cudaMallocAsync((void**)&F, (size_t)m * m * sizeof(double) + 8, s));
-    HSSMF_CUDA(cudaMemsetAsync(F, 0, (size_t)m * m * sizeof(double), s));
-    FrontDev view = h;
+    HSSMF_CUDA(cudaMallocAsync((void**)&F, (size_t)m * m * sizeof(double) + 8 + (size_t)ns * 4, st));
+    HSSMF_CUDA(cudaMemsetAsync(F, 0, (size_t)m * m * sizeof(double), st));
+    FrontDev view = hf0[i];
     view.P = F;
     view.U = F + (size_t)ns * m;
     view.C = F + ns + (size_t)ns * m;
     view.ldu = m;
     view.ldc = m;
-    int* scr = scratch_ints(ns + 8);
-    view.perm = scr + 8;
-    hf[i] = view;
-    upload_front(i);
-    std::vector<int> one_id{i};
-    std::vector<long long> cp{0, fn.child0 >= 0 ? t.nodes[fn.child0].nu() : 0, 0,
-                              fn.child1 >= 0 ? t.nodes[fn.child1].nu() : 0};
-    HSSMF_CUDA(cudaMemcpyAsync(scr, one_id.data(), sizeof(int), cudaMemcpyHostToDevice, s));
-    long long* dcp = nullptr;
-    HSSMF_CUDA(cudaMallocAsync((void**)&dcp, 4 * sizeof(long long), s));
-    HSSMF_CUDA(cudaMemcpyAsync(dcp, cp.data(), 4 * sizeof(long long), cudaMemcpyHostToDevice, s));
-    const FrontDev* Fd = d_fronts.as<FrontDev>();
-    DenseKernels::assemble_sparse(Fd, scr, 1, d_ptr.as<int>(), d_ind.as<int>(), d_val.as<double>(), s);
-    DenseKernels::extend_add(Fd, scr, 1, 0, dcp, cp[1], s);
-    DenseKernels::extend_add(Fd, scr, 1, 1, dcp + 2, cp[3], s);
-    HSSMF_CUDA(cudaFreeAsync(dcp, s));
-    HSSMF_CUDA(cudaStreamSynchronize(s));
+    view.perm = reinterpret_cast<int*>(F + (size_t)m * m + 1);  // identity written by assembly
+    assemble_on(i, view, st);
+    stream_sync(st);
     hf[i] = hf0[i];
-    upload_front(i);
+    upload_front_on(i, st);
+    stream_sync(st);
     return F;
   }
 
@@ -612,7 +646,7 @@ namespace hssmf_b200 {
   void Engine::Impl::factor_hss_level(const std::vector<int>& lst) {
     if (lst.empty()) return;
     std::vector<double*> F(lst.size());
-    for (size_t q = 0; q < lst.size(); q++) F[q] = assemble_hss_front(lst[q]);
+    for (size_t q = 0; q < lst.size(); q++) F[q] = assemble_hss_front(lst[q], s);
     size_t width = hstreams.size();
     if (const char* e = getenv("HSSMF_HSS_STREAMS")) width = std::max(1, atoi(e));
     const int nw = (int)std::min<size_t>(lst.size(), std::min(width, hstreams.size()));
@@ -636,9 +670,15 @@ namespace hssmf_b200 {
     // the pool's live bytes plus the engine's own (cudaMalloc) storage
     const size_t budget = (size_t)(0.6 * (double)dtotal), fixed = devmem_bytes();
     std::atomic<int> running{0};
+    // largest fronts first, so that the longest compressions start at once
+    std::vector<int> order(lst.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return t.nodes[lst[a]].m() > t.nodes[lst[b]].m(); });
     auto work = [&](int w) {
       cudaSetDevice(dev);
-      for (int q = next++; q < (int)lst.size(); q = next++) {
+      for (int qi = next++; qi < (int)lst.size(); qi = next++) {
+        const int q = order[qi];
         for (;;) {
           size_t used = 0;
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
@@ -730,6 +770,259 @@ namespace hssmf_b200 {
   }
 
 
+  // Dependency-driven factorization of the region R: the HSS fronts of the
+  // deepest HSS level and every front above it. A front starts on one of the
+  // worker streams as soon as both children are done (no level barrier);
+  // ready fronts are taken by their remaining critical path (sum of m^2 up to
+  // the root). Update blocks of region fronts are pool allocations freed once
+  // the parent has assembled them. Dense region fronts are assembled into
+  // their persistent storage and factored by the dynamic partial LU.
+  void Engine::Impl::factor_region(const std::vector<int>& R) {
+    const int nn = (int)t.nodes.size();
+    if (R.empty()) return;
+    std::vector<char> inr(nn, 0);
+    for (int i : R) inr[i] = 1;
+    std::vector<int> pend(nn, 0);
+    std::vector<double> cpath(nn, 0.0);
+    for (int i = nn - 1; i >= 0; i--) {  // parents have larger ids (postorder)
+      const auto& f = t.nodes[i];
+      cpath[i] = (double)f.m() * f.m() + (f.parent >= 0 ? cpath[f.parent] : 0.0);
+    }
+    std::vector<int> ready;
+    for (int i : R) {
+      const auto& f = t.nodes[i];
+      for (int c : {f.child0, f.child1})
+        if (c >= 0 && inr[c]) pend[i]++;
+      if (!pend[i]) ready.push_back(i);
+    }
+    region_c.assign(nn, nullptr);
+    std::vector<HssResult> res(nn);
+    std::vector<int> singular(nn, -1);
+    std::vector<double> tq(nn, 0.0), tw(nn, 0.0), ts(nn, 0.0), peak(nn, 0.0);
+    std::mutex mu;
+    std::condition_variable cv;
+    int remaining = (int)R.size();
+    bool abort = false;
+    std::string err;
+    int dev = 0;
+    HSSMF_CUDA(cudaGetDevice(&dev));
+    size_t width = hstreams.size();
+    if (const char* e = getenv("HSSMF_HSS_STREAMS")) width = std::max(1, atoi(e));
+    const int nw = (int)std::min<size_t>(R.size(), std::min(width, hstreams.size()));
+    cudaMemPool_t pool;
+    HSSMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    size_t dfree = 0, dtotal = 0;
+    HSSMF_CUDA(cudaMemGetInfo(&dfree, &dtotal));
+    // admission by estimated peak: an HSS front holds its dense m x m front
+    // plus samples, Gram matrices and per-node bases, up to about 5.5 m^2
+    // doubles (C5, m = 16k: 11 GB); a dense region front its nu x nu block.
+    // Running fronts are charged their full estimate on top of the pool's
+    // current use (conservative: their allocations are counted twice).
+    const size_t budget = (size_t)(0.9 * (double)dtotal), fixed = devmem_bytes();
+    auto est = [&](int i) {
+      const auto& f = t.nodes[i];
+      const double m = f.m(), nu = f.nu();
+      return (size_t)(want_hss[i] ? 44.0 * m * m : 8.0 * nu * nu);
+    };
+    std::atomic<int> running{0};
+    std::atomic<size_t> charged{0};
+    std::atomic<bool> exclusive{false};
+    static const bool dbg = getenv("HSSMF_DEBUG") != nullptr;
+    auto now = [] {
+      return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t0 = now();
+
+    // one front on stream st; returns after its results are on the device
+    auto process = [&](int i, cudaStream_t st) {
+      const auto& fn = t.nodes[i];
+      const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
+      double* C = nullptr;
+      if (nu) HSSMF_CUDA(cudaMallocAsync((void**)&C, (size_t)nu * nu * sizeof(double), st));
+      // on an exception the front's own blocks go back to the pool (a retry
+      // allocates afresh)
+      struct Guard {
+        double*& c;
+        double* f = nullptr;
+        cudaStream_t st;
+        bool armed = true;
+        ~Guard() {
+          if (!armed) return;
+          if (c) cudaFreeAsync(c, st);
+          if (f) cudaFreeAsync(f, st);
+          c = nullptr;
+        }
+      } guard{C, nullptr, st};
+      if (want_hss[i]) {
+        hf0[i].C = C;
+        hf0[i].ldc = nu;
+        double* F = assemble_hss_front(i, st);
+        guard.f = F;
+        HssResult r = compress_hss_front(i, F, st);
+        guard.f = nullptr;  // compress_hss_front owns F from here on
+        if (r.hss) {
+          r.hss->set_stream(s);
+          hss[i] = std::move(r.hss);
+          hf[i] = hf0[i];
+          hf[i].hss = 1;
+        } else if (r.singular_col < 0) {
+          hf[i] = r.front;  // rank-guard fallback (C = the region block)
+        }
+        singular[i] = r.singular_col;
+        res[i] = std::move(r);
+      } else {
+        FrontDev f = hf0[i];
+        f.C = C;
+        f.ldc = nu;
+        HSSMF_CUDA(cudaMemsetAsync(f.P, 0, (size_t)m * ns * sizeof(double), st));
+        if (nu) {
+          HSSMF_CUDA(cudaMemsetAsync(f.U, 0, (size_t)ns * nu * sizeof(double), st));
+          HSSMF_CUDA(cudaMemsetAsync(C, 0, (size_t)nu * nu * sizeof(double), st));
+        }
+        assemble_on(i, f, st);
+        auto stt = partial_lu_dynamic({f}, st);
+        singular[i] = stt[0];
+        hf[i] = f;
+      }
+      upload_front_on(i, st);
+      stream_sync(st);
+      // the children's update blocks have been assembled: release them
+      for (int c : {fn.child0, fn.child1})
+        if (c >= 0 && region_c[c]) {
+          HSSMF_CUDA(cudaFreeAsync(region_c[c], st));
+          region_c[c] = nullptr;
+        }
+      region_c[i] = C;
+      guard.armed = false;
+    };
+
+    auto work = [&](int w) {
+      cudaSetDevice(dev);
+      const cudaStream_t st = hstreams[w];
+      for (;;) {
+        int i = -1;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return abort || remaining == 0 || !ready.empty(); });
+          if (abort || remaining == 0) return;
+          auto it = std::max_element(ready.begin(), ready.end(),
+                                     [&](int a, int b) { return cpath[a] < cpath[b]; });
+          i = *it;
+          ready.erase(it);
+        }
+        // admission: the estimated peak fits the budget, or nothing else runs
+        const size_t ei = est(i);
+        for (;;) {
+          size_t used = 0;
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+          if (!exclusive && (running.load() == 0 || used + fixed + charged.load() + ei < budget)) break;
+          std::this_thread::sleep_for(std::chrono::milliseconds(2));
+        }
+        running++;
+        charged += ei;
+        const double a = now();
+        ts[i] = a;
+        size_t used0 = 0;
+        if (dbg && nw <= 1) {  // serial debug runs measure each front's peak footprint
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used0);
+          size_t zero = 0;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+        }
+        const SyncClock c0 = sync_clock();
+        std::string e;
+        try {
+          try {
+            process(i, st);
+          } catch (const CudaError& x) {
+            if (!strstr(x.what(), "out of memory")) throw;
+            if (dbg) {
+              size_t used = 0;
+              cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+              fprintf(stderr, "[hssmf]   front %d m=%d: out of memory (pool %.1f GB, charged %.1f GB, "
+                      "engine %.1f GB, running %d): %s\n", i, t.nodes[i].m(), used / 1e9,
+                      charged.load() / 1e9, fixed / 1e9, running.load(), x.what());
+            }
+            // retry alone: no new front starts, the running ones drain; the
+            // pool's idle reserve goes back to the driver (module loads and
+            // cudaMalloc cannot use it)
+            exclusive = true;
+            running--;
+            while (running.load() > 0) std::this_thread::sleep_for(std::chrono::milliseconds(2));
+            running++;
+            for (auto hs : hstreams) stream_sync(hs);
+            cudaMemPoolTrimTo(pool, 0);
+            if (dbg) fprintf(stderr, "[hssmf]   front %d: out of memory concurrently, retried alone\n", i);
+            stream_sync(st);
+            process(i, st);
+            exclusive = false;
+          }
+        } catch (const std::exception& x) {
+          e = x.what();
+          exclusive = false;
+        }
+        running--;
+        charged -= ei;
+        if (dbg && nw <= 1) {
+          size_t hi = 0;
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi);
+          peak[i] = (double)(hi > used0 ? hi - used0 : 0);
+        }
+        tq[i] = now() - a;
+        tw[i] = sync_clock().wait_s - c0.wait_s;
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!e.empty()) {
+            if (!abort) err = "front " + std::to_string(i) + ": " + e;
+            abort = true;
+          } else {
+            remaining--;
+            const int p = t.nodes[i].parent;
+            if (p >= 0 && inr[p] && --pend[p] == 0) ready.push_back(p);
+          }
+        }
+        cv.notify_all();
+      }
+    };
+    if (nw <= 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int w = 0; w < nw; w++) th.emplace_back(work, w);
+      for (auto& x : th) x.join();
+    }
+    for (auto st : hstreams) stream_sync(st);
+    if (abort) throw CudaError(err);
+    for (int i : R) {
+      if (res[i].fallback) {
+        fallback_mem.push_back(std::move(res[i].keep));
+        fallback_mem.push_back(std::move(res[i].piv));
+      }
+      if (singular[i] >= 0) region_singular[i] = singular[i];
+    }
+    if (dbg) {
+      size_t used = 0, high = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high);
+      fprintf(stderr, "[hssmf] region: %zu fronts, wall %.3f s, pool used %.1f GB (high %.1f GB)\n",
+              R.size(), now() - t0, used / 1e9, high / 1e9);
+      for (int i : R) {
+        if (!want_hss[i]) continue;
+        const auto& fn = t.nodes[i];
+        HssMatrixDev* h = hss[i].get();
+        fprintf(stderr, "[hssmf]   front %d L%d m=%d ns=%d  start %.3f  %.3f s (sync wait %.3f s, peak %.2f GB = %.2f m^2 doubles) rounds=%d d=%d rank=%d |",
+                i, fn.level, fn.m(), fn.ns(), ts[i] - t0, tq[i], tw[i], peak[i] / 1e9,
+                peak[i] / (8.0 * fn.m() * (double)fn.m()), h ? h->rounds() : -1,
+                h ? h->d_final() : -1, h ? h->hss_rank() : -1);
+        if (h) {
+          auto ps = h->phase_stats();
+          for (int p = 0; p < kHssPhases; p++) fprintf(stderr, " %.0f", ps[p].ms);
+          h->restore_phase_stats(ps);
+        }
+        fprintf(stderr, "\n");
+      }
+    }
+  }
+
   void Engine::factor() {
     HSSMF_CUDA(cudaSetDevice(device_));
     auto& D = *d_;
@@ -750,8 +1043,10 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemsetAsync(D.status.p, 0xff, nn * sizeof(int), stream_));
     const FrontDev* F = D.d_fronts.as<FrontDev>();
     const int nlev = (int)D.levels.size();
-    std::vector<int> hss_fail_front, hss_fail_col;
+    D.region_singular.assign(nn, -1);
+    const int Lh = D.region_level;
     for (int L = nlev - 1; L >= 0; L--) {
+      if (Lh >= 0 && L < Lh) break;
       auto& P = D.levels[L];
       const int* ids = D.d_ids.as<int>() + P.dids_off;
       if (P.p_bytes)
@@ -782,7 +1077,19 @@ namespace hssmf_b200 {
         D.launch(K_GEMM_SCHUR, P.flops_schur, 0,
                  [&] { gemm_run(P.schur, 'N', 'N', -1.0, 1.0, stream_); });
       }
-      if (!P.hss.empty()) {
+      if (L == Lh) {
+        std::vector<int> R;
+        for (int i = 0; i < nn; i++) {
+          const int fl = D.t.nodes[i].level;
+          if (fl < Lh || (fl == Lh && D.want_hss[i])) R.push_back(i);
+        }
+        HSSMF_CUDA(cudaStreamSynchronize(stream_));
+        D.launch(K_HSS, 0, 0, [&] { D.factor_region(R); });
+        double hfl = 0;
+        for (int i : R)
+          if (D.hss[i]) hfl += D.hss[i]->flops();
+        if (profile_ && !D.evs.empty()) D.evs.back().flops = hfl;
+      } else if (!P.hss.empty()) {
         HSSMF_CUDA(cudaStreamSynchronize(stream_));
         D.launch(K_HSS, 0, 0, [&] { D.factor_hss_level(P.hss); });
         double hfl = 0;
@@ -815,11 +1122,13 @@ namespace hssmf_b200 {
       }
     }
     // first failure in postorder = the one the sequential reference reports
-    for (int i = 0; i < nn; i++)
-      if (st[i] >= 0)
-        throw SolverFailure(3, i, st[i],
+    for (int i = 0; i < nn; i++) {
+      const int col = st[i] >= 0 ? st[i] : D.region_singular[i];
+      if (col >= 0)
+        throw SolverFailure(3, i, col,
                             "front " + std::to_string(i) +
-                                ": exactly singular, zero pivot column " + std::to_string(st[i]));
+                                ": exactly singular, zero pivot column " + std::to_string(col));
+    }
     // stats (multifrontal.hpp:432-445, 496-500) and the solve lists
     std::vector<int> sids;
     for (int L = nlev - 1; L >= 0; L--) {
