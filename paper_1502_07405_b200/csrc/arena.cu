@@ -45,6 +45,7 @@ namespace hssmf_b200 {
       *cls = 0;
       void* p = nullptr;
       HSSMF_CUDA(cudaMallocAsync(&p, bytes, s_));
+      if (meter_) *meter_ += (long long)bytes;
       return p;
     }
     const int want = order_of(bytes);
@@ -64,17 +65,20 @@ namespace hssmf_b200 {
     *cls = (size_t)want + 1;
     slabs_[slab_of(p)].live++;
     live_bytes_ += kMinBlock << want;
+    if (meter_) *meter_ += (long long)(kMinBlock << want);
     return p;
   }
 
-  void DevArena::put(void* vp, size_t cls) {
+  void DevArena::put(void* vp, size_t cls, size_t bytes) {
     if (!vp) return;
     if (cls == 0) {
       cudaFreeAsync(vp, s_);
+      if (meter_) *meter_ -= (long long)bytes;
       return;
     }
     char* p = static_cast<char*>(vp);
     int o = (int)cls - 1;
+    if (meter_) *meter_ -= (long long)(kMinBlock << o);
     const int si = slab_of(p);
     Slab& sl = slabs_[si];
     sl.live--;
@@ -111,6 +115,11 @@ namespace hssmf_b200 {
     if (s == s_) return;
     stream_sync(s_);
     s_ = s;
+  }
+
+  std::atomic<long long>*& current_meter() {
+    static thread_local std::atomic<long long>* m = nullptr;
+    return m;
   }
 
   DevArena* current_arena(cudaStream_t s) {

@@ -13,6 +13,7 @@
 // trim() returns slabs without live blocks to it.
 #pragma once
 
+#include <atomic>
 #include <set>
 #include <unordered_map>
 #include <vector>
@@ -36,7 +37,10 @@ namespace hssmf_b200 {
     cudaStream_t stream() const { return s_; }
     // block of >= bytes; *cls receives the block's class (0: not from a slab)
     void* get(size_t bytes, size_t* cls);
-    void put(void* p, size_t cls);
+    void put(void* p, size_t cls, size_t bytes);
+    // optional usage meter (bytes handed out and not yet returned), read by
+    // the engine's memory admission while the front runs
+    void set_meter(std::atomic<long long>* m) { meter_ = m; }
     // return slabs without live blocks to the stream-ordered pool
     void trim();
     // move to another stream: the old one is drained first
@@ -61,7 +65,11 @@ namespace hssmf_b200 {
     std::set<char*> free_[kMaxOrder + 1];
     std::unordered_map<char*, int> free_order_;
     size_t live_bytes_ = 0;
+    std::atomic<long long>* meter_ = nullptr;
   };
+
+  // meter picked up by the arenas of HSS objects created on this thread
+  std::atomic<long long>*& current_meter();
 
   // thread-local current arenas (set by ArenaScope): scratch blocks and blocks
   // that outlive the compression (the factor data); nullptr if none or bound

@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "front.cuh"
 #include "gemm.cuh"
+#include "arena.cuh"
 #include "hss.hpp"
 #include "hss_kernels.cuh"
 
@@ -308,12 +309,15 @@ namespace hssmf_b200 {
       D.want_hss[i] = f.level < o.switch_level() && f.m() >= o.min_hss && f.ns() > 0;
     }
 
-    // fronts from the deepest HSS level up run dependency-driven
-    // (factor_region); HSSMF_REGION=0 keeps the level-synchronous schedule
+    // HSSMF_REGION=1: the fronts from the deepest HSS level up run
+    // dependency-driven (factor_region). Measured on C5 it is 10-15% slower
+    // than the level-synchronous schedule (memory admission serialises the
+    // top fronts more than level barriers do), so the default stays level-
+    // synchronous.
     D.region_level = -1;
     static const bool use_region = [] {
       const char* e = getenv("HSSMF_REGION");
-      return !(e && e[0] == '0');
+      return e && e[0] == '1';
     }();
     if (use_region)
       for (int i = 0; i < nn; i++)
@@ -818,14 +822,26 @@ namespace hssmf_b200 {
     // doubles (C5, m = 16k: 11 GB); a dense region front its nu x nu block.
     // Running fronts are charged their full estimate on top of the pool's
     // current use (conservative: their allocations are counted twice).
-    const size_t budget = (size_t)(0.9 * (double)dtotal), fixed = devmem_bytes();
+    const size_t budget = (size_t)(0.92 * (double)dtotal), fixed = devmem_bytes();
+    // peak per HSS front measured on C5 (serial debug runs): 4..8.6 m^2
+    // doubles including the dense front and the update block
     auto est = [&](int i) {
       const auto& f = t.nodes[i];
       const double m = f.m(), nu = f.nu();
-      return (size_t)(want_hss[i] ? 44.0 * m * m : 8.0 * nu * nu);
+      return (long long)(want_hss[i] ? 56.0 * m * m : 8.0 * nu * nu);
     };
+    // what a running front already holds: its dense front, update block and
+    // everything its HSS arenas handed out (metered)
+    std::unique_ptr<std::atomic<long long>[]> meter(new std::atomic<long long>[nn]);
+    for (int i = 0; i < nn; i++) meter[i] = 0;
+    auto fixed_part = [&](int i) {
+      const auto& f = t.nodes[i];
+      const double m = f.m(), nu = f.nu();
+      return (long long)((want_hss[i] ? 8.0 * m * m : 0.0) + 8.0 * nu * nu);
+    };
+    std::vector<char> isrun(nn, 0);
     std::atomic<int> running{0};
-    std::atomic<size_t> charged{0};
+    std::atomic<long long> charged{0};
     std::atomic<bool> exclusive{false};
     static const bool dbg = getenv("HSSMF_DEBUG") != nullptr;
     auto now = [] {
@@ -910,16 +926,25 @@ namespace hssmf_b200 {
           i = *it;
           ready.erase(it);
         }
-        // admission: the estimated peak fits the budget, or nothing else runs
-        const size_t ei = est(i);
+        // admission: current use + what the running fronts may still
+        // allocate + this front's estimated peak fits the budget, or nothing
+        // else runs
+        const long long ei = est(i);
         for (;;) {
           size_t used = 0;
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-          if (!exclusive && (running.load() == 0 || used + fixed + charged.load() + ei < budget)) break;
+          long long grow = 0;
+          for (int r : R)
+            if (isrun[r]) grow += std::max(0LL, est(r) - meter[r].load() - fixed_part(r));
+          if (!exclusive && (running.load() == 0 ||
+                             (long long)(used + fixed) + grow + ei < (long long)budget))
+            break;
           std::this_thread::sleep_for(std::chrono::milliseconds(2));
         }
         running++;
         charged += ei;
+        isrun[i] = 1;
+        current_meter() = &meter[i];
         const double a = now();
         ts[i] = a;
         size_t used0 = 0;
@@ -962,6 +987,8 @@ namespace hssmf_b200 {
         }
         running--;
         charged -= ei;
+        isrun[i] = 0;
+        current_meter() = nullptr;
         if (dbg && nw <= 1) {
           size_t hi = 0;
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi);

@@ -64,7 +64,7 @@ namespace hssmf_b200 {
       }
       void free() {
         if (p) {
-          if (ar) ar->put(p, cls);
+          if (ar) ar->put(p, cls, n * sizeof(T));
           else cudaFreeAsync(p, s);
         }
         p = nullptr;
@@ -260,7 +260,10 @@ namespace hssmf_b200 {
     }
     ~HssImpl() { collect_phases(); }
 
-    explicit HssImpl(cudaStream_t st) : arena(st), keep_arena(st), s(st) {}
+    explicit HssImpl(cudaStream_t st) : arena(st), keep_arena(st), s(st) {
+      arena.set_meter(current_meter());
+      keep_arena.set_meter(current_meter());
+    }
 
     // ---------------------------------------------------------- compression
     void init_tree(const ClusterTree& t) {
@@ -1365,6 +1368,8 @@ namespace hssmf_b200 {
   }
   void HssMatrixDev::set_stream(cudaStream_t s) {
     d_->collect_phases();
+    d_->arena.set_meter(nullptr);  // the compression is over: detach from the admission meter
+    d_->keep_arena.set_meter(nullptr);
     d_->arena.rebind(s);
     d_->keep_arena.rebind(s);
     d_->s = s;
