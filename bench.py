@@ -290,7 +290,7 @@ def reference_arm(args, cfg, op):
     line = {
         "metric": METRIC, "value": scaled, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": scaled * 1e3,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_json(cfg, op, args),
         "cpu_baseline": {"value": scaled, "unit": "s", "cores": thr, "kind": "reference",
                          "sample": desc + f"; measured {t:.3f} s/step, scaled x{tfl / sfl:.1f}"},
@@ -316,7 +316,7 @@ def config_json(cfg, op, args):
     return {"workload": cfg.name, "n": op.a.size(), "nnz": op.a.nnz(), "fronts": op.t.size(),
             "nd_leaf": cfg.nd_leaf, "hss": {"ls": cfg.ls, "min_hss": cfg.min_hss,
                                             "eps": cfg.eps, "leaf": cfg.leaf, "mode": cfg.mode},
-            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "parallelism": f"subtree{args.gpus}" if args.gpus > 1 else "single",
             "l2": "inputs > L2 (factor storage tens of GB), no flush needed"}
 
 
@@ -362,16 +362,34 @@ def main():
     opts = cfg.solver_options()
     peaks = measured_peaks(torch, dev)
 
-    # first factorization (upload + schedule + numeric)
-    m = P.mf_factor(op.a, op.t, opts, device=local)
     b_dev = torch.from_numpy(b).to(dev)
     x_dev = torch.empty_like(b_dev)
+    dist_mode = world > 1
+    if dist_mode:
+        # subtree-to-GPU partition: rank r factors its subtree
+        # and the top fronts it owns; updates / bupd / x(upd) cross GPUs over
+        # NCCL point-to-point at the subtree roots only
+        from paper_1502_07405_b200.parallel import DistributedMf, TorchTransport
+        m = DistributedMf(op.a, op.t, opts, world, rank=rank, transport=TorchTransport(dev),
+                          device=local)
+        eng = m.engines[rank].m
+        xs = {rank: x_dev.view(1, n)}
 
-    def step():
-        m.refactor()
-        x_dev.copy_(b_dev)
-        torch.cuda.current_stream(dev).synchronize()
-        m.solve_device(x_dev.data_ptr(), n, 1)
+        def step():
+            m.factor()
+            x_dev.copy_(b_dev)
+            torch.cuda.current_stream(dev).synchronize()
+            m.solve_device(xs)
+    else:
+        # first factorization (upload + schedule + numeric)
+        m = P.mf_factor(op.a, op.t, opts, device=local)
+        eng = m
+
+        def step():
+            m.refactor()
+            x_dev.copy_(b_dev)
+            torch.cuda.current_stream(dev).synchronize()
+            m.solve_device(x_dev.data_ptr(), n, 1)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -388,7 +406,7 @@ def main():
     dev_ms = 0.0
     for _ in range(args.steps):
         step()
-        f, s = m.timing()
+        f, s = eng.timing()
         dev_ms += f + s
     barrier()
     t1 = time.perf_counter()
@@ -400,19 +418,35 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
 
-    # correctness of the timed factors (relative residual)
-    x = x_dev.cpu().numpy()
+    # correctness of the timed factors (relative residual); multi-GPU: every
+    # rank holds its own separators, summed once into the full solution
+    if dist_mode:
+        xc = m.combine(xs)
+        dist.all_reduce(xc)
+        x = xc.view(-1).cpu().numpy()
+    else:
+        x = x_dev.cpu().numpy()
     relres = float(np.linalg.norm(op.a.matvec(x) - b) / np.linalg.norm(b))
 
-    # e2e through the public API: mf_factor(host CSR) + mf_solve_new(host b)
-    del m
+    # e2e through the public API: factor from the host CSR + solve of host b
+    del m, eng
     torch.cuda.empty_cache()
     barrier()
     e0 = time.perf_counter()
     for _ in range(max(1, min(args.steps, 2))):
-        m = P.mf_factor(op.a, op.t, opts, device=local)
-        xh = P.mf_solve_new(m, b)
-        del m
+        if dist_mode:
+            md = DistributedMf(op.a, op.t, opts, world, rank=rank, transport=TorchTransport(dev),
+                               device=local)
+            md.factor()
+            xl = md.solve(b)
+            xt = torch.from_numpy(np.ascontiguousarray(xl)).to(dev)
+            dist.all_reduce(xt)
+            xh = xt.cpu().numpy()
+            del md
+        else:
+            md = P.mf_factor(op.a, op.t, opts, device=local)
+            xh = P.mf_solve_new(md, b)
+            del md
     barrier()
     e_ms = (time.perf_counter() - e0) / max(1, min(args.steps, 2)) * 1e3
     h2d = int(ptr.nbytes + ind.nbytes + val.nbytes + b.nbytes)
@@ -421,14 +455,25 @@ def main():
     # per-kernel-class profile pass (events around each launch)
     # HSS fronts of a level normally run concurrently on several streams; the
     # profiled step runs them one at a time so per-class device times add up
+    # (multi-GPU: rank 0's share of a partitioned step)
     os.environ["HSSMF_HSS_STREAMS"] = "1"
-    m = P.mf_factor(op.a, op.t, opts, device=local)
-    m.set_profile(True)
-    m.reset_kernel_stats()
-    m.refactor()
-    m.solve_device(x_dev.data_ptr(), n, 1)
-    ks = m.kernel_stats()
-    m.set_profile(False)
+    if dist_mode:
+        mp_ = DistributedMf(op.a, op.t, opts, world, rank=rank, transport=TorchTransport(dev),
+                            device=local)
+        ep = mp_.engines[rank].m
+        ep.set_profile(True)
+        ep.reset_kernel_stats()
+        mp_.factor()
+        x_dev.copy_(b_dev)
+        mp_.solve_device({rank: x_dev.view(1, n)})
+    else:
+        ep = P.mf_factor(op.a, op.t, opts, device=local)
+        ep.set_profile(True)
+        ep.reset_kernel_stats()
+        ep.refactor()
+        ep.solve_device(x_dev.data_ptr(), n, 1)
+    ks = ep.kernel_stats()
+    ep.set_profile(False)
     os.environ.pop("HSSMF_HSS_STREAMS", None)
     # hss_front_total wraps the hss_* phases: keep the leaves of the breakdown
     ks = [k for k in ks if k["name"] != "hss_front_total"]
@@ -451,7 +496,7 @@ def main():
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_json(cfg, op, args),
         "device_ms_per_step": dev_ms / args.steps,
         "relres": relres,

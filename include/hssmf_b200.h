@@ -115,6 +115,36 @@ int hssmf_refactor(hssmf_factors* f, const double* val, int on_device, hssmf_sta
  * leading dimension ldb, in the tree ordering, solved in place; host or device */
 int hssmf_solve(hssmf_factors* f, double* b, int ldb, int nrhs, int on_device,
                 hssmf_status* st);
+/* ---- multi-GPU subtree partition (no reference counterpart:
+ * the reference is single-node OpenMP, multifrontal.hpp:398-503 is the
+ * sequential schedule these phases reproduce) ----
+ * analysis with an ownership mask (one char per front): only owned fronts are
+ * factored / solved by this handle; the update blocks and forward
+ * contributions of their non-owned children are imported between phases. */
+int hssmf_analyze_owned(int device, const hssmf_csr* a, const hssmf_tree* t,
+                        const hssmf_options* o, const char* owned, hssmf_factors** out,
+                        hssmf_status* st);
+int hssmf_nlevels(const hssmf_factors* f);
+/* factor the owned fronts of tree levels lo..hi (deepest first); the phase
+ * with hi = nlevels-1 starts a new factorization, the one with lo = 0 ends it */
+int hssmf_factor_levels(hssmf_factors* f, int lo, int hi, hssmf_status* st);
+/* update block of a front (nu x nu, ld nu): what factor_front passes to the
+ * parent (multifrontal.hpp:340-344 dense cb, :369-376 HSS Schur operator) */
+int hssmf_update_export(const hssmf_factors* f, int front, double* dst, int on_device,
+                        hssmf_status* st);
+int hssmf_update_import(hssmf_factors* f, int front, const double* src, int on_device,
+                        hssmf_status* st);
+/* forward-sweep contribution of a front (nu x nrhs, ld nu, device memory):
+ * the bupd mf_forward passes up (multifrontal.hpp:545-560) */
+int hssmf_bupd_export(const hssmf_factors* f, int front, double* dst, int nrhs,
+                      hssmf_status* st);
+int hssmf_bupd_import(hssmf_factors* f, int front, const double* src, int nrhs,
+                      hssmf_status* st);
+/* one sweep of the solve over levels lo..hi on device x (n x nrhs, ld ldx):
+ * forward = 1 (deepest first) or backward = 0 (root first) */
+int hssmf_solve_levels(hssmf_factors* f, double* x, int ldx, int nrhs, int lo, int hi,
+                       int forward, hssmf_status* st);
+
 /* MfFactors::{front_stats, hss_fronts, fallbacks, max_front_rank, factor_nnz()}
  * (multifrontal.hpp:454-468); type 0 dense 1 hss 2 hss_dense */
 void hssmf_factor_summary(const hssmf_factors* f, int* nnodes, int* hss_fronts,

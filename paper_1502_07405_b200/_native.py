@@ -58,6 +58,15 @@ _SIGS = {
     "hssmf_factor": (C.c_int, [C.c_int, vp, vp, C.POINTER(Options), C.POINTER(vp),
                                C.POINTER(Status)]),
     "hssmf_refactor": (C.c_int, [vp, vp, C.c_int, C.POINTER(Status)]),
+    "hssmf_analyze_owned": (C.c_int, [C.c_int, vp, vp, vp, vp, C.POINTER(vp), C.POINTER(Status)]),
+    "hssmf_nlevels": (C.c_int, [vp]),
+    "hssmf_factor_levels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(Status)]),
+    "hssmf_update_export": (C.c_int, [vp, C.c_int, vp, C.c_int, C.POINTER(Status)]),
+    "hssmf_update_import": (C.c_int, [vp, C.c_int, vp, C.c_int, C.POINTER(Status)]),
+    "hssmf_bupd_export": (C.c_int, [vp, C.c_int, vp, C.c_int, C.POINTER(Status)]),
+    "hssmf_bupd_import": (C.c_int, [vp, C.c_int, vp, C.c_int, C.POINTER(Status)]),
+    "hssmf_solve_levels": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(Status)]),
     "hssmf_solve": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Status)]),
     "hssmf_factor_summary": (None, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                     C.POINTER(C.c_int), C.POINTER(C.c_int),

@@ -315,6 +315,11 @@ class MfFactors:
     def __init__(self, handle, n):
         self._h = handle
         self.n = n
+        self.refresh()
+        self.factored = True
+
+    def refresh(self):
+        """re-read the summary and per-front stats (after factor phases)"""
         L = N.lib()
         nn, hf, fb, mr, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_longlong()
         L.hssmf_factor_summary(self._h, C.byref(nn), C.byref(hf), C.byref(fb), C.byref(mr),
@@ -327,7 +332,6 @@ class MfFactors:
         self.flops = np.zeros(nn, np.int64)
         L.hssmf_front_stats(self._h, self.level, self.dim, self.sep, self.rank, self.flops,
                             self.type)
-        self.factored = True
 
     @property
     def front_stats(self):

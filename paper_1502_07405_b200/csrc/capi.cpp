@@ -262,6 +262,53 @@ int hssmf_factor(int device, const hssmf_csr* a, const hssmf_tree* t, const hssm
   return rc;
 }
 
+int hssmf_analyze_owned(int device, const hssmf_csr* a, const hssmf_tree* t,
+                        const hssmf_options* o, const char* owned, hssmf_factors** out,
+                        hssmf_status* st) {
+  *out = nullptr;
+  auto f = std::make_unique<hssmf_factors>();
+  const int rc = guard(st, [&] {
+    f->e = std::make_unique<Engine>(device);
+    f->e->analyze(a->a, t->t, to_opts(o), owned);
+  });
+  if (rc == HSSMF_OK) *out = f.release();
+  return rc;
+}
+
+int hssmf_nlevels(const hssmf_factors* f) { return f->e->nlevels(); }
+
+int hssmf_factor_levels(hssmf_factors* f, int lo, int hi, hssmf_status* st) {
+  return guard(st, [&] { f->e->factor_levels(lo, hi); });
+}
+
+int hssmf_update_export(const hssmf_factors* f, int front, double* dst, int on_device,
+                        hssmf_status* st) {
+  return guard(st, [&] { f->e->export_update(front, dst, on_device != 0); });
+}
+
+int hssmf_update_import(hssmf_factors* f, int front, const double* src, int on_device,
+                        hssmf_status* st) {
+  return guard(st, [&] { f->e->import_update(front, src, on_device != 0); });
+}
+
+int hssmf_bupd_export(const hssmf_factors* f, int front, double* dst, int nrhs,
+                      hssmf_status* st) {
+  return guard(st, [&] { f->e->export_bupd(front, dst, nrhs); });
+}
+
+int hssmf_bupd_import(hssmf_factors* f, int front, const double* src, int nrhs,
+                      hssmf_status* st) {
+  return guard(st, [&] { f->e->import_bupd(front, src, nrhs); });
+}
+
+int hssmf_solve_levels(hssmf_factors* f, double* x, int ldx, int nrhs, int lo, int hi,
+                       int forward, hssmf_status* st) {
+  return guard(st, [&] {
+    if (ldx < f->e->n()) throw SolverFailure(1, -1, -1, "mf solve: rhs rows mismatch");
+    f->e->solve_levels(x, ldx, nrhs, lo, hi, forward != 0);
+  });
+}
+
 int hssmf_refactor(hssmf_factors* f, const double* val, int on_device, hssmf_status* st) {
   return guard(st, [&] {
     if (val) f->e->set_values(val, on_device != 0);

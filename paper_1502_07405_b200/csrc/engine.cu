@@ -220,6 +220,9 @@ namespace hssmf_b200 {
     // dependency-driven factorization of the fronts from the deepest HSS
     // level up (see factor_region)
     void factor_region(const std::vector<int>& R);
+    std::vector<char> owned;        // fronts factored by this engine
+    std::vector<int> boundary;      // non-owned children of owned fronts
+    std::vector<DevMem> imported;   // imported update blocks (per front)
     std::vector<double*> region_c;  // pool-allocated update blocks of region fronts
     std::vector<int> region_singular;  // first zero-pivot column per region front
     int region_level = -1;             // deepest level holding an HSS front
@@ -259,7 +262,7 @@ namespace hssmf_b200 {
     if (stream_) cudaStreamDestroy(stream_);
   }
 
-  void Engine::analyze(const Csr& a, const Etree& t, const Options& o) {
+  void Engine::analyze(const Csr& a, const Etree& t, const Options& o, const char* owned) {
     HSSMF_CUDA(cudaSetDevice(device_));
     auto& D = *d_;
     if (a.n != t.n) throw SolverFailure(1, -1, -1, "mf factor: matrix and tree sizes differ");
@@ -270,6 +273,22 @@ namespace hssmf_b200 {
     n_ = a.n;
     factored_ = false;
     const int nn = (int)D.t.nodes.size();
+    D.owned.assign(nn, 1);
+    bool partial = false;
+    if (owned)
+      for (int i = 0; i < nn; i++) {
+        D.owned[i] = owned[i] ? 1 : 0;
+        partial |= !owned[i];
+      }
+    D.boundary.clear();
+    if (partial)
+      for (int i = 0; i < nn; i++) {
+        if (!D.owned[i]) continue;
+        for (int c : {D.t.nodes[i].child0, D.t.nodes[i].child1})
+          if (c >= 0 && !D.owned[c]) D.boundary.push_back(c);
+      }
+    D.imported.clear();
+    D.imported.resize(nn);
     int nlev = 0;
     for (const auto& f : D.t.nodes) nlev = std::max(nlev, f.level + 1);
 
@@ -306,7 +325,7 @@ namespace hssmf_b200 {
     D.want_hss.assign(nn, 0);
     for (int i = 0; i < nn; i++) {
       const auto& f = D.t.nodes[i];
-      D.want_hss[i] = f.level < o.switch_level() && f.m() >= o.min_hss && f.ns() > 0;
+      D.want_hss[i] = D.owned[i] && f.level < o.switch_level() && f.m() >= o.min_hss && f.ns() > 0;
     }
 
     // HSSMF_REGION=1: the fronts from the deepest HSS level up run
@@ -319,12 +338,13 @@ namespace hssmf_b200 {
       const char* e = getenv("HSSMF_REGION");
       return e && e[0] == '1';
     }();
-    if (use_region)
+    if (use_region && !partial)
       for (int i = 0; i < nn; i++)
         if (D.want_hss[i]) D.region_level = std::max(D.region_level, D.t.nodes[i].level);
     D.lv.assign(nlev, {});
     auto& lv = D.lv;
-    for (int i = 0; i < nn; i++) lv[D.t.nodes[i].level].push_back(i);
+    for (int i = 0; i < nn; i++)
+      if (D.owned[i]) lv[D.t.nodes[i].level].push_back(i);
     D.levels.assign(nlev, LevelPlan());
     std::vector<int> ids;
 
@@ -375,6 +395,10 @@ namespace hssmf_b200 {
         if (!D.want_hss[i]) ids.push_back(i);
       P.ndf = (int)ids.size() - P.dids_off;
     }
+    for (int c : D.boundary) {  // imported forward contributions of remote children
+      D.bupd_off[c] = boff;
+      boff += D.t.nodes[c].nu();
+    }
     D.bupd_total = boff;
     D.persist.alloc(std::max<size_t>(poff, 256));
     D.ipersist.alloc(std::max<size_t>(ipoff * sizeof(int), 256));
@@ -397,12 +421,13 @@ namespace hssmf_b200 {
       h.hss = D.want_hss[i];
       h.ldu = h.ns;
       h.ldc = h.nu;
-      h.P = D.want_hss[i] ? nullptr : D.persist.as<double>(p_at[i]);
-      h.U = D.want_hss[i] ? nullptr : D.persist.as<double>(u_at[i]);
+      const bool store = D.owned[i] && !D.want_hss[i];
+      h.P = store ? D.persist.as<double>(p_at[i]) : nullptr;
+      h.U = store ? D.persist.as<double>(u_at[i]) : nullptr;
       const bool region = D.region_level >= 0 &&
                           (f.level < D.region_level || (f.level == D.region_level && D.want_hss[i]));
-      h.C = region ? nullptr : D.trans[f.level % 2].as<double>(c_at[i]);
-      h.piv = D.want_hss[i] ? nullptr : D.ipersist.as<int>() + piv_at[i];
+      h.C = (region || !D.owned[i]) ? nullptr : D.trans[f.level % 2].as<double>(c_at[i]);
+      h.piv = store ? D.ipersist.as<int>() + piv_at[i] : nullptr;
       h.perm = h.piv ? h.piv + h.ns : nullptr;
       h.upd = D.d_upd.as<int>() + upd_off[i];
       h.pos0 = pos_off0[i] >= 0 ? D.d_pos.as<int>() + pos_off0[i] : nullptr;
@@ -1050,29 +1075,38 @@ namespace hssmf_b200 {
     }
   }
 
-  void Engine::factor() {
+  int Engine::nlevels() const { return (int)d_->levels.size(); }
+
+  void Engine::factor_levels(int lo, int hi) {
     HSSMF_CUDA(cudaSetDevice(device_));
     auto& D = *d_;
     D.profile = profile_;
     hss_set_phase_timing(profile_ || getenv("HSSMF_DEBUG") != nullptr);
     const int nn = (int)D.hf.size();
-    // previous HSS / fallback state is rebuilt
-    D.hss.clear();
-    D.hss.resize(nn);
-    D.fallback_mem.clear();
-    D.hf = D.hf0;
-    D.upload_fronts();
-    D.n_hss = D.n_fallback = D.max_rank = 0;
+    const int nlev = (int)D.levels.size();
+    lo = std::max(lo, 0);
+    hi = std::min(hi, nlev - 1);
+    const bool first = hi == nlev - 1;
+    if (first) {
+      // previous HSS / fallback state is rebuilt
+      D.hss.clear();
+      D.hss.resize(nn);
+      D.fallback_mem.clear();
+      D.hf = D.hf0;
+      D.upload_fronts();
+      D.n_hss = D.n_fallback = D.max_rank = 0;
+      D.region_singular.assign(nn, -1);
+      HSSMF_CUDA(cudaMemsetAsync(D.status.p, 0xff, nn * sizeof(int), stream_));
+      factor_ms_ = 0;
+      factored_ = false;
+    }
     cudaEvent_t e0, e1;
     HSSMF_CUDA(cudaEventCreate(&e0));
     HSSMF_CUDA(cudaEventCreate(&e1));
     HSSMF_CUDA(cudaEventRecord(e0, stream_));
-    HSSMF_CUDA(cudaMemsetAsync(D.status.p, 0xff, nn * sizeof(int), stream_));
     const FrontDev* F = D.d_fronts.as<FrontDev>();
-    const int nlev = (int)D.levels.size();
-    D.region_singular.assign(nn, -1);
     const int Lh = D.region_level;
-    for (int L = nlev - 1; L >= 0; L--) {
+    for (int L = hi; L >= lo; L--) {
       if (Lh >= 0 && L < Lh) break;
       auto& P = D.levels[L];
       const int* ids = D.d_ids.as<int>() + P.dids_off;
@@ -1132,7 +1166,7 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaStreamSynchronize(stream_));
     float ms = 0;
     HSSMF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    factor_ms_ = ms;
+    factor_ms_ += ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (profile_) {
@@ -1182,7 +1216,51 @@ namespace hssmf_b200 {
       }
       D.max_rank = std::max(D.max_rank, s.rank);
     }
-    factored_ = true;
+    factored_ = lo == 0;
+  }
+
+  void Engine::export_update(int f, double* dst, bool on_device) const {
+    const auto& D = *d_;
+    const int nu = D.t.nodes[f].nu();
+    const FrontDev& h = D.hf[f];
+    if (!nu) return;
+    if (!h.C) throw SolverFailure(2, f, -1, "export_update: front has no update block here");
+    HSSMF_CUDA(cudaMemcpy2DAsync(dst, (size_t)nu * sizeof(double), h.C, (size_t)h.ldc * sizeof(double),
+                                 (size_t)nu * sizeof(double), nu,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream_));
+    HSSMF_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  void Engine::import_update(int f, const double* src, bool on_device) {
+    auto& D = *d_;
+    const int nu = D.t.nodes[f].nu();
+    if (!nu) return;
+    auto& m = D.imported[f];
+    if (m.bytes < (size_t)nu * nu * sizeof(double)) m.alloc((size_t)nu * nu * sizeof(double));
+    HSSMF_CUDA(cudaMemcpyAsync(m.p, src, (size_t)nu * nu * sizeof(double),
+                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
+    D.hf[f].C = m.as<double>();
+    D.hf[f].ldc = nu;
+    D.upload_front(f);  // synchronises the stream
+  }
+
+  void Engine::export_bupd(int f, double* dst, int nrhs) const {
+    const auto& D = *d_;
+    const int nu = D.t.nodes[f].nu();
+    if (!nu || nrhs <= 0) return;
+    HSSMF_CUDA(cudaMemcpyAsync(dst, D.hf[f].bupd, (size_t)nu * nrhs * sizeof(double),
+                               cudaMemcpyDeviceToDevice, stream_));
+    HSSMF_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  void Engine::import_bupd(int f, const double* src, int nrhs) {
+    auto& D = *d_;
+    const int nu = D.t.nodes[f].nu();
+    if (!nu || nrhs <= 0) return;
+    if (nrhs > D.bupd_nr) D.set_bupd_capacity(nrhs);
+    HSSMF_CUDA(cudaMemcpyAsync(D.hf[f].bupd, src, (size_t)nu * nrhs * sizeof(double),
+                               cudaMemcpyDeviceToDevice, stream_));
+    HSSMF_CUDA(cudaStreamSynchronize(stream_));
   }
 
   void Engine::solve(double* b, int ldb, int nrhs, bool on_device) {
@@ -1190,8 +1268,6 @@ namespace hssmf_b200 {
     auto& D = *d_;
     if (!factored_) throw SolverFailure(2, -1, -1, "mf solve: not factored");
     if (nrhs <= 0) return;
-    D.profile = profile_;
-    if (nrhs > D.bupd_nr) D.set_bupd_capacity(nrhs);
     double* x = b;
     int ldx = ldb;
     if (!on_device || ldb != n_) {
@@ -1204,67 +1280,13 @@ namespace hssmf_b200 {
                                    on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                    stream_));
     }
-    int max_nu = 0;
-    for (const auto& f : D.t.nodes) max_nu = std::max(max_nu, f.nu());
-    if (D.x2buf.bytes < (size_t)max_nu * sizeof(double) + 8)
-      D.x2buf.alloc((size_t)max_nu * sizeof(double) + 8);
     cudaEvent_t e0, e1;
     HSSMF_CUDA(cudaEventCreate(&e0));
     HSSMF_CUDA(cudaEventCreate(&e1));
     HSSMF_CUDA(cudaEventRecord(e0, stream_));
-    const FrontDev* F = D.d_fronts.as<FrontDev>();
     const int nlev = (int)D.levels.size();
-    const int nr = D.bupd_nr;
-    // forward sweep, deepest level first (mf_forward, multifrontal.hpp:507-567)
-    for (int L = nlev - 1; L >= 0; L--) {
-      auto& P = D.levels[L];
-      const int* ids = D.d_ids.as<int>() + P.ids_off;
-      const int* sids = D.d_sids.as<int>() + P.sids_off;
-      if (P.b_count)
-        HSSMF_CUDA(cudaMemsetAsync(D.bupd.as<double>() + P.b_off * nr, 0,
-                                   P.b_count * nr * sizeof(double), stream_));
-      D.launch(K_SOLVE_FWD, 0, 0, [&] {
-        for (int slot = 0; slot < 2; slot++)
-          DenseKernels::fold_children(F, ids, P.nf, slot, x, ldx, nrhs, P.max_child_nu[slot],
-                                      stream_);
-        if (P.nsf) {
-          DenseKernels::fwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
-          DenseKernels::fwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_nu, stream_);
-        }
-        for (int i : P.hss) {
-          if (!D.hss[i]) continue;
-          const auto& h = D.hf[i];
-          for (int r = 0; r < nrhs; r++) {
-            double* xr = x + (size_t)r * ldx + h.sep_begin;
-            if (h.nu) D.hss[i]->partial_forward(xr, h.bupd + (size_t)r * h.nu);
-            else D.hss[i]->solve_full(xr);
-          }
-        }
-      });
-    }
-    // backward sweep, root first (mf_backward, multifrontal.hpp:569-607)
-    for (int L = 0; L < nlev; L++) {
-      auto& P = D.levels[L];
-      const int* sids = D.d_sids.as<int>() + P.sids_off;
-      D.launch(K_SOLVE_BWD, 0, 0, [&] {
-        if (P.nsf) {
-          DenseKernels::bwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
-          DenseKernels::bwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
-        }
-        for (int i : P.hss) {
-          if (!D.hss[i]) continue;
-          const auto& h = D.hf[i];
-          if (!h.nu) continue;
-          for (int r = 0; r < nrhs; r++) {
-            double* xr = x + (size_t)r * ldx;
-            CopyDesc g{xr, 1, 0, h.upd, nullptr, 0, 0, D.x2buf.as<double>(), h.nu, nullptr,
-                       nullptr, 0, 0, h.nu, 1, 1.0, 0, 0};
-            index_copy_run({g}, stream_);
-            D.hss[i]->partial_backward(xr + h.sep_begin, D.x2buf.as<double>());
-          }
-        }
-      });
-    }
+    solve_levels(x, ldx, nrhs, 0, nlev - 1, true);
+    solve_levels(x, ldx, nrhs, 0, nlev - 1, false);
     HSSMF_CUDA(cudaEventRecord(e1, stream_));
     if (x != b)
       HSSMF_CUDA(cudaMemcpy2DAsync(b, (size_t)ldb * sizeof(double), x, n_ * sizeof(double),
@@ -1278,6 +1300,77 @@ namespace hssmf_b200 {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (profile_) D.collect();
+  }
+
+  void Engine::solve_levels(double* x, int ldx, int nrhs, int lo, int hi, bool forward) {
+    HSSMF_CUDA(cudaSetDevice(device_));
+    auto& D = *d_;
+    if (nrhs <= 0) return;
+    D.profile = profile_;
+    if (nrhs > D.bupd_nr) D.set_bupd_capacity(nrhs);
+    int max_nu = 0;
+    for (const auto& f : D.t.nodes) max_nu = std::max(max_nu, f.nu());
+    if (D.x2buf.bytes < (size_t)max_nu * sizeof(double) + 8)
+      D.x2buf.alloc((size_t)max_nu * sizeof(double) + 8);
+    const FrontDev* F = D.d_fronts.as<FrontDev>();
+    const int nlev = (int)D.levels.size();
+    lo = std::max(lo, 0);
+    hi = std::min(hi, nlev - 1);
+    const int nr = D.bupd_nr;
+    if (forward) {
+      // forward sweep, deepest level first (mf_forward, multifrontal.hpp:507-567)
+      for (int L = hi; L >= lo; L--) {
+        auto& P = D.levels[L];
+        const int* ids = D.d_ids.as<int>() + P.ids_off;
+        const int* sids = D.d_sids.as<int>() + P.sids_off;
+        if (P.b_count)
+          HSSMF_CUDA(cudaMemsetAsync(D.bupd.as<double>() + P.b_off * nr, 0,
+                                     P.b_count * nr * sizeof(double), stream_));
+        D.launch(K_SOLVE_FWD, 0, 0, [&] {
+          for (int slot = 0; slot < 2; slot++)
+            DenseKernels::fold_children(F, ids, P.nf, slot, x, ldx, nrhs, P.max_child_nu[slot],
+                                        stream_);
+          if (P.nsf) {
+            DenseKernels::fwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
+            DenseKernels::fwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_nu, stream_);
+          }
+          for (int i : P.hss) {
+            if (!D.hss[i]) continue;
+            const auto& h = D.hf[i];
+            for (int r = 0; r < nrhs; r++) {
+              double* xr = x + (size_t)r * ldx + h.sep_begin;
+              if (h.nu) D.hss[i]->partial_forward(xr, h.bupd + (size_t)r * h.nu);
+              else D.hss[i]->solve_full(xr);
+            }
+          }
+        });
+      }
+    } else {
+      // backward sweep, root first (mf_backward, multifrontal.hpp:569-607)
+      for (int L = lo; L <= hi; L++) {
+        auto& P = D.levels[L];
+        const int* sids = D.d_sids.as<int>() + P.sids_off;
+        D.launch(K_SOLVE_BWD, 0, 0, [&] {
+          if (P.nsf) {
+            DenseKernels::bwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
+            DenseKernels::bwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
+          }
+          for (int i : P.hss) {
+            if (!D.hss[i]) continue;
+            const auto& h = D.hf[i];
+            if (!h.nu) continue;
+            for (int r = 0; r < nrhs; r++) {
+              double* xr = x + (size_t)r * ldx;
+              CopyDesc g{xr, 1, 0, h.upd, nullptr, 0, 0, D.x2buf.as<double>(), h.nu, nullptr,
+                         nullptr, 0, 0, h.nu, 1, 1.0, 0, 0};
+              index_copy_run({g}, stream_);
+              D.hss[i]->partial_backward(xr + h.sep_begin, D.x2buf.as<double>());
+            }
+          }
+        });
+      }
+    }
+    HSSMF_CUDA(cudaStreamSynchronize(stream_));
   }
 
   long long Engine::factor_nnz() const {

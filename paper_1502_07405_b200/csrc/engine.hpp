@@ -53,10 +53,26 @@ namespace hssmf_b200 {
     Engine(int device);
     ~Engine();
 
-    // upload structure + values, build the static schedule
-    void analyze(const Csr& a, const Etree& t, const Options& o);
+    // upload structure + values, build the static schedule. owned (optional,
+    // one flag per front): only these fronts are factored and solved here;
+    // the updates / bupd of their non-owned children are imported (multi-GPU
+    // subtree partition)
+    void analyze(const Csr& a, const Etree& t, const Options& o, const char* owned = nullptr);
     // numeric factorization from the resident values
-    void factor();
+    void factor() { factor_levels(0, nlevels() - 1); }
+    // the fronts of tree levels lo..hi (deepest first); a multi-GPU run calls
+    // it phase by phase with update imports in between
+    void factor_levels(int lo, int hi);
+    int nlevels() const;
+    // update block (nu x nu, ld nu) of front f: out to dst / in from src
+    void export_update(int f, double* dst, bool on_device) const;
+    void import_update(int f, const double* src, bool on_device);
+    // forward-sweep contribution bupd (nu x nrhs, ld nu) of front f, device memory
+    void export_bupd(int f, double* dst, int nrhs) const;
+    void import_bupd(int f, const double* src, int nrhs);
+    // one sweep over levels lo..hi on a device x (n x nrhs, ld ldx): forward
+    // deepest first, backward root first
+    void solve_levels(double* x, int ldx, int nrhs, int lo, int hi, bool forward);
     // replace the matrix values (same pattern) from host or device memory
     void set_values(const double* val, bool on_device);
     // solve in place: b is n x nrhs column-major (ld = ldb), host or device

@@ -87,3 +87,231 @@ def exchange_updates(part: Partition, rank: int, payload_of, send, recv):
         elif dst == rank:
             got[c] = recv((nu, nu), src)
     return got
+
+
+# ---- phased factorization / solve over a subtree partition ------------------
+#
+# Every rank runs the same sequence of phases; a phase touches only the fronts
+# the rank owns. Exchanges happen between phases, edge by edge in one global
+# order (deepest parent level first, then by child id), so every send meets
+# its receive without a global barrier:
+#
+#   factor:  levels >= L (own subtree)  | for l = L-1..0: updates of the
+#            children of level-l fronts cross over, then level l
+#   solve:   forward levels >= L | for l = L-1..0: bupd of level-(l+1)
+#            children cross over, forward level l | for l = 0..L-1: backward
+#            level l, then x(upd) of the level-(l+1) children crosses back |
+#            backward levels >= L
+#
+# `engine` objects expose factor_levels / export_update / import_update /
+# export_bupd / import_bupd / solve_levels (PartFactors on a GPU; a recording
+# fake in the CPU tests). `transport` moves arrays between ranks: send(obj,
+# dst), recv(shape, src) -> obj (torch.distributed over NCCL on GPUs, a
+# mailbox for several ranks in one process, gloo on CPU).
+
+
+def _edges_into(part: Partition, t_level, l):
+    return sorted([e for e in part.edges if t_level[e[1]] == l], key=lambda e: e[0])
+
+
+def phased_factor(part: Partition, t_level, nlev, engines: dict, transport):
+    """engines: {rank: engine} for the ranks living in this process"""
+    L = part.level
+    for e in engines.values():
+        e.factor_levels(L, nlev - 1)
+    for l in range(L - 1, -1, -1):
+        for (c, p, src, dst, nu) in _edges_into(part, t_level, l):
+            if src in engines:
+                transport.send(engines[src].export_update(c), dst, src)
+            if dst in engines:
+                engines[dst].import_update(c, transport.recv((nu, nu), src, dst))
+        for e in engines.values():
+            e.factor_levels(l, l)
+
+
+def phased_solve(part: Partition, t_level, nlev, upd_of, engines: dict, xs: dict, nrhs,
+                 transport):
+    """xs: {rank: device x (n x nrhs)} solved in place on every rank; each
+    rank ends up with x correct on the separators of the fronts it owns"""
+    L = part.level
+    for r, e in engines.items():
+        e.solve_levels(xs[r], L, nlev - 1, True)
+    for l in range(L - 1, -1, -1):
+        for (c, p, src, dst, nu) in _edges_into(part, t_level, l):
+            if src in engines:
+                transport.send(engines[src].export_bupd(c, nrhs), dst, src)
+            if dst in engines:
+                engines[dst].import_bupd(c, transport.recv((nu, nrhs), src, dst), nrhs)
+        for r, e in engines.items():
+            e.solve_levels(xs[r], l, l, True)
+    for l in range(0, L):
+        for r, e in engines.items():
+            e.solve_levels(xs[r], l, l, False)
+        # x at the update indices of the level-(l+1) children goes back down
+        # (owner of the parent -> owner of the child)
+        for (c, p, src, dst, nu) in _edges_into(part, t_level, l):
+            if dst in engines:
+                transport.send(engines[dst].gather_x(xs[dst], upd_of(c)), src, dst)
+            if src in engines:
+                engines[src].scatter_x(xs[src], upd_of(c), transport.recv((nu, nrhs), dst, src))
+    for r, e in engines.items():
+        e.solve_levels(xs[r], L, nlev - 1, False)
+
+
+def separator_mask(t, owner, rank):
+    """rows of x computed by `rank` (the separators of its fronts)"""
+    m = np.zeros(int(t.sep_end.max(initial=0)), bool)
+    for i in np.nonzero(np.asarray(owner) == rank)[0]:
+        m[t.sep_begin[i]:t.sep_end[i]] = True
+    return m
+
+
+class Mailbox:
+    """transport for several ranks in one process (one GPU): messages are
+    copied into a queue keyed by (src, dst)"""
+
+    def __init__(self):
+        self.q = {}
+
+    def send(self, obj, dst, src):
+        self.q.setdefault((src, dst), []).append(obj.clone() if hasattr(obj, "clone") else obj.copy())
+
+    def recv(self, shape, src, dst):
+        return self.q[(src, dst)].pop(0)
+
+
+class TorchTransport:
+    """torch.distributed point-to-point (NCCL over NVLink on GPUs, gloo on
+    CPU); tensors are device (NCCL) or host (gloo) float64"""
+
+    def __init__(self, device=None):
+        import torch
+        self.torch = torch
+        self.device = device
+
+    def send(self, obj, dst, src):
+        self.torch.distributed.send(obj.contiguous(), dst)
+
+    def recv(self, shape, src, dst):
+        buf = self.torch.empty(shape[::-1] if len(shape) == 2 else shape, dtype=self.torch.float64,
+                               device=self.device)
+        self.torch.distributed.recv(buf, src)
+        return buf
+
+
+class PartFactors:
+    """One rank's share of a subtree-partitioned factorization on a GPU
+    (C-ABI hssmf_analyze_owned & co). Arrays crossing ranks are torch
+    tensors on this rank's device; a (nu x k) column-major block is a torch
+    (k, nu) row-major tensor."""
+
+    def __init__(self, a, t, opts, part: Partition, rank: int, device: int = 0):
+        import ctypes as C
+        import torch
+        from . import _native as N
+        from .api import MfFactors, _call
+        self.C, self.N, self.torch, self._call = C, N, torch, _call
+        self.part, self.rank, self.device = part, rank, device
+        self.dev = torch.device("cuda", device)
+        owned = np.ascontiguousarray(np.asarray(part.owner) == rank, np.int8)
+        h = C.c_void_p()
+        o = opts.native()
+        _call("hssmf_analyze_owned", int(device), a._h, t._h, C.byref(o),
+              owned.ctypes.data_as(C.c_void_p), C.byref(h))
+        self.m = MfFactors(h, a.size())
+        self.m.factored = False
+        self.nlev = N.lib().hssmf_nlevels(h)
+        self.nu = np.diff(np.asarray(t.upd_ptr))
+        self.n = a.size()
+
+    @property
+    def h(self):
+        return self.m._h
+
+    def factor_levels(self, lo, hi):
+        self._call("hssmf_factor_levels", self.h, int(lo), int(hi))
+        if lo == 0:
+            self.m.refresh()
+            self.m.factored = True
+
+    def export_update(self, f):
+        nu = int(self.nu[f])
+        buf = self.torch.empty((nu, nu), dtype=self.torch.float64, device=self.dev)
+        self._call("hssmf_update_export", self.h, int(f), self.C.c_void_p(buf.data_ptr()), 1)
+        return buf
+
+    def import_update(self, f, buf):
+        self._call("hssmf_update_import", self.h, int(f), self.C.c_void_p(buf.data_ptr()), 1)
+
+    def export_bupd(self, f, nrhs):
+        nu = int(self.nu[f])
+        buf = self.torch.empty((nrhs, nu), dtype=self.torch.float64, device=self.dev)
+        self._call("hssmf_bupd_export", self.h, int(f), self.C.c_void_p(buf.data_ptr()), int(nrhs))
+        return buf
+
+    def import_bupd(self, f, buf, nrhs):
+        self._call("hssmf_bupd_import", self.h, int(f), self.C.c_void_p(buf.data_ptr()), int(nrhs))
+
+    def solve_levels(self, x, lo, hi, forward):
+        nrhs = x.shape[0]
+        self._call("hssmf_solve_levels", self.h, self.C.c_void_p(x.data_ptr()), self.n, int(nrhs),
+                   int(lo), int(hi), 1 if forward else 0)
+
+    def gather_x(self, x, rows):
+        return x[:, rows].contiguous()
+
+    def scatter_x(self, x, rows, vals):
+        x[:, rows] = vals
+
+
+class DistributedMf:
+    """Subtree-partitioned factorization + solve over nranks GPUs (SURVEY
+    §8e). rank=None keeps every rank in this process on `device` (several
+    engines on one GPU, messages through a Mailbox: the single-GPU check of
+    the partitioned path); otherwise this process is `rank` and `transport`
+    (TorchTransport over NCCL) reaches the others."""
+
+    def __init__(self, a, t, opts, nranks, rank=None, transport=None, device=0):
+        import torch
+        self.torch = torch
+        self.t = t
+        self.part = subtree_partition(t, nranks)
+        self.ranks = list(range(nranks)) if rank is None else [rank]
+        self.transport = transport or Mailbox()
+        self.dev = torch.device("cuda", device)
+        self.engines = {r: PartFactors(a, t, opts, self.part, r, device) for r in self.ranks}
+        self.nlev = next(iter(self.engines.values())).nlev
+        self.masks = {r: torch.from_numpy(separator_mask(t, self.part.owner, r)).to(self.dev)
+                      for r in self.ranks}
+        self._upd = {}
+
+    def upd_of(self, c):
+        if c not in self._upd:
+            self._upd[c] = self.torch.from_numpy(self.t.upd(c).astype(np.int64)).to(self.dev)
+        return self._upd[c]
+
+    def factor(self):
+        phased_factor(self.part, self.t.level, self.nlev, self.engines, self.transport)
+
+    def solve_device(self, xs: dict):
+        """xs: {rank: (nrhs, n) float64 device tensor}, solved in place; each
+        rank's x is correct on its own separators"""
+        nrhs = next(iter(xs.values())).shape[0]
+        phased_solve(self.part, self.t.level, self.nlev, self.upd_of, self.engines, xs, nrhs,
+                     self.transport)
+
+    def combine(self, xs: dict):
+        """the solution rows of this process's ranks (other rows 0)"""
+        out = None
+        for r in self.ranks:
+            v = self.torch.where(self.masks[r], xs[r], self.torch.zeros_like(xs[r]))
+            out = v if out is None else out + v
+        return out
+
+    def solve(self, b):
+        bb = np.asarray(b, np.float64)
+        b2 = bb.reshape(-1, 1) if bb.ndim == 1 else bb
+        xs = {r: self.torch.from_numpy(np.ascontiguousarray(b2.T)).to(self.dev) for r in self.ranks}
+        self.solve_device(xs)
+        x = self.combine(xs).cpu().numpy().T
+        return x.reshape(bb.shape)

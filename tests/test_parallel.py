@@ -100,3 +100,114 @@ def test_update_exchange_gloo_world2():
     assert all(ok for _, ok, _ in res)
     # rank 0 owns the root (child0 subtree) and receives rank 1's subtree-root update
     assert res[0][2] and not res[1][2]
+
+
+# ---- the phased factor / solve protocol, with a recording stand-in engine ----
+class FakeEngine:
+    """Stand-in for PartFactors: 'factoring' front f gives val[f] = f + sum of
+    the children's vals (a child's val must be local or imported), the forward
+    sweep fwd[f] = val[f] + sum of the children's fwd, the backward sweep
+    x[f] = fwd[f] + x[parent]. Checks that every phase finds its inputs."""
+
+    def __init__(self, t, part, rank):
+        self.t, self.part, self.rank = t, part, rank
+        self.own = np.asarray(part.owner) == rank
+        self.val, self.fwd = {}, {}
+
+    def _kids(self, f):
+        return [c for c in (self.t.child0[f], self.t.child1[f]) if c >= 0]
+
+    def _at(self, lo, hi):
+        return [f for f in range(len(self.own)) if self.own[f] and lo <= self.t.level[f] <= hi]
+
+    def factor_levels(self, lo, hi):
+        for f in sorted(self._at(lo, hi), key=lambda f: -self.t.level[f]):
+            self.val[f] = float(f) + sum(self.val[c] for c in self._kids(f))
+
+    def _nu(self, f):
+        return int(self.t.upd_ptr[f + 1] - self.t.upd_ptr[f])
+
+    def export_update(self, f):  # nu x nu, like the real update block
+        nu = self._nu(f)
+        return torch.full((nu, nu), self.val[f], dtype=torch.float64)
+
+    def import_update(self, f, buf):
+        self.val[f] = float(buf[0, 0])
+
+    def export_bupd(self, f, nrhs):
+        return torch.full((nrhs, self._nu(f)), self.fwd[f], dtype=torch.float64)
+
+    def import_bupd(self, f, buf, nrhs):
+        self.fwd[f] = float(buf[0, 0])
+
+    def solve_levels(self, x, lo, hi, forward):
+        fs = self._at(lo, hi)
+        if forward:
+            for f in sorted(fs, key=lambda f: -self.t.level[f]):
+                self.fwd[f] = self.val[f] + sum(self.fwd[c] for c in self._kids(f))
+        else:
+            for f in sorted(fs, key=lambda f: self.t.level[f]):
+                p = self.t.parent[f]
+                x[0, f] = self.fwd[f] + (float(x[0, p]) if p >= 0 else 0.0)
+
+    def gather_x(self, x, rows):
+        return x[:, rows].clone()
+
+    def scatter_x(self, x, rows, vals):
+        x[:, rows] = vals
+
+
+def _expected(t):
+    nn = len(t.child0)
+    val, fwd, x = np.zeros(nn), np.zeros(nn), np.zeros(nn)
+    for f in range(nn):  # postorder
+        kids = [c for c in (t.child0[f], t.child1[f]) if c >= 0]
+        val[f] = f + sum(val[c] for c in kids)
+        fwd[f] = val[f] + sum(fwd[c] for c in kids)
+    for f in range(nn - 1, -1, -1):
+        p = t.parent[f]
+        x[f] = fwd[f] + (x[p] if p >= 0 else 0.0)
+    return val, x
+
+
+def _phased_worker(rank, world, port, q):
+    from paper_1502_07405_b200.parallel import TorchTransport, phased_factor, phased_solve
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    op = P.ordered_grid("p3d", 24, 32)
+    t = op.t
+    part = subtree_partition(t, world)
+    eng = FakeEngine(t, part, rank)
+    nlev = int(t.level.max()) + 1
+    tr = TorchTransport(None)
+    phased_factor(part, t.level, nlev, {rank: eng}, tr)
+    x = torch.zeros((1, len(t.child0)), dtype=torch.float64)
+    # upd_of(c) -> nu_c copies of the parent's slot in this stand-in x
+    def upd_of(c):
+        return torch.full((int(t.upd_ptr[c + 1] - t.upd_ptr[c]),), int(t.parent[c]),
+                          dtype=torch.long)
+    phased_solve(part, t.level, nlev, upd_of, {rank: eng}, {rank: x}, 1, tr)
+    val, xe = _expected(t)
+    own = np.nonzero(eng.own)[0]
+    ok_val = all(abs(eng.val[f] - val[f]) < 1e-9 for f in own)
+    ok_x = all(abs(float(x[0, f]) - xe[f]) < 1e-9 for f in own)
+    q.put((rank, ok_val, ok_x))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_phased_protocol_gloo(world):
+    # every rank's phases find their children's updates / bupd and their
+    # parents' x where the sequential schedule would have them
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_phased_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=180) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(ok_v and ok_x for _, ok_v, ok_x in res), res
