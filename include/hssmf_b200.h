@@ -33,7 +33,8 @@ typedef enum {
   HSSMF_ERR_CUDA = 4,
   HSSMF_ERR_NCCL = 5,
   HSSMF_ERR_RANK = 6,
-  HSSMF_ERR_OTHER = 7
+  HSSMF_ERR_OTHER = 7,
+  HSSMF_ERR_DIVERGENCE = 8  /* KrylovDivergenceError (krylov.hpp) */
 } hssmf_code;
 
 typedef struct {
@@ -144,6 +145,26 @@ int hssmf_bupd_import(hssmf_factors* f, int front, const double* src, int nrhs,
  * forward = 1 (deepest first) or backward = 0 (root first) */
 int hssmf_solve_levels(hssmf_factors* f, double* x, int ldx, int nrhs, int lo, int hi,
                        int forward, hssmf_status* st);
+
+/* ---- preconditioned iterative solves (krylov.hpp:93-232) ----
+ * gmres(A, M^-1 = mf_solve(m), b, restart, rtol, atol, maxit) and
+ * iterative_refinement(A, M^-1, b, rtol, atol, maxit), run on the device:
+ * A is applied by a CSR SpMV kernel, M^-1 by the factors' solve, the Krylov
+ * basis lives in HBM. m = NULL: identity preconditioner (device 0).
+ * b, x: host vectors of length n (x = the solution, zero initial guess);
+ * history (optional, history_cap entries) receives the residual norms. */
+typedef struct {
+  int iterations;
+  double rel_resid, abs_resid;
+  int converged, stagnated;
+  int history_len;
+} hssmf_krylov_report;
+int hssmf_gmres(const hssmf_csr* a, hssmf_factors* m, const double* b, double* x, int restart,
+                double rtol, double atol, int maxit, hssmf_krylov_report* rep, double* history,
+                int history_cap, hssmf_status* st);
+int hssmf_refine(const hssmf_csr* a, hssmf_factors* m, const double* b, double* x, double rtol,
+                 double atol, int maxit, hssmf_krylov_report* rep, double* history,
+                 int history_cap, hssmf_status* st);
 
 /* MfFactors::{front_stats, hss_fronts, fallbacks, max_front_rank, factor_nnz()}
  * (multifrontal.hpp:454-468); type 0 dense 1 hss 2 hss_dense */

@@ -19,6 +19,7 @@
 #ifndef HSSMF_B200_HSSMF_HPP
 #define HSSMF_B200_HSSMF_HPP
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -33,6 +34,7 @@ namespace hssmf_b200 {
   using SolverError = ::hssmf::SolverError;
   using IoError = ::hssmf::IoError;
   using SingularMatrixError = ::hssmf::SingularMatrixError;
+  using KrylovDivergenceError = ::hssmf::KrylovDivergenceError;
 #else
   struct SolverError : std::runtime_error {
     explicit SolverError(const std::string& m) : std::runtime_error(m) {}
@@ -48,6 +50,9 @@ namespace hssmf_b200 {
    private:
     int column_;
   };
+  struct KrylovDivergenceError : SolverError {
+    explicit KrylovDivergenceError(const std::string& m) : SolverError(m) {}
+  };
 #endif
 
   namespace detail {
@@ -60,6 +65,7 @@ namespace hssmf_b200 {
 #else
         case HSSMF_ERR_SINGULAR: throw SingularMatrixError(m, st.column);
 #endif
+        case HSSMF_ERR_DIVERGENCE: throw KrylovDivergenceError(m);
         default: throw SolverError(m);
       }
     }
@@ -192,6 +198,82 @@ namespace hssmf_b200 {
     Dense x(b);
     mf_solve(m, x);
     return x;
+  }
+
+  // SolveReport (reference krylov.hpp:22-29)
+  struct SolveReport {
+    int iterations = 0;
+    double rel_resid = 0, abs_resid = 0;
+    bool converged = false, stagnated = false;
+    std::vector<double> history;
+  };
+
+  namespace detail {
+    template<class Sparse>
+    hssmf_csr* upload_csr(const Sparse& a) {
+      hssmf_status st{};
+      hssmf_csr* c = nullptr;
+      check(hssmf_csr_create(a.size(), a.ptr().data(), a.ind().data(), a.val().data(), &c, &st), st);
+      return c;
+    }
+    template<class Call>
+    std::pair<std::vector<double>, SolveReport> krylov(int n, int maxit, Call&& call) {
+      std::vector<double> x(n), hist(maxit + 2);
+      hssmf_krylov_report r{};
+      hssmf_status st{};
+      const int rc = call(x.data(), &r, hist.data(), static_cast<int>(hist.size()), &st);
+      check(rc, st);
+      SolveReport rep;
+      rep.iterations = r.iterations;
+      rep.rel_resid = r.rel_resid;
+      rep.abs_resid = r.abs_resid;
+      rep.converged = r.converged != 0;
+      rep.stagnated = r.stagnated != 0;
+      rep.history.assign(hist.begin(), hist.begin() + std::min<int>(r.history_len, hist.size()));
+      return {std::move(x), std::move(rep)};
+    }
+  }  // namespace detail
+
+  // gmres(A, M^-1 = mf_solve(m), b, restart, rtol, atol, maxit) (reference
+  // krylov.hpp:93-184 with apply_a = a.matvec and apply_m_inv = the mf_op
+  // closure of test_krylov.cpp:26-32), run on the device
+  template<class Sparse>
+  std::pair<std::vector<double>, SolveReport> gmres(const Sparse& a, MfFactors& m,
+                                                    const std::vector<double>& b,
+                                                    int restart = 30, double rtol = 1e-6,
+                                                    double atol = 1e-10, int maxit = 500) {
+    if (restart < 1) throw IoError("gmres: restart must be >= 1");
+    hssmf_csr* c = detail::upload_csr(a);
+    try {
+      auto out = detail::krylov(a.size(), maxit, [&](double* x, hssmf_krylov_report* r, double* h,
+                                                     int cap, hssmf_status* st) {
+        return hssmf_gmres(c, m.handle(), b.data(), x, restart, rtol, atol, maxit, r, h, cap, st);
+      });
+      hssmf_csr_free(c);
+      return out;
+    } catch (...) {
+      hssmf_csr_free(c);
+      throw;
+    }
+  }
+
+  // iterative_refinement (reference krylov.hpp:189-229)
+  template<class Sparse>
+  std::pair<std::vector<double>, SolveReport> iterative_refinement(
+      const Sparse& a, MfFactors& m, const std::vector<double>& b, double rtol = 1e-6,
+      double atol = 1e-10, int maxit = 500) {
+    hssmf_csr* c = detail::upload_csr(a);
+    try {
+      auto out = detail::krylov(a.size(), maxit, [&](double* x, hssmf_krylov_report* r, double* h,
+                                                     int cap, hssmf_status* st) {
+        return hssmf_refine(c, m.handle(), b.data(), x, rtol, atol, maxit, r, h, cap, st);
+      });
+      hssmf_csr_free(c);
+      return out;
+    } catch (...) {
+      hssmf_csr_free(c);
+      throw;
+    }
   }
 
 }  // namespace hssmf_b200

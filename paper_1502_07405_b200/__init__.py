@@ -5,8 +5,9 @@ See DESIGN.md. Numerics run only in the sm_100a kernels of libhssmf_b200.so.
 """
 from .api import (  # noqa: F401
     EliminationTree, FrontStat, GridGeometry, GridProblem, HssFactors, HssOptions,
-    HssRankExceeded, IoError, MfFactors, SingularMatrixError, SolverError, SolverOptions,
-    SparseMatrix, front_cluster_tree, generate_convdiff3d, generate_grid_problem,
-    hss_compress, mf_factor, mf_solve, mf_solve_new, nested_dissection_geometric,
-    ordered_grid, ordered_problem, symbolic_factorization,
+    HssRankExceeded, IoError, KrylovDivergenceError, MfFactors, SingularMatrixError,
+    SolveReport, SolverError, SolverOptions, SparseMatrix, front_cluster_tree,
+    generate_convdiff3d, generate_grid_problem, gmres, hss_compress, iterative_refinement,
+    mf_factor, mf_solve, mf_solve_new, nested_dissection_geometric, ordered_grid,
+    ordered_problem, symbolic_factorization,
 )

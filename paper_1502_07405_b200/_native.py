@@ -58,6 +58,10 @@ _SIGS = {
     "hssmf_factor": (C.c_int, [C.c_int, vp, vp, C.POINTER(Options), C.POINTER(vp),
                                C.POINTER(Status)]),
     "hssmf_refactor": (C.c_int, [vp, vp, C.c_int, C.POINTER(Status)]),
+    "hssmf_gmres": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_double, C.c_double, C.c_int, vp, vp,
+                              C.c_int, C.POINTER(Status)]),
+    "hssmf_refine": (C.c_int, [vp, vp, vp, vp, C.c_double, C.c_double, C.c_int, vp, vp, C.c_int,
+                               C.POINTER(Status)]),
     "hssmf_analyze_owned": (C.c_int, [C.c_int, vp, vp, vp, vp, C.POINTER(vp), C.POINTER(Status)]),
     "hssmf_nlevels": (C.c_int, [vp]),
     "hssmf_factor_levels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(Status)]),

@@ -42,6 +42,10 @@ class HssRankExceeded(SolverError):
     pass
 
 
+class KrylovDivergenceError(SolverError):
+    pass
+
+
 class CudaError(SolverError):
     pass
 
@@ -60,6 +64,8 @@ def _check(rc, st: N.Status):
         raise CudaError(msg)
     if rc == 6:
         raise HssRankExceeded(msg)
+    if rc == 8:
+        raise KrylovDivergenceError(msg)
     raise SolverError(msg)
 
 
@@ -433,6 +439,52 @@ def mf_solve_new(m: MfFactors, b: np.ndarray) -> np.ndarray:
     x = np.array(b, dtype=np.float64, order="F", copy=True)
     mf_solve(m, x)
     return x
+
+
+# ---- preconditioned iterative solves (krylov.hpp:18-232) ---------------------
+@dataclass
+class SolveReport:
+    """krylov.hpp:22-29: residuals are the left-preconditioned ones"""
+    iterations: int = 0
+    rel_resid: float = 0.0
+    abs_resid: float = 0.0
+    converged: bool = False
+    stagnated: bool = False
+    history: list = field(default_factory=list)
+
+
+class _KrylovReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("rel_resid", C.c_double), ("abs_resid", C.c_double),
+                ("converged", C.c_int), ("stagnated", C.c_int), ("history_len", C.c_int)]
+
+
+def _krylov(fn, a, m, b, extra, maxit):
+    bb = np.ascontiguousarray(b, np.float64).reshape(-1)
+    if bb.shape[0] != a.size():
+        raise IoError("krylov: rhs size mismatch")
+    x = np.zeros_like(bb)
+    rep = _KrylovReport()
+    hist = np.zeros(maxit + 2, np.float64)
+    _call(fn, a._h, m._h if m is not None else None, bb.ctypes.data_as(C.c_void_p),
+          x.ctypes.data_as(C.c_void_p), *extra, C.byref(rep), hist.ctypes.data_as(C.c_void_p),
+          len(hist))
+    r = SolveReport(rep.iterations, rep.rel_resid, rep.abs_resid, bool(rep.converged),
+                    bool(rep.stagnated), hist[:rep.history_len].tolist())
+    return x, r
+
+
+def gmres(a: SparseMatrix, m, b, restart=30, rtol=1e-6, atol=1e-10, maxit=500):
+    """krylov.hpp:93-184 with A = a (CSR SpMV on the device) and M^-1 =
+    mf_solve(m) (m None: identity); returns (x, SolveReport)"""
+    if restart < 1:
+        raise IoError("gmres: restart must be >= 1")
+    return _krylov("hssmf_gmres", a, m, b, (int(restart), float(rtol), float(atol), int(maxit)),
+                   maxit)
+
+
+def iterative_refinement(a: SparseMatrix, m, b, rtol=1e-6, atol=1e-10, maxit=500):
+    """krylov.hpp:189-229"""
+    return _krylov("hssmf_refine", a, m, b, (float(rtol), float(atol), int(maxit)), maxit)
 
 
 # ---- standalone dense HSS (hss_compress.hpp:373-383, hss_ulv.hpp) ----------

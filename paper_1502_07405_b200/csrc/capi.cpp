@@ -15,6 +15,7 @@
 #include "hss_dense.hpp"
 #include "host/analysis.hpp"
 #include "kernels_test.hpp"
+#include "krylov.hpp"
 #include "staging.cuh"
 
 using namespace hssmf_b200;
@@ -71,6 +72,8 @@ namespace {
       return fail(st, HSSMF_ERR_SINGULAR, e.what(), -1, e.column);
     } catch (const HssRankError& e) {
       return fail(st, HSSMF_ERR_RANK, e.what(), e.node, -1);
+    } catch (const KrylovDivergence& e) {
+      return fail(st, HSSMF_ERR_DIVERGENCE, e.what());
     } catch (const CudaError& e) {
       return fail(st, HSSMF_ERR_CUDA, e.what());
     } catch (const std::exception& e) {
@@ -90,6 +93,44 @@ namespace {
     r.max_rank = o->max_rank;
     r.mode = o->mode;
     return r;
+  }
+}  // namespace
+
+namespace {
+  template<typename Run>
+  int krylov_call(const hssmf_csr* a, hssmf_factors* m, const double* b, double* x,
+                  hssmf_krylov_report* rep, double* history, int history_cap, hssmf_status* st,
+                  Run&& run) {
+    return guard(st, [&] {
+      const Csr& A = a->a;
+      if (m && (!m->e || !m->e->factored()))
+        throw SolverFailure(2, -1, -1, "krylov: factors not factored");
+      if (m && m->e->n() != A.n) throw SolverFailure(1, -1, -1, "krylov: size mismatch");
+      if (m) HSSMF_CUDA(cudaSetDevice(m->e->device()));
+      const int n = A.n;
+      struct Buf {
+        void* p = nullptr;
+        explicit Buf(size_t b) { HSSMF_CUDA(cudaMalloc(&p, b ? b : 8)); }
+        ~Buf() { cudaFree(p); }
+      } dptr((n + 1) * 4), dind(A.ind.size() * 4), dval(A.val.size() * 8), db(n * 8), dx(n * 8);
+      HSSMF_CUDA(cudaMemcpy(dptr.p, A.ptr.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+      HSSMF_CUDA(cudaMemcpy(dind.p, A.ind.data(), A.ind.size() * 4, cudaMemcpyHostToDevice));
+      HSSMF_CUDA(cudaMemcpy(dval.p, A.val.data(), A.val.size() * 8, cudaMemcpyHostToDevice));
+      HSSMF_CUDA(cudaMemcpy(db.p, b, (size_t)n * 8, cudaMemcpyHostToDevice));
+      CsrDevView v{n, (const int*)dptr.p, (const int*)dind.p, (const double*)dval.p};
+      KrylovReport r = run(v, m ? m->e.get() : nullptr, (const double*)db.p, (double*)dx.p);
+      HSSMF_CUDA(cudaMemcpy(x, dx.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+      if (rep) {
+        rep->iterations = r.iterations;
+        rep->rel_resid = r.rel_resid;
+        rep->abs_resid = r.abs_resid;
+        rep->converged = r.converged;
+        rep->stagnated = r.stagnated;
+        rep->history_len = (int)r.history.size();
+      }
+      if (history)
+        for (int i = 0; i < std::min(history_cap, (int)r.history.size()); i++) history[i] = r.history[i];
+    });
   }
 }  // namespace
 
@@ -307,6 +348,24 @@ int hssmf_solve_levels(hssmf_factors* f, double* x, int ldx, int nrhs, int lo, i
     if (ldx < f->e->n()) throw SolverFailure(1, -1, -1, "mf solve: rhs rows mismatch");
     f->e->solve_levels(x, ldx, nrhs, lo, hi, forward != 0);
   });
+}
+
+int hssmf_gmres(const hssmf_csr* a, hssmf_factors* m, const double* b, double* x, int restart,
+                double rtol, double atol, int maxit, hssmf_krylov_report* rep, double* history,
+                int history_cap, hssmf_status* st) {
+  return krylov_call(a, m, b, x, rep, history, history_cap, st,
+                     [&](const CsrDevView& v, Engine* e, const double* db, double* dx) {
+                       return krylov_gmres(v, e, db, dx, restart, rtol, atol, maxit, nullptr);
+                     });
+}
+
+int hssmf_refine(const hssmf_csr* a, hssmf_factors* m, const double* b, double* x, double rtol,
+                 double atol, int maxit, hssmf_krylov_report* rep, double* history,
+                 int history_cap, hssmf_status* st) {
+  return krylov_call(a, m, b, x, rep, history, history_cap, st,
+                     [&](const CsrDevView& v, Engine* e, const double* db, double* dx) {
+                       return krylov_refine(v, e, db, dx, rtol, atol, maxit, nullptr);
+                     });
 }
 
 int hssmf_refactor(hssmf_factors* f, const double* val, int on_device, hssmf_status* st) {

@@ -93,6 +93,7 @@ namespace hssmf_b200 {
     void reset_kernel_stats();
     size_t device_bytes() const;
     cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
 
     struct Impl;
 

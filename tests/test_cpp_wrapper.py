@@ -29,3 +29,4 @@ def test_wrapper_drop_in_factor_solve():
     assert out.returncode == 0, out.stdout + out.stderr
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["relres"] < 1e-12 and d["singular_col"] == 1 and d["front0"] == 1
+    assert d["gmres_converged"] == 1 and d["gmres_iterations"] <= 2
