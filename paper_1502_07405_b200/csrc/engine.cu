@@ -772,6 +772,8 @@ namespace hssmf_b200 {
         if (res[q].hss) {
           auto ps = res[q].hss->phase_stats();
           for (int p = 0; p < kHssPhases; p++) fprintf(stderr, " %.0f", ps[p].ms);
+          fprintf(stderr, " | host");
+          for (int p = 0; p < kHssPhases; p++) fprintf(stderr, " %.0f", ps[p].host_ms);
           // phase_stats drains the event list: re-add so profiling still sees it
           res[q].hss->restore_phase_stats(ps);
         }

@@ -3,6 +3,7 @@
 #include "hss.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <numeric>
 
@@ -62,6 +63,9 @@ namespace hssmf_b200 {
       void zero() {
         if (n) HSSMF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
       }
+      void zero_on(cudaStream_t st) {
+        if (n) HSSMF_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+      }
       void free() {
         if (p) {
           if (ar) ar->put(p, cls, n * sizeof(T));
@@ -72,6 +76,28 @@ namespace hssmf_b200 {
         ar = nullptr;
       }
       ~DBuf() { free(); }
+    };
+
+    // a second stream of one front (speculative sampling), ordered after the
+    // front's main stream at follow()
+    struct SideStream {
+      cudaStream_t s = nullptr;
+      cudaEvent_t done = nullptr, fork = nullptr;
+      SideStream() {
+        HSSMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        HSSMF_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        HSSMF_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      }
+      ~SideStream() {
+        cudaStreamSynchronize(s);
+        cudaEventDestroy(done);
+        cudaEventDestroy(fork);
+        cudaStreamDestroy(s);
+      }
+      void follow(cudaStream_t main) {
+        HSSMF_CUDA(cudaEventRecord(fork, main));
+        HSSMF_CUDA(cudaStreamWaitEvent(s, fork, 0));
+      }
     };
 
     // rows x cols matrix (ld = rows) whose column count grows by appending
@@ -226,20 +252,24 @@ namespace hssmf_b200 {
     // per-phase device time (CUDA events on the HSS stream), collected on demand
     struct PhEv { int ph; cudaEvent_t a, b; double flops; };
     std::vector<PhEv> phev;
-    double ph_ms[kHssPhases] = {}, ph_fl[kHssPhases] = {};
+    double ph_ms[kHssPhases] = {}, ph_fl[kHssPhases] = {}, ph_host[kHssPhases] = {};
     int ph_n[kHssPhases] = {};
     struct Ph {
       HssImpl* h;
       int id;
       cudaEvent_t a = nullptr;
       double f0;
+      std::chrono::steady_clock::time_point t0;
       Ph(HssImpl* hh, int i) : h(hh), id(i), f0(hh->flops) {
         if (!g_phase_timing) return;
+        t0 = std::chrono::steady_clock::now();
         HSSMF_CUDA(cudaEventCreate(&a));
         HSSMF_CUDA(cudaEventRecord(a, h->s));
       }
       ~Ph() {
         if (!a) return;
+        h->ph_host[id] +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         cudaEvent_t b;
         if (cudaEventCreate(&b) == cudaSuccess && cudaEventRecord(b, h->s) == cudaSuccess)
           h->phev.push_back({id, a, b, h->flops - f0});
@@ -318,25 +348,53 @@ namespace hssmf_b200 {
         nodes[root].state = DONE;
         return;
       }
+      // the next round's sampling products are computed speculatively on a
+      // side stream while this round's (latency-bound) IDs run; a round that
+      // ends the compression wastes one round of sampling. The samples are
+      // the same seeded columns and the same GEMMs, so results are unchanged.
+      SideStream side;
+      DBuf<double> scale2;
+      scale2.alloc_keep(1, s);
+      int spec_d = -1;
+      auto sample = [&](int c0, int c1, cudaStream_t st, double* sc_acc) {
+        const int dn = c1 - c0;
+        rng_fill(seeds.p, 0, m, c0, c1, R.col(c0), m, st);
+        // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
+        // hss_compress.hpp:359-363)
+        gemm_run_splitk({A, R.col(c0), Sr.col(c0), m, dn, m, (int)lda, m, m}, 'N', 'N', 1.0, 0.0, st);
+        gemm_run_splitk({A, R.col(c0), Sc.col(c0), m, dn, m, (int)lda, m, m}, 'T', 'N', 1.0, 0.0, st);
+        maxabs_run(Sr.col(c0), m, m, dn, sc_acc, st);
+        maxabs_run(Sc.col(c0), m, m, dn, sc_acc, st);
+      };
       while (true) {
         rounds++;
         const int dold = R.cols, dn = d - dold;
-        R.ensure(d);
-        Sr.ensure(d);
-        Sc.ensure(d);
         {
           Ph ph_(this, 0);
-          rng_fill(seeds.p, 0, m, dold, d, R.col(dold), m, s);
-          // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
-          // hss_compress.hpp:359-363)
-          gemm_run_splitk({A, R.col(dold), Sr.col(dold), m, dn, m, (int)lda, m, m}, 'N', 'N', 1.0,
-                          0.0, s);
-          gemm_run_splitk({A, R.col(dold), Sc.col(dold), m, dn, m, (int)lda, m, m}, 'T', 'N', 1.0,
-                          0.0, s);
+          if (spec_d == d) {
+            // this round's columns came from the side stream
+            HSSMF_CUDA(cudaStreamWaitEvent(s, side.done, 0));
+            maxabs_run(scale2.p, 1, 1, 1, scale.p, s);
+          } else {
+            R.ensure(d);
+            Sr.ensure(d);
+            Sc.ensure(d);
+            sample(dold, d, s, scale.p);
+          }
           flops += 4.0 * m * m * dn;
           R.cols = Sr.cols = Sc.cols = d;
-          maxabs_run(Sr.col(dold), m, m, dn, scale.p, s);
-          maxabs_run(Sc.col(dold), m, m, dn, scale.p, s);
+          spec_d = -1;
+          if (d - o.p < o.max_rank && !getenv("HSSMF_NO_SPEC_SAMPLING")) {
+            const int d2 = d + o.dd;
+            R.ensure(d2);
+            Sr.ensure(d2);
+            Sc.ensure(d2);
+            side.follow(s);  // buffers (re)allocated on s: the side stream starts after them
+            scale2.zero_on(side.s);
+            sample(d, d2, side.s, scale2.p);
+            HSSMF_CUDA(cudaEventRecord(side.done, side.s));
+            spec_d = d2;
+          }
         }
         double sc = 0;
         d2h(&sc, scale.p, sizeof(double), s);
@@ -349,6 +407,9 @@ namespace hssmf_b200 {
         if (d - o.p >= o.max_rank) throw HssRankError(fail, o.max_rank);
         d += o.dd;
       }
+      // a speculative round may still run: the main stream waits for it
+      // before anything reuses its buffers
+      if (spec_d >= 0) HSSMF_CUDA(cudaStreamWaitEvent(s, side.done, 0));
     }
 
     // index lists for the permuted gather of a stacked pair of r-row blocks
@@ -1429,6 +1490,7 @@ namespace hssmf_b200 {
       v[i].ms = d_->ph_ms[i];
       v[i].flops = d_->ph_fl[i];
       v[i].count = d_->ph_n[i];
+      v[i].host_ms = d_->ph_host[i];
     }
     return v;
   }

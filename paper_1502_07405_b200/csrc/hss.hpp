@@ -65,6 +65,7 @@ namespace hssmf_b200 {
   struct HssPhaseStat {
     double ms = 0, flops = 0;
     int count = 0;
+    double host_ms = 0;  // host time spent issuing the phase (incl. its syncs)
   };
 
   class HssMatrixDev {
