@@ -173,3 +173,21 @@ def test_gmres_on_c3_reaches_tight_residual():
     x, rep = P.gmres(op.a, m, b, 30, 1e-10, 0.0, 60)
     assert rep.converged
     assert rel_residual(op.a, x, b) <= 1e-9
+
+
+def test_run_stats_of_a_device_factorization():
+    import json
+    from paper_1502_07405_b200.stats import run_stats, stats_csv_row, stats_to_json
+    op = P.ordered_grid("p2d", 31, 16)
+    so = P.SolverOptions(nd_leaf=16, ls=3, min_hss=24, leaf=16, eps=1e-6, d0=32, dd=32, p=8)
+    m = P.mf_factor(op.a, op.t, so)
+    b = np.random.default_rng(29).standard_normal(op.a.size())
+    x, rep = P.iterative_refinement(op.a, m, b)
+    s = run_stats(m, so, op.a, source="p2d 31", method="refinement", iterations=rep.iterations,
+                  relres=rel_residual(op.a, x, b), converged=rep.converged)
+    j = json.loads(stats_to_json(s))
+    assert j["factor"]["hss_fronts"] == m.hss_fronts >= 1
+    assert j["factor"]["fronts"] == len(j["per_front"]) == len(m.level)
+    assert sum(f["type"] == "hss" for f in j["per_front"]) == m.hss_fronts
+    assert j["solve"]["converged"] and j["config"]["eps"] == 1e-6
+    assert len(stats_csv_row(s).split(",")) >= 39
