@@ -215,6 +215,13 @@ int hssmf_dev_gemm(int device, char ta, char tb, int m, int n, int k, double alp
 int hssmf_dev_id(int device, const double* y, int m, int n, double eps, int max_rank,
                  double abs_tol, int* perm, int* rank, int* certified, double* coeffs,
                  hssmf_status* st);
+/* the Gram route of the same ID (no reference counterpart: a BLAS3 restatement
+ * of rrqr_tolerance, rrqr.hpp:32-151, used by the HSS path for eps >= 5e-5):
+ * pivoted Cholesky of Y^T Y with the CPQR stop rules; r receives R = L^T
+ * (rank x n, column j = position j) */
+int hssmf_dev_gram_id(int device, const double* y, int m, int n, double eps, int max_rank,
+                      double abs_tol, int* perm, int* rank, int* certified, double* r,
+                      hssmf_status* st);
 /* lu_partial_pivot (lu.hpp:80-85) on the device panel kernels; a is m x n (m>=n) */
 int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st);
 

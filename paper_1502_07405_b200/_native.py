@@ -99,6 +99,9 @@ _SIGS = {
     "hssmf_dev_id": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_int,
                                C.c_double, i32p, C.POINTER(C.c_int), C.POINTER(C.c_int), vp,
                                C.POINTER(Status)]),
+    "hssmf_dev_gram_id": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_int,
+                                    C.c_double, i32p, C.POINTER(C.c_int), C.POINTER(C.c_int), vp,
+                                    C.POINTER(Status)]),
     "hssmf_dev_lu": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, i32p, C.POINTER(Status)]),
     "hssmf_bench_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_double), C.POINTER(Status)]),

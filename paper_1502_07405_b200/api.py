@@ -579,6 +579,19 @@ def dev_interpolative_decomposition(y, eps, max_rank=-1, abs_tol=0.0, device=0):
     return perm, k, bool(cert.value), X[: k * (n - k)].reshape((k, n - k), order="F")
 
 
+def dev_gram_id(y, eps, max_rank=-1, abs_tol=0.0, device=0):
+    """Gram-route ID of y (d x n): (perm, rank, certified, R = L^T in position order)."""
+    Y = np.asfortranarray(y, np.float64)
+    m, n = Y.shape
+    perm = np.zeros(n, np.int32)
+    rank, cert = C.c_int(), C.c_int()
+    R = np.zeros(max(1, min(m, n) * n), np.float64)
+    _call("hssmf_dev_gram_id", device, Y.ctypes.data_as(C.c_void_p), m, n, eps, max_rank, abs_tol,
+          perm, C.byref(rank), C.byref(cert), R.ctypes.data_as(C.c_void_p))
+    k = rank.value
+    return perm, k, bool(cert.value), R[: k * n].reshape((k, n), order="F")
+
+
 def dev_lu(a, device=0):
     A = np.array(a, np.float64, order="F", copy=True)
     m, n = A.shape

@@ -502,6 +502,14 @@ int hssmf_dev_id(int device, const double* y, int m, int n, double eps, int max_
   });
 }
 
+int hssmf_dev_gram_id(int device, const double* y, int m, int n, double eps, int max_rank,
+                      double abs_tol, int* perm, int* rank, int* certified, double* r,
+                      hssmf_status* st) {
+  return guard(st, [&] {
+    test_gram_id(device, y, m, n, eps, max_rank, abs_tol, perm, rank, certified, r);
+  });
+}
+
 int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st) {
   return guard(st, [&] { *ms = bench_gemm(device, m, n, k, iters); });
 }

@@ -676,7 +676,12 @@ namespace hssmf_b200 {
     if (lst.empty()) return;
     std::vector<double*> F(lst.size());
     for (size_t q = 0; q < lst.size(); q++) F[q] = assemble_hss_front(lst[q], s);
-    size_t width = hstreams.size();
+    // fronts of >= 9000 rows saturate the device on their own (the Gram-route
+    // trailing updates are full-device, HBM-bound kernels, and concurrent
+    // ones starve the 16-CTA cluster panels): at most 4 of them at a time
+    int mmax = 0;
+    for (int i : lst) mmax = std::max(mmax, t.nodes[i].m());
+    size_t width = mmax >= 9000 ? std::min<size_t>(4, hstreams.size()) : hstreams.size();
     if (const char* e = getenv("HSSMF_HSS_STREAMS")) width = std::max(1, atoi(e));
     const int nw = (int)std::min<size_t>(lst.size(), std::min(width, hstreams.size()));
     std::vector<HssResult> res(lst.size());
@@ -688,7 +693,7 @@ namespace hssmf_b200 {
       return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
     const double t0 = now();
-    std::vector<double> tq(lst.size()), tw(lst.size());
+    std::vector<double> tq(lst.size()), tw(lst.size()), tstart(lst.size());
     std::vector<long long> nw_(lst.size());
     // admission: a front starts only while the device pool is below the
     // budget, unless nothing else runs (the rest is caught by the retry below)
@@ -716,6 +721,7 @@ namespace hssmf_b200 {
         }
         running++;
         const double a = now();
+        tstart[q] = a - t0;
         const SyncClock c0 = sync_clock();
         try {
           res[q] = compress_hss_front(lst[q], F[q], hstreams[w]);
@@ -765,8 +771,8 @@ namespace hssmf_b200 {
               lst.size(), now() - t0, used / 1e9, high / 1e9);
       for (size_t q = 0; q < lst.size(); q++) {
         const auto& fn = t.nodes[lst[q]];
-        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  %.3f s (sync wait %.3f s in %lld, arena %.0f MB) rounds=%d d=%d rank=%d |",
-                lst[q], fn.m(), fn.ns(), tq[q], tw[q], nw_[q],
+        fprintf(stderr, "[hssmf]   front %d m=%d ns=%d  start %.3f s, %.3f s (sync wait %.3f s in %lld, arena %.0f MB) rounds=%d d=%d rank=%d |",
+                lst[q], fn.m(), fn.ns(), tstart[q], tq[q], tw[q], nw_[q],
                 res[q].hss ? res[q].hss->arena_bytes() / 1e6 : 0.0, res[q].hss ? res[q].hss->rounds() : -1,
                 res[q].hss ? res[q].hss->d_final() : -1, res[q].hss ? res[q].hss->hss_rank() : -1);
         if (res[q].hss) {

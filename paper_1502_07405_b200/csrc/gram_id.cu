@@ -292,6 +292,275 @@ namespace hssmf_b200 {
       }
       cl.sync();  // no CTA leaves while a peer may still address its shared memory
     }
+
+    // ---- v2 panel: one row per thread, the row's panel columns in registers
+    // (the step loop is unrolled, so every panel column has a fixed register),
+    // a shared-memory copy only for the candidate push. Per step the critical
+    // path is: mbarrier wake -> warp-parallel decision over the CL candidates
+    // -> G(i, pj) load (the winner's panel row is read while it is in
+    // flight) -> division / downdate -> warp argmax -> one CTA barrier ->
+    // warp w pushes the CTA's candidate and its panel row to peer w
+    // (st.async, byte-counted mbarrier). No replicated position arrays: the
+    // CPQR column swap is resolved locally (the row at position j is the one
+    // whose position equals j; it takes the pivot's old position, which
+    // travels with the candidate).
+    __device__ __forceinline__ void warp_best(double& v, int& p, int& ix) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (better(v2, p2, v, p)) { v = v2; p = p2; ix = i2; }
+      }
+    }
+
+    template <int T, int NB>
+    __global__ void __launch_bounds__(T, 1)
+    gram_panel2_kernel(const GramTask* __restrict__ tasks, int k0, double eps, double abs_tol,
+                       int CL, int init) {
+      constexpr int NW = T / 32;
+      cg::cluster_group cl = cg::this_cluster();
+      const int rank = (int)cl.block_rank();
+      const GramTask Tk = tasks[blockIdx.x / CL];
+      const int n = Tk.n;
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      const int i = rank * T + tid;
+      const bool have = i < n;
+      extern __shared__ __align__(16) double sm2[];
+      double* Lp = sm2;  // [NB][T]: own rows' panel columns (push source)
+      __shared__ __align__(16) Cand stc[2][16];
+      __shared__ __align__(16) double strow[2][16][NB];
+      __shared__ __align__(8) unsigned long long mbar[2];
+      __shared__ Cand wred[2][NW];
+
+      if (__ldcg(Tk.state + 1) && !init) return;  // finished in an earlier panel (uniform)
+      double dg = 0.0;
+      int pos = INT_MAX, flg = 1;
+      if (have) {
+        if (init) {
+          dg = Tk.G[i + (size_t)i * n];
+          pos = i;
+          flg = 0;
+        } else {
+          dg = __ldcg(Tk.dg + i);
+          pos = __ldcg(Tk.pos_of + i);
+          flg = __ldcg(Tk.flag + i);
+        }
+      }
+      // own row's panel columns (zero until set; pivoted rows stay 0)
+#pragma unroll
+      for (int q = 0; q < NB; q++) Lp[q * T + tid] = 0.0;
+      double r11 = init ? 0.0 : __ldcg(Tk.r11);
+      if (tid == 0) {
+        mbar_init(smem_u32(&mbar[0]), 1);
+        mbar_init(smem_u32(&mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      // candidate of this CTA for the step whose buffer is b; the panel row
+      // carries nv values. Warp w sends it to peer w.
+      auto propose = [&](int b, int nv) {
+        double v = (have && !flg) ? dg : -1.0;
+        int p = (have && !flg) ? pos : INT_MAX, ix = (have && !flg) ? i : -1;
+        warp_best(v, p, ix);
+        if (lane == 0) wred[b][warp] = {v, p, ix};
+        __syncthreads();
+        if (warp >= CL) return;
+        if (lane < NW) {
+          const Cand c = wred[b][lane];
+          v = c.v;
+          p = c.pos;
+          ix = c.idx;
+        } else {
+          v = -1.0;
+          p = INT_MAX;
+          ix = -1;
+        }
+        warp_best(v, p, ix);
+        const int peer = warp;
+        const uint32_t rbar = mapa(smem_u32(&mbar[b]), peer);
+        if (lane == 0)
+          st_async_v2(mapa(smem_u32(&stc[b][rank]), peer), (unsigned long long)__double_as_longlong(v),
+                      (unsigned long long)(unsigned)p | ((unsigned long long)(unsigned)ix << 32), rbar);
+        if (lane < nv) {
+          const double rv = ix >= 0 ? Lp[lane * T + (ix - rank * T)] : 0.0;
+          st_async_b64(mapa(smem_u32(&strow[b][rank][lane]), peer),
+                       (unsigned long long)__double_as_longlong(rv), rbar);
+        }
+      };
+      int stopped = 0, cert = 0, jend = k0;
+      if (n == 0 || Tk.kmax_dim == 0) {
+        stopped = 1;
+        cert = 1;
+      }
+      cl.sync();  // every peer's mbarriers are initialised
+      if (!stopped) propose(0, 0);
+      // rolled step loop: an unrolled one overflows the instruction cache
+#pragma unroll 1
+      for (int jj = 0; jj < NB; jj++) {
+        if (!stopped) {
+          const int j = k0 + jj, buf = jj & 1;
+          if (tid == 0) mbar_arrive_expect(smem_u32(&mbar[buf]), (uint32_t)(CL * (16 + 8 * jj)));
+          mbar_wait(smem_u32(&mbar[buf]), (jj >> 1) & 1);
+          // decision (rrqr.hpp:62-77: largest residual norm, lowest position on ties)
+          double bv = -1.0;
+          int bp = INT_MAX, bi = -1;
+          if (lane < CL) {
+            const Cand c = stc[buf][lane];
+            bv = c.v;
+            bp = c.pos;
+            bi = c.idx;
+          }
+          warp_best(bv, bp, bi);
+          const double pv = bv > 0.0 ? sqrt(bv) : 0.0;
+          int stop = 0, ct = 0;
+          if (j == 0) {
+            r11 = pv;
+            if (pv == 0.0 || pv <= abs_tol) { stop = 1; ct = 1; }
+          } else if (pv <= eps * r11 || pv <= abs_tol) {
+            stop = 1;
+            ct = 1;
+          }
+          if (!stop && j == Tk.kmax) {
+            stop = 1;
+            ct = (j == Tk.kmax_dim);
+          }
+          if (stop) {
+            stopped = 1;
+            cert = ct;
+            jend = j;
+          } else {
+            const int pj = bi, pp = bp;
+            const double ljj = pv;
+            const bool act = have && !flg;
+            double gv = 0.0;
+            if (act && i != pj) gv = i >= pj ? Tk.G[i + (size_t)pj * n] : Tk.G[pj + (size_t)i * n];
+            const double* prow = strow[buf][pj / T];
+            double t0 = 0.0, t1 = 0.0;
+            const double* lrow = Lp + tid;
+            int q = 0;
+#pragma unroll 4
+            for (; q + 1 < jj; q += 2) {
+              t0 += lrow[q * T] * prow[q];
+              t1 += lrow[(q + 1) * T] * prow[q + 1];
+            }
+            if (q < jj) t0 += lrow[q * T] * prow[q];
+            if (act) {
+              double lo;
+              if (i == pj) {
+                flg = 1;
+                lo = ljj;
+              } else {
+                lo = (gv - (t0 + t1)) / ljj;
+                double dd = dg - lo * lo;
+                if (dd < 0.0) dd = 0.0;
+                dg = dd;
+              }
+              Lp[jj * T + tid] = lo;
+            }
+            if (have) {
+              if (i == pj) pos = j;
+              else if (pos == j) pos = pp;
+            }
+            if (j + 1 == Tk.kmax_dim) {  // factorization exhausted exactly
+              stopped = 1;
+              cert = 1;
+              jend = j + 1;
+            } else {
+              propose(buf ^ 1, jj + 1);
+              jend = j + 1;
+            }
+          }
+        }
+      }
+      // the panel's columns of L (pivoted rows hold 0), state for the next
+      // panel / the host, the current ID permutation
+      const int ncol = jend - k0;
+      if (have) {
+        for (int q = 0; q < ncol; q++) Tk.L[i + (size_t)(k0 + q) * n] = Lp[q * T + tid];
+        __stcg(Tk.dg + i, dg);
+        __stcg(Tk.flag + i, flg);
+        __stcg(Tk.pos_of + i, pos);
+        __stcg(Tk.orig_at + pos, i);
+      }
+      if (rank == 0 && tid == 0) {
+        if (k0 == 0) __stcg(Tk.r11, r11);
+        __stcg(Tk.state + 0, jend);
+        __stcg(Tk.state + 1, stopped);
+        __stcg(Tk.state + 2, cert);
+      }
+      cl.sync();  // no CTA leaves while a peer may still address its shared memory
+    }
+
+    // trailing update of the Gram matrix after a panel: G_lower -= Lp Lp^T,
+    // Lp = the panel's NB columns of L (n x NB, ld n). HBM-bound (each lower
+    // element read and written once, 2 NB flops): 64 x 64 tiles of the lower
+    // triangle, the two L row blocks staged in shared memory, 4 x 4 outputs
+    // per thread, the G tile loads issued before the products. Tasks that
+    // stopped in the panel are skipped.
+    template <int NB>
+    __global__ void __launch_bounds__(256, 2)
+    gram_syrk_kernel(const GramTask* __restrict__ tasks, int k0) {
+      const GramTask Tk = tasks[blockIdx.y];
+      const int n = Tk.n;
+      const int nbt = (n + 63) >> 6;
+      const int t = blockIdx.x;
+      if (t >= nbt * (nbt + 1) / 2) return;
+      if (__ldcg(Tk.state + 1)) return;
+      int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while (ti * (ti + 1) / 2 > t) ti--;
+      while ((ti + 1) * (ti + 2) / 2 <= t) ti++;
+      const int tj = t - ti * (ti + 1) / 2;
+      const int i0 = ti * 64, j0 = tj * 64;
+      extern __shared__ __align__(16) double sm3[];
+      double (*As)[64] = reinterpret_cast<double (*)[64]>(sm3);
+      double (*Bs)[64] = reinterpret_cast<double (*)[64]>(sm3 + NB * 64);
+      // thread (tx, ty) owns rows i0 + tx + 16 a and columns j0 + 4 ty + b, so
+      // that a warp's G accesses are 128-byte row runs of two columns
+      const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+      // the two L row blocks by cp.async (all in flight at once), then the G
+      // tile loads, which complete while the products run
+      const double* Lk = Tk.L + (size_t)k0 * n;
+#pragma unroll
+      for (int e = tid; e < NB * 64; e += 256) {
+        const int q = e >> 6, r = e & 63;
+        const bool va = i0 + r < n, vb = j0 + r < n;
+        cp_async8(&As[q][r], va ? Lk + i0 + r + (size_t)q * n : Lk, va);
+        cp_async8(&Bs[q][r], vb ? Lk + j0 + r + (size_t)q * n : Lk, vb);
+      }
+      cp_async_commit();
+      double* G = Tk.G + i0 + tx + (size_t)(j0 + ty * 4) * n;
+      const int jm = n - (j0 + ty * 4), im = n - (i0 + tx);
+      double c[4][4];
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+          c[a][b] = (16 * a < im && b < jm) ? G[16 * a + (size_t)b * n] : 0.0;
+      cp_async_wait<0>();
+      __syncthreads();
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < NB; q++) {
+        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[q][ty * 4]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[q][ty * 4 + 2]);
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+          const double av = As[q][tx + 16 * a];
+#pragma unroll
+          for (int b = 0; b < 4; b++) acc[a][b] = fma(av, bv[b], acc[a][b]);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+          if (16 * a < im && b < jm && i0 + tx + 16 * a >= j0 + ty * 4 + b)
+            G[16 * a + (size_t)b * n] = c[a][b] - acc[a][b];
+    }
   }  // namespace
 
   void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
@@ -337,9 +606,63 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaMemcpyAsync(d, tasks.data(), nt * sizeof(GramTask), cudaMemcpyHostToDevice, s));
     }
     std::vector<int> hst(3 * nt);
+    // v2 panel (one row per thread) up to 16 x 512 rows; HSSMF_GRAM_V1=1 keeps
+    // the shared-memory panel kernel (measurement knob)
+    const bool force_v1 = getenv("HSSMF_GRAM_V1") != nullptr;
+    constexpr int NB2 = 32;
+    const bool v2 = !force_v1 && max_n <= 16 * 512;
+    int T2 = 512, CL2 = 1;
+    if (v2) {
+      if (max_n <= 256) T2 = 256;
+      while (CL2 * T2 < max_n) CL2 *= 2;
+      static bool attr2 = false;
+      if (!attr2) {
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<512, NB2>,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<512, NB2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * NB2 * 8));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<256, NB2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * NB2 * 8));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_kernel<NB2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 64 * 8));
+        attr2 = true;
+      }
+      CL = CL2;
+      nb = NB2;
+    }
     // all panels are queued without host round trips: a finished task's
     // panel kernel returns at once and its trailing GEMM is skipped on device
     for (int k0 = 0; k0 <= kmax; k0 += nb) {
+      if (v2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nt * CL2);
+        cfg.blockDim = dim3(T2);
+        cfg.dynamicSmemBytes = (size_t)T2 * NB2 * 8;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (T2 == 512)
+          HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<512, NB2>, (const GramTask*)d, k0,
+                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
+        else
+          HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<256, NB2>, (const GramTask*)d, k0,
+                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
+        HSSMF_LAUNCH_CHECK();
+        if (k0 + nb > kmax) break;
+        const int nbt = (max_n + 63) / 64;
+        gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
+            (const GramTask*)d, k0);
+        HSSMF_LAUNCH_CHECK();
+        if (flops)
+          for (const auto& T : tasks)
+            if (k0 <= T.kmax) *flops += (double)T.n * T.n * NB2;
+        continue;
+      }
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(nt * CL);
       cfg.blockDim = dim3(GT);

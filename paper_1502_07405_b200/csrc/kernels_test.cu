@@ -68,6 +68,40 @@ namespace hssmf_b200 {
                             cudaMemcpyDeviceToHost));
   }
 
+  // Gram route of the ID (gram_id.cuh): G = Y^T Y (lower triangle), pivoted
+  // Cholesky with the CPQR stop rules; returns the permutation, rank,
+  // certification and R = L^T (rank x n, columns in position order)
+  void test_gram_id(int device, const double* y, int m, int n, double eps, int max_rank,
+                    double abs_tol, int* perm, int* rank, int* certified, double* r) {
+    HSSMF_CUDA(cudaSetDevice(device));
+    Buf Y((size_t)m * n * 8), G((size_t)n * n * 8);
+    HSSMF_CUDA(cudaMemcpy(Y.p, y, (size_t)m * n * 8, cudaMemcpyHostToDevice));
+    if (n && m) {
+      GemmProblem g{Y.as<double>(), Y.as<double>(), G.as<double>(), n, n, m, m, m, n};
+      g.lower = 1;
+      gemm_run_host({g}, 'T', 'N', 1.0, 0.0, 0);
+    }
+    const int kdim = std::min(m, n), kmax = max_rank < 0 ? kdim : std::min(kdim, max_rank);
+    const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
+    Buf L((size_t)n * kcap * 8), dg((size_t)n * 8), fl((size_t)n * 4), pos((size_t)n * 4),
+        P((size_t)n * 4), st(12), r11(8);
+    GramTask t{G.as<double>(), L.as<double>(), dg.as<double>(), fl.as<int>(), P.as<int>(),
+               pos.as<int>(), st.as<int>(), r11.as<double>(), n, kdim, kmax, kcap};
+    std::vector<int> rk, ce;
+    gram_cholesky_run({t}, eps, abs_tol, 0, rk, ce);
+    HSSMF_CUDA(cudaDeviceSynchronize());
+    *rank = rk[0];
+    *certified = ce[0];
+    HSSMF_CUDA(cudaMemcpy(perm, P.p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    const int k = rk[0];
+    if (k) {
+      std::vector<double> hl((size_t)n * k);
+      HSSMF_CUDA(cudaMemcpy(hl.data(), L.p, hl.size() * 8, cudaMemcpyDeviceToHost));
+      for (int j = 0; j < n; j++)
+        for (int q = 0; q < k; q++) r[q + (size_t)j * k] = hl[perm[j] + (size_t)q * n];
+    }
+  }
+
   void test_lu(int device, double* a, int m, int n, int* piv) {
     if (m != n) throw std::invalid_argument("dev lu: square matrices only");
     HSSMF_CUDA(cudaSetDevice(device));

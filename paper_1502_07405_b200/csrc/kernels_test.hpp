@@ -10,6 +10,8 @@ namespace hssmf_b200 {
                  int ldc);
   void test_id(int device, const double* y, int m, int n, double eps, int max_rank,
                double abs_tol, int* perm, int* rank, int* certified, double* coeffs);
+  void test_gram_id(int device, const double* y, int m, int n, double eps, int max_rank,
+                    double abs_tol, int* perm, int* rank, int* certified, double* r);
   void test_lu(int device, double* a, int m, int n, int* piv);
   double bench_gemm(int device, int m, int n, int k, int iters);
   // pivoted-Cholesky ID kernel timing: ntask tasks of an n x n Gram matrix of

@@ -117,3 +117,39 @@ def test_id_cluster_cpqr_matches_reference(oracle, monkeypatch, cl):
 def test_id_zero_and_empty():
     p, k, cert, _ = A.dev_interpolative_decomposition(np.zeros((8, 5)), 1e-6)
     assert k == 0 and cert and list(p) == [0, 1, 2, 3, 4]
+
+
+@pytest.mark.parametrize("v1", ["0", "1"])
+@pytest.mark.parametrize("m,n,rank", [(60, 200, 40), (200, 480, 150), (300, 1000, 260),
+                                      (160, 3000, 140), (120, 7000, 100)])
+def test_gram_id_matches_reference(oracle, monkeypatch, v1, m, n, rank):
+    # the Gram route (pivoted Cholesky of Y^T Y; single CTA, 2/4/8/16-CTA
+    # clusters, many 32-step panels) against the reference's Householder CPQR
+    if v1 == "1":
+        monkeypatch.setenv("HSSMF_GRAM_V1", "1")
+    rng = np.random.default_rng(m + n)
+    y = (rng.standard_normal((m, rank)) * np.logspace(0, -6, rank)) @ rng.standard_normal((rank, n))
+    for eps, mr, at in [(1e-4, -1, 0.0), (1e-3, -1, 0.0), (1e-4, rank // 3, 0.0),
+                        (1e-4, -1, 1e-2 * np.abs(y).max())]:
+        p, k, cert, r = A.dev_gram_id(y, eps, mr, at)
+        wp, wk, wcert, _ = oracle.interpolative_decomposition(y, eps, mr, at)
+        assert (k, cert) == (wk, wcert)
+        assert sorted(p) == list(range(n))
+        assert np.array_equal(p[:min(k, 12)], wp[:min(k, 12)])
+        if k:
+            # R = L^T: upper triangular on the pivots, R^T R = Y^T Y on them
+            r1 = r[:, :k]
+            assert np.allclose(np.tril(r1, -1), 0.0)
+            yp = y[:, p[:k]]
+            assert np.allclose(r1.T @ r1, yp.T @ yp, rtol=1e-9, atol=1e-9 * np.abs(yp.T @ yp).max())
+            # the whole R reproduces the Gram rows of the pivots
+            assert np.allclose(r1.T @ r, yp.T @ y[:, p], rtol=1e-8,
+                               atol=1e-8 * np.abs(yp.T @ y).max())
+
+
+def test_gram_id_zero_and_empty():
+    p, k, cert, _ = A.dev_gram_id(np.zeros((8, 5)), 1e-4)
+    assert k == 0 and cert and list(p) == [0, 1, 2, 3, 4]
+    y = np.random.default_rng(1).standard_normal((6, 4))
+    p, k, cert, _ = A.dev_gram_id(y, 1e-12)  # full rank: exhausted = certified
+    assert k == 4 and cert
