@@ -225,6 +225,19 @@ int hssmf_dev_gram_id(int device, const double* y, int m, int n, double eps, int
 /* lu_partial_pivot (lu.hpp:80-85) on the device panel kernels; a is m x n (m>=n) */
 int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st);
 
+/* measurement (no reference counterpart): per-kernel device-time probes used
+ * by bench.py's roofline entries. While enabled, every launch of the probed
+ * kernels is bracketed by CUDA events on its stream; read returns, per kind
+ * (0 = DMMA grouped GEMM, 1 = Gram-ID cluster panel, 2 = Gram-ID trailing
+ * SYRK), the launch count, summed device ms and algorithmic flops / bytes,
+ * and resets them. */
+typedef struct {
+  long long launches;
+  double ms, flops, bytes;
+} hssmf_probe_stat;
+int hssmf_probe_enable(int on, hssmf_status* st);
+int hssmf_probe_read(hssmf_probe_stat* out /* [3] */, hssmf_status* st);
+
 /* measurement: average device time (ms) of `iters` m x n x k DGEMMs (NN) on
  * the DMMA kernel, device-resident operands; used for the FP64 roofline */
 int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st);

@@ -24,6 +24,11 @@ class Status(C.Structure):
                 ("msg", C.c_char * 512)]
 
 
+class ProbeStat(C.Structure):
+    _fields_ = [("launches", C.c_longlong), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
 class Options(C.Structure):
     _fields_ = [("ls", C.c_int), ("eps", C.c_double), ("leaf", C.c_int), ("d0", C.c_int),
                 ("dd", C.c_int), ("p", C.c_int), ("min_hss", C.c_int),
@@ -103,6 +108,8 @@ _SIGS = {
                                     C.c_double, i32p, C.POINTER(C.c_int), C.POINTER(C.c_int), vp,
                                     C.POINTER(Status)]),
     "hssmf_dev_lu": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, i32p, C.POINTER(Status)]),
+    "hssmf_probe_enable": (C.c_int, [C.c_int, C.POINTER(Status)]),
+    "hssmf_probe_read": (C.c_int, [C.POINTER(ProbeStat), C.POINTER(Status)]),
     "hssmf_bench_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_double), C.POINTER(Status)]),
     "hssmf_bench_gram": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

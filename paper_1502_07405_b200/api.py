@@ -592,6 +592,21 @@ def dev_gram_id(y, eps, max_rank=-1, abs_tol=0.0, device=0):
     return perm, k, bool(cert.value), R[: k * n].reshape((k, n), order="F")
 
 
+PROBE_KINDS = ("gemm_dmma", "gram_panel", "gram_syrk")
+
+
+def probe_enable(on=True):
+    """Per-kernel device-time probes (measurement only, see hssmf_probe_enable)."""
+    _call("hssmf_probe_enable", 1 if on else 0)
+
+
+def probe_read():
+    out = (N.ProbeStat * len(PROBE_KINDS))()
+    _call("hssmf_probe_read", out)
+    return {k: {"launches": int(o.launches), "ms": o.ms, "flops": o.flops, "bytes": o.bytes}
+            for k, o in zip(PROBE_KINDS, out)}
+
+
 def dev_lu(a, device=0):
     A = np.array(a, np.float64, order="F", copy=True)
     m, n = A.shape

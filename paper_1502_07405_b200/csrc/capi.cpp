@@ -510,6 +510,18 @@ int hssmf_dev_gram_id(int device, const double* y, int m, int n, double eps, int
   });
 }
 
+int hssmf_probe_enable(int on, hssmf_status* st) {
+  return guard(st, [&] { probe_enable(on != 0); });
+}
+
+int hssmf_probe_read(hssmf_probe_stat* out, hssmf_status* st) {
+  return guard(st, [&] {
+    ProbeStat p[PROBE_KINDS];
+    probe_read(p);
+    for (int k = 0; k < PROBE_KINDS; k++) out[k] = {p[k].launches, p[k].ms, p[k].flops, p[k].bytes};
+  });
+}
+
 int hssmf_bench_gemm(int device, int m, int n, int k, int iters, double* ms, hssmf_status* st) {
   return guard(st, [&] { *ms = bench_gemm(device, m, n, k, iters); });
 }

@@ -82,3 +82,29 @@ namespace hssmf_b200 {
 #endif
 
 }  // namespace hssmf_b200
+
+namespace hssmf_b200 {
+  // ---- per-kernel device-time probes (bench.py's roofline entries) ----------
+  // When enabled, the launchers of the probed kernels bracket every launch with
+  // CUDA events on the launching stream and record the launch's algorithmic
+  // flops / bytes; probe_read() synchronizes the device, sums and resets.
+  enum ProbeKind { PROBE_GEMM = 0, PROBE_GRAM_PANEL = 1, PROBE_GRAM_SYRK = 2, PROBE_KINDS = 3 };
+  struct ProbeStat {
+    long long launches;
+    double ms, flops, bytes;
+  };
+  bool probe_enabled();
+  void probe_enable(bool on);
+  void probe_read(ProbeStat out[PROBE_KINDS]);
+  // device counter the Gram SYRK kernel adds its live tasks' algorithmic bytes
+  // to (stopped tasks are skipped on the device, so the host cannot count them)
+  unsigned long long* probe_device_bytes();
+  struct ProbeScope {
+    int kind;
+    cudaStream_t s;
+    double flops, bytes;
+    cudaEvent_t a = nullptr;
+    ProbeScope(int k, cudaStream_t st, double f, double b);
+    ~ProbeScope();
+  };
+}  // namespace hssmf_b200

@@ -449,6 +449,7 @@ namespace hssmf_b200 {
       b.prefix = reinterpret_cast<const int*>(gpre.size());
       b.nprob = (int)probs.size();
       b.tiles = pre.back();
+      b.flops = gemm_flops(probs);
       gp.insert(gp.end(), probs.begin(), probs.end());
       gpre.insert(gpre.end(), pre.begin(), pre.end());
       return b;

@@ -205,6 +205,7 @@ namespace hssmf_b200 {
     const bool TA = ta != 'N', TB = tb != 'N';
     set_gemm_attrs();
     dim3 grid(b.tiles), block(THREADS);
+    ProbeScope pr(PROBE_GEMM, s, probe_enabled() ? b.flops : 0.0, 0.0);
     if (!TA && !TB) gemm_grouped_kernel<false, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
     else if (TA && !TB) gemm_grouped_kernel<true, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
     else if (!TA && TB) gemm_grouped_kernel<false, true><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
@@ -283,6 +284,11 @@ namespace hssmf_b200 {
       if (!b.nprob) return;
       const int tiles = b.pre[b.nprob];
       if (tiles) {
+        double fl = 0;
+        if (probe_enabled())
+          for (int q = 0; q < b.nprob; q++)
+            fl += (b.p[q].lower ? 1.0 : 2.0) * b.p[q].m * b.p[q].n * b.p[q].k;
+        ProbeScope pr(PROBE_GEMM, s, fl, 0.0);
         gemm_param_kernel<<<tiles, THREADS, SMEM, s>>>(b);
         HSSMF_LAUNCH_CHECK();
       }

@@ -40,6 +40,7 @@ namespace hssmf_b200 {
     const int* prefix = nullptr;
     int nprob = 0;
     int tiles = 0;
+    double flops = 0;  // 2 m n k summed (probe accounting)
   };
 
   constexpr int kGemmBM = 64, kGemmBN = 64;

@@ -498,13 +498,16 @@ namespace hssmf_b200 {
     // stopped in the panel are skipped.
     template <int NB>
     __global__ void __launch_bounds__(256, 2)
-    gram_syrk_kernel(const GramTask* __restrict__ tasks, int k0) {
+    gram_syrk_kernel(const GramTask* __restrict__ tasks, int k0, unsigned long long* probe_bytes) {
       const GramTask Tk = tasks[blockIdx.y];
       const int n = Tk.n;
       const int nbt = (n + 63) >> 6;
       const int t = blockIdx.x;
       if (t >= nbt * (nbt + 1) / 2) return;
       if (__ldcg(Tk.state + 1)) return;
+      // algorithmic bytes of a live task: its lower triangle read and written once
+      if (probe_bytes && t == 0 && threadIdx.x == 0)
+        atomicAdd(probe_bytes, (unsigned long long)n * (n + 1) / 2 * 16ull);
       int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
       while (ti * (ti + 1) / 2 > t) ti--;
       while ((ti + 1) * (ti + 2) / 2 <= t) ti++;
@@ -646,18 +649,24 @@ namespace hssmf_b200 {
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (T2 == 512)
-          HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<512, NB2>, (const GramTask*)d, k0,
-                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
-        else
-          HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<256, NB2>, (const GramTask*)d, k0,
-                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
-        HSSMF_LAUNCH_CHECK();
+        {
+          ProbeScope prp(PROBE_GRAM_PANEL, s, 0.0, 0.0);
+          if (T2 == 512)
+            HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<512, NB2>, (const GramTask*)d,
+                                          k0, eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
+          else
+            HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<256, NB2>, (const GramTask*)d,
+                                          k0, eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
+          HSSMF_LAUNCH_CHECK();
+        }
         if (k0 + nb > kmax) break;
         const int nbt = (max_n + 63) / 64;
-        gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
-            (const GramTask*)d, k0);
-        HSSMF_LAUNCH_CHECK();
+        {
+          ProbeScope prs(PROBE_GRAM_SYRK, s, 0.0, 0.0);
+          gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
+              (const GramTask*)d, k0, probe_enabled() ? probe_device_bytes() : nullptr);
+          HSSMF_LAUNCH_CHECK();
+        }
         if (flops)
           for (const auto& T : tasks)
             if (k0 <= T.kmax) *flops += (double)T.n * T.n * NB2;

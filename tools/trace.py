@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--tail-s", type=float, default=4.0)
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     g = P.generate_convdiff3d(cfg.k, 0.1) if cfg.kind == "cd3d" else P.generate_grid_problem(cfg.kind, cfg.k)
@@ -58,6 +59,7 @@ def main():
     kern = collections.defaultdict(lambda: [0, 0.0])
     kiv, t0, t1 = [], 1e30, 0
     threads = collections.defaultdict(float)
+    sev = collections.defaultdict(list)
     for e in ev:
         if e.get("ph") != "X":
             continue
@@ -73,6 +75,8 @@ def main():
             kern[nm][0] += 1
             kern[nm][1] += d
             kiv.append((float(e["ts"]), float(e["ts"]) + d))
+            st = e.get("args", {}).get("stream", -1)
+            sev[st].append((float(e["ts"]), d, nm))
         if c in ("kernel", "cuda_runtime", "cuda_driver", "gpu_memcpy", "gpu_memset"):
             t0 = min(t0, float(e["ts"]))
             t1 = max(t1, float(e["ts"]) + d)
@@ -87,6 +91,26 @@ def main():
            "api": [(k, v[0], round(v[1] / 1e3, 2), round(v[1] / max(v[0], 1), 2))
                    for k, v in sorted(api.items(), key=lambda x: -x[1][1])[:20]],
            "kernels": [(k, v[0], round(v[1] / 1e3, 2)) for k, v in sorted(kern.items(), key=lambda x: -x[1][1])[:20]]}
+    # per stream, over the final `tail_s` seconds of the timeline (the top
+    # HSS levels): busy fraction and kernel-time breakdown
+    tail_us = a.tail_s * 1e6
+    per = []
+    for st, lst in sev.items():
+        w = [(ts, d, nm) for ts, d, nm in lst if ts >= t1 - tail_us]
+        if not w:
+            continue
+        by = collections.Counter()
+        cnt = collections.Counter()
+        for ts, d, nm in w:
+            by[nm] += d
+            cnt[nm] += 1
+        span_s = max(ts + d for ts, d, _ in w) - min(ts for ts, _, _ in w)
+        per.append({"stream": st, "kernels": len(w), "busy_ms": round(sum(by.values()) / 1e3, 1),
+                    "span_ms": round(span_s / 1e3, 1),
+                    "top": [(k, cnt[k], round(v / 1e3, 1)) for k, v in by.most_common(12)]})
+    per.sort(key=lambda x: -x["busy_ms"])
+    out["tail_s"] = a.tail_s
+    out["tail_streams"] = per[:6]
     print(json.dumps(out, indent=1))
     with open(path, "rb") as f, gzip.open(path + ".gz", "wb") as g2:
         g2.write(f.read())
