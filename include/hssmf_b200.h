@@ -86,6 +86,28 @@ void hssmf_csr_free(hssmf_csr* a);
  * EliminationTree::from_separators (elimination_tree.cpp:10-26); perm[old]=new */
 int hssmf_nd_geometric(const int* dims, int ndims, int leaf, int* perm, hssmf_tree** out,
                        hssmf_status* st);
+/* nested_dissection_graph (ordering.cpp:224-236) of the structurally
+ * symmetrized adjacency of a (SparseMatrix::symmetric_graph,
+ * sparse_matrix.hpp:127-145), then EliminationTree::from_separators; fronts
+ * may have one child or an empty separator; perm[old] = new */
+int hssmf_nd_graph(const hssmf_csr* a, int leaf, int* perm, hssmf_tree** out, hssmf_status* st);
+/* reorder_tree_separators (separator_reorder.cpp:119-135) on the adjacency of
+ * a (already in the tree ordering): every front with selected[i] != 0 gets HSS
+ * separator clusters of at most b vertices (FrontNode::sep_clusters), used by
+ * front_cluster_tree (multifrontal.hpp:318-326) when it is compressed;
+ * perm[old] = new relabels inside those separators. As with the reference the
+ * caller then permutes a (hssmf_csr_permuted) and re-runs hssmf_symbolic. */
+int hssmf_reorder_separators(hssmf_tree* t, const hssmf_csr* a, const char* selected, int b,
+                             int* perm, hssmf_status* st);
+/* a front's separator cluster tree (postorder, root last); returns the node
+ * count (0: none, -1: bad front), arrays may be NULL */
+int hssmf_tree_sep_clusters(const hssmf_tree* t, int front, int* begin, int* end, int* child0,
+                            int* child1, int* parent);
+/* sets a front's separator clusters (the drop-in path for trees reordered by
+ * the reference's own reorder_tree_separators) */
+int hssmf_tree_set_sep_clusters(hssmf_tree* t, int front, int nnodes, const int* begin,
+                                const int* end, const int* child0, const int* child1,
+                                hssmf_status* st);
 /* EliminationTree with explicit nodes (upd sets optional: upd_ptr may be NULL) */
 int hssmf_tree_create(int n, int nnodes, const int* sep_begin, const int* sep_end,
                       const int* child0, const int* child1, const int* parent,

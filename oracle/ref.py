@@ -59,6 +59,8 @@ def lib():
                                       C.c_int, C.c_int, C.c_int]),
         "ref_ordered_from_arrays": (vp, [C.c_int, _i32p, _i32p, _f64c, C.c_int, _i32p,
                                          _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
+        "ref_ordered_graph": (vp, [C.c_int, _i32p, _i32p, _f64c, C.c_int, C.c_int, vp]),
+        "ref_ordered_sep_clusters": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp]),
         "ref_ordered_free": (None, [vp]),
         "ref_ordered_n": (C.c_int, [vp]),
         "ref_ordered_nnz": (C.c_longlong, [vp]),
@@ -153,6 +155,13 @@ class Ordered:
     def nnodes(self):
         return len(self.sep_begin)
 
+    def sep_clusters(self, i):
+        L = lib()
+        nn = L.ref_ordered_sep_clusters(self.h, int(i), None, None, None, None, None)
+        arr = [np.zeros(nn, np.int32) for _ in range(5)]
+        L.ref_ordered_sep_clusters(self.h, int(i), *[x.ctypes.data_as(C.c_void_p) for x in arr])
+        return arr
+
     def __del__(self):
         try:
             if self.h:
@@ -171,6 +180,20 @@ def ordered_csr_geom(ptr, ind, val, dims, ndims, nd_leaf) -> Ordered:
     return Ordered(lib().ref_ordered_csr_geom(
         n, np.ascontiguousarray(ptr, np.int32), np.ascontiguousarray(ind, np.int32),
         np.ascontiguousarray(val, np.float64), dims[0], dims[1], dims[2], ndims, nd_leaf))
+
+
+def ordered_graph(ptr, ind, val, nd_leaf, reorder_b=0, selected=None) -> Ordered:
+    """graph ND pipeline of the reference (+ separator reordering)"""
+    n = len(ptr) - 1
+    sel = None
+    if selected is not None:
+        sel = np.ascontiguousarray(np.asarray(selected, bool).astype(np.int8))
+    o = Ordered(lib().ref_ordered_graph(
+        n, np.ascontiguousarray(ptr, np.int32), np.ascontiguousarray(ind, np.int32),
+        np.ascontiguousarray(val, np.float64), int(nd_leaf), int(reorder_b),
+        sel.ctypes.data_as(C.c_void_p) if sel is not None else None))
+    o._keep = sel
+    return o
 
 
 def ordered_from_arrays(n, ptr, ind, val, sep_begin, sep_end, child0, child1, parent,

@@ -66,6 +66,7 @@ namespace hssmf {
 #include "hssmf/ordering.hpp"
 #include "hssmf/random_sampler.hpp"
 #include "hssmf/rrqr.hpp"
+#include "hssmf/separator_reorder.hpp"
 #include "hssmf/lu.hpp"
 #include "hssmf/solver_options.hpp"
 #include "hssmf/sparse_matrix.hpp"
@@ -208,6 +209,51 @@ void* ref_ordered_from_arrays(int n, const int* ptr, const int* ind, const doubl
   o->perm.resize(n);
   std::iota(o->perm.begin(), o->perm.end(), 0);
   return o;
+}
+
+// graph pipeline: nested_dissection_graph (ordering.cpp:224-236) + symbolic;
+// reorder_b > 0: reorder_tree_separators (separator_reorder.cpp:119-135) of the
+// selected fronts (selected == NULL: every front with a separator), then the
+// relabeled matrix and its symbolic analysis
+void* ref_ordered_graph(int n, const int* ptr, const int* ind, const double* val, int nd_leaf,
+                        int reorder_b, const char* selected) {
+  auto a = csr_copy(n, ptr, ind, val);
+  std::vector<int> gptr, gind;
+  a.symmetric_graph(gptr, gind);
+  Permutation perm;
+  auto st = nested_dissection_graph(n, gptr, gind, nd_leaf, perm);
+  auto* o = new Ordered;
+  o->a = a.permuted(perm.perm);
+  o->t = EliminationTree::from_separators(st, n);
+  symbolic_factorization(o->a, o->t);
+  o->perm = perm.perm;
+  if (reorder_b > 0) {
+    std::vector<char> sel(o->t.size());
+    for (int i = 0; i < o->t.size(); i++)
+      sel[i] = selected ? selected[i] : (o->t.node(i).sep_size() > 0);
+    std::vector<int> pptr, pind;
+    o->a.symmetric_graph(pptr, pind);
+    auto r = reorder_tree_separators(o->t, sel, pptr, pind, reorder_b);
+    o->a = o->a.permuted(r.perm);
+    for (int i = 0; i < n; i++) o->perm[i] = r.perm[o->perm[i]];
+    symbolic_factorization(o->a, o->t);
+  }
+  o->t.compute_levels();
+  return o;
+}
+
+int ref_ordered_sep_clusters(void* h, int front, int* begin, int* end, int* c0, int* c1,
+                             int* parent) {
+  const auto& c = static_cast<Ordered*>(h)->t.node(front).sep_clusters;
+  for (int i = 0; i < c.size(); i++) {
+    const auto& x = c.node(i);
+    if (begin) begin[i] = x.begin;
+    if (end) end[i] = x.end;
+    if (c0) c0[i] = x.child0;
+    if (c1) c1[i] = x.child1;
+    if (parent) parent[i] = x.parent;
+  }
+  return c.size();
 }
 
 void ref_ordered_free(void* h) { delete static_cast<Ordered*>(h); }

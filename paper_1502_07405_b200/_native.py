@@ -59,6 +59,11 @@ _SIGS = {
                                C.POINTER(C.c_longlong)]),
     "hssmf_tree_get": (None, [vp, i32p, i32p, i32p, i32p, i32p, i32p, i32p, i32p]),
     "hssmf_tree_free": (None, [vp]),
+    "hssmf_nd_graph": (C.c_int, [vp, C.c_int, i32p, C.POINTER(vp), C.POINTER(Status)]),
+    "hssmf_reorder_separators": (C.c_int, [vp, vp, vp, C.c_int, i32p, C.POINTER(Status)]),
+    "hssmf_tree_sep_clusters": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp]),
+    "hssmf_tree_set_sep_clusters": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp,
+                                              C.POINTER(Status)]),
     "hssmf_front_cluster_tree": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
     "hssmf_factor": (C.c_int, [C.c_int, vp, vp, C.POINTER(Options), C.POINTER(vp),
                                C.POINTER(Status)]),

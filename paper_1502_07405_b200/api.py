@@ -204,6 +204,23 @@ class EliminationTree:
     def size(self):
         return len(self.sep_begin)
 
+    def sep_clusters(self, i):
+        """FrontNode::sep_clusters of front i as (begin, end, child0, child1,
+        parent) arrays (empty when the separator was not reordered)"""
+        L = N.lib()
+        nn = L.hssmf_tree_sep_clusters(self._h, int(i), None, None, None, None, None)
+        if nn < 0:
+            raise IoError("sep_clusters: front out of range")
+        arr = [np.zeros(nn, np.int32) for _ in range(5)]
+        L.hssmf_tree_sep_clusters(self._h, int(i), *[x.ctypes.data_as(C.c_void_p) for x in arr])
+        return arr
+
+    def set_sep_clusters(self, i, begin, end, child0, child1):
+        a = lambda x: np.ascontiguousarray(x, np.int32)  # noqa: E731
+        b, e, c0, c1 = a(begin), a(end), a(child0), a(child1)
+        _call("hssmf_tree_set_sep_clusters", self._h, int(i), len(b),
+              *[x.ctypes.data_as(C.c_void_p) for x in (b, e, c0, c1)])
+
     def root_id(self):
         return self.size() - 1
 
@@ -228,6 +245,44 @@ def nested_dissection_geometric(geom: GridGeometry, leaf: int):
     _call("hssmf_nd_geometric", np.ascontiguousarray(geom.dims, np.int32), geom.ndims,
           int(leaf), perm, C.byref(h))
     return EliminationTree(h), perm
+
+
+def nested_dissection_graph(a: SparseMatrix, leaf: int):
+    """ordering.cpp:224-236 on a.symmetric_graph() + from_separators; returns
+    (tree without upd sets, perm with perm[old] = new)"""
+    perm = np.zeros(a.size(), np.int32)
+    h = C.c_void_p()
+    _call("hssmf_nd_graph", a._h, int(leaf), perm, C.byref(h))
+    return EliminationTree(h), perm
+
+
+def reorder_tree_separators(t: EliminationTree, a: SparseMatrix, selected, b: int):
+    """separator_reorder.cpp:119-135: selected fronts get separator clusters
+    of at most b vertices; returns perm[old] = new (identity elsewhere). The
+    caller permutes a and re-runs symbolic_factorization."""
+    sel = np.ascontiguousarray(np.asarray(selected, bool).astype(np.int8))
+    if len(sel) != t.size():
+        raise IoError("reorder: one selection flag per front")
+    perm = np.zeros(t.n, np.int32)
+    _call("hssmf_reorder_separators", t._h, a._h, sel.ctypes.data_as(C.c_void_p), int(b), perm)
+    return perm
+
+
+def ordered_graph(a: SparseMatrix, nd_leaf: int, reorder_b: int = 0, selected=None):
+    """graph-ordering pipeline: ND + symbolic, then (reorder_b > 0) separator
+    reordering of the selected fronts (default: every front with a
+    separator) and the symbolic analysis of the relabeled matrix"""
+    t, perm = nested_dissection_graph(a, nd_leaf)
+    ap = a.permuted(perm)
+    symbolic_factorization(ap, t)
+    if reorder_b > 0:
+        if selected is None:
+            selected = (t.sep_end - t.sep_begin) > 0
+        r = reorder_tree_separators(t, ap, selected, reorder_b)
+        ap = ap.permuted(r)
+        perm = r[perm]
+        symbolic_factorization(ap, t)
+    return OrderedProblem(ap, t, perm, None)
 
 
 def symbolic_factorization(a: SparseMatrix, t: EliminationTree):
@@ -260,7 +315,7 @@ def ordered_problem(g: GridProblem, nd_leaf: int) -> OrderedProblem:
     return OrderedProblem(a, t, perm, g.geom)
 
 
-def ordered_grid(kind: str, k: int, nd_leaf: int, nu: float = 1e-4) -> OrderedProblem:
+def ordered_grid(kind: str, k: int, nd_leaf: int, nu: float = 1e-4) -> OrderedProblem:  # noqa: E302
     return ordered_problem(generate_grid_problem(kind, k, nu), nd_leaf)
 
 

@@ -249,6 +249,61 @@ int hssmf_symbolic(const hssmf_csr* a, hssmf_tree* t, hssmf_status* st) {
   });
 }
 
+int hssmf_nd_graph(const hssmf_csr* a, int leaf, int* perm, hssmf_tree** out, hssmf_status* st) {
+  return guard(st, [&] {
+    std::vector<int> gptr, gind, p;
+    a->a.symmetric_graph(gptr, gind);
+    auto* t = new hssmf_tree;
+    t->t = nested_dissection_graph(a->a.n, gptr, gind, leaf, p);
+    if (a->a.n) std::memcpy(perm, p.data(), p.size() * sizeof(int));
+    *out = t;
+  });
+}
+
+int hssmf_reorder_separators(hssmf_tree* t, const hssmf_csr* a, const char* selected, int b,
+                             int* perm, hssmf_status* st) {
+  return guard(st, [&] {
+    if (a->a.n != t->t.n) throw SolverFailure(1, -1, -1, "reorder: size mismatch");
+    std::vector<int> gptr, gind;
+    a->a.symmetric_graph(gptr, gind);
+    std::vector<char> sel(selected, selected + t->t.nodes.size());
+    const auto p = reorder_tree_separators(t->t, sel, gptr, gind, b);
+    if (t->t.n) std::memcpy(perm, p.data(), p.size() * sizeof(int));
+  });
+}
+
+int hssmf_tree_sep_clusters(const hssmf_tree* t, int front, int* begin, int* end, int* child0,
+                            int* child1, int* parent) {
+  if (front < 0 || front >= (int)t->t.nodes.size()) return -1;
+  const auto& c = t->t.nodes[front].sep_clusters.nodes;
+  for (size_t i = 0; i < c.size(); i++) {
+    if (begin) begin[i] = c[i].begin;
+    if (end) end[i] = c[i].end;
+    if (child0) child0[i] = c[i].child0;
+    if (child1) child1[i] = c[i].child1;
+    if (parent) parent[i] = c[i].parent;
+  }
+  return (int)c.size();
+}
+
+int hssmf_tree_set_sep_clusters(hssmf_tree* t, int front, int nnodes, const int* begin,
+                                const int* end, const int* child0, const int* child1,
+                                hssmf_status* st) {
+  return guard(st, [&] {
+    if (front < 0 || front >= (int)t->t.nodes.size())
+      throw SolverFailure(1, -1, -1, "sep clusters: front out of range");
+    ClusterTree c;
+    c.nodes.resize(nnodes);
+    for (int i = 0; i < nnodes; i++) c.nodes[i] = {begin[i], end[i], child0[i], child1[i], -1};
+    for (int i = 0; i < nnodes; i++) {
+      if (child0[i] >= i || child1[i] >= i || (child0[i] < 0) != (child1[i] < 0))
+        throw SolverFailure(1, -1, -1, "sep clusters: not a postorder binary tree");
+      if (child0[i] >= 0) c.nodes[child0[i]].parent = c.nodes[child1[i]].parent = i;
+    }
+    t->t.nodes[front].sep_clusters = std::move(c);
+  });
+}
+
 void hssmf_tree_info(const hssmf_tree* t, int* n, int* nnodes, long long* upd_total) {
   *n = t->t.n;
   *nnodes = (int)t->t.nodes.size();

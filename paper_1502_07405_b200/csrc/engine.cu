@@ -610,7 +610,7 @@ namespace hssmf_b200 {
     HssResult res;
     const auto& fn = t.nodes[i];
     const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
-    auto tree = front_cluster_tree(ns, nu, opt.leaf);
+    auto tree = front_cluster_tree(fn, opt.leaf);
     std::vector<long long> seeds(m);
     for (int l = 0; l < m; l++) seeds[l] = l < ns ? fn.sep_begin + l : fn.upd[l - ns];
     HssOpts ho;

@@ -43,10 +43,24 @@ namespace hssmf_b200 {
   // first-order upwind with the reference's upwind rule (grid_problems.hpp:57-61)
   Csr convdiff3d_const(int k, double scale, Geometry& g);
 
+  struct Cluster {
+    int begin = 0, end = 0, child0 = -1, child1 = -1, parent = -1;
+    bool leaf() const { return child0 < 0; }
+    int size() const { return end - begin; }
+  };
+  struct ClusterTree {
+    std::vector<Cluster> nodes;  // postorder, root last
+    int root() const { return (int)nodes.size() - 1; }
+    static ClusterTree balanced(int n, int leaf);
+    static ClusterTree join(const ClusterTree& a, const ClusterTree& b);
+  };
   struct FrontNode {
     int sep_begin = 0, sep_end = 0;
     int child0 = -1, child1 = -1, parent = -1, level = 0;
     std::vector<int> upd;
+    // HSS clusters of the separator from separator reordering
+    // (FrontNode::sep_clusters, elimination_tree.hpp:20); empty = balanced
+    ClusterTree sep_clusters;
     int ns() const { return sep_end - sep_begin; }
     int nu() const { return (int)upd.size(); }
     int m() const { return ns() + nu(); }
@@ -64,18 +78,34 @@ namespace hssmf_b200 {
   Etree nested_dissection_geometric(const Geometry& g, int leaf, std::vector<int>& perm);
   void symbolic_factorization(const Csr& a, Etree& t);
 
-  struct Cluster {
-    int begin = 0, end = 0, child0 = -1, child1 = -1, parent = -1;
-    bool leaf() const { return child0 < 0; }
-    int size() const { return end - begin; }
-  };
-  struct ClusterTree {
-    std::vector<Cluster> nodes;  // postorder, root last
-    int root() const { return (int)nodes.size() - 1; }
-    static ClusterTree balanced(int n, int leaf);
-    static ClusterTree join(const ClusterTree& a, const ClusterTree& b);
-  };
-  // front_cluster_tree (multifrontal.hpp:318-326) without separator clusters
+  // front_cluster_tree (multifrontal.hpp:318-326): balanced separator
+  // clusters, or the front's own when they cover the separator exactly
   ClusterTree front_cluster_tree(int ns, int nu, int leaf);
+  ClusterTree front_cluster_tree(const FrontNode& f, int leaf);
+
+  // ---- graph ordering and separator reordering (ordering.cpp:47-119,
+  // 171-236; separator_reorder.cpp:10-135), integer outputs bit-exact ----
+  struct Bisection {
+    std::vector<int> part0, part1, sep;
+  };
+  // level-set bisection of the vertex subset verts; level is scratch of size
+  // >= n holding -2 everywhere (restored on return)
+  Bisection level_set_bisection(const std::vector<int>& verts, const int* gptr,
+                                const int* gind, std::vector<int>& level, bool extract_sep);
+  // nested dissection of a symmetric adjacency (no diagonal); perm[old] = new;
+  // nodes carry separators only (upd empty)
+  Etree nested_dissection_graph(int n, const std::vector<int>& gptr,
+                                const std::vector<int>& gind, int leaf, std::vector<int>& perm);
+  void separator_enriched_graph(const std::vector<int>& sep_verts, int n,
+                                const std::vector<int>& gptr, const std::vector<int>& gind,
+                                std::vector<int>& sptr, std::vector<int>& sind);
+  ClusterTree reorder_separator(const std::vector<int>& sep_verts, int n,
+                                const std::vector<int>& gptr, const std::vector<int>& gind,
+                                int b, std::vector<int>& new_to_old);
+  // relabels the separators of the selected fronts (sep_clusters set);
+  // returns perm[old] = new on the current numbering
+  std::vector<int> reorder_tree_separators(Etree& t, const std::vector<char>& selected,
+                                           const std::vector<int>& gptr,
+                                           const std::vector<int>& gind, int b);
 
 }  // namespace hssmf_b200
