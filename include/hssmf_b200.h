@@ -34,7 +34,8 @@ typedef enum {
   HSSMF_ERR_NCCL = 5,
   HSSMF_ERR_RANK = 6,
   HSSMF_ERR_OTHER = 7,
-  HSSMF_ERR_DIVERGENCE = 8  /* KrylovDivergenceError (krylov.hpp) */
+  HSSMF_ERR_DIVERGENCE = 8, /* KrylovDivergenceError (krylov.hpp) */
+  HSSMF_ERR_STRUCTURAL = 9   /* StructuralSingularError (errors.hpp:32-35) */
 } hssmf_code;
 
 typedef struct {
@@ -81,6 +82,19 @@ void hssmf_csr_get(const hssmf_csr* a, int* ptr, int* ind, double* val);
 /* y = A x (SparseMatrix::matvec N, sparse_matrix.hpp:70-86), deterministic row order */
 void hssmf_csr_matvec(const hssmf_csr* a, const double* x, double* y);
 void hssmf_csr_free(hssmf_csr* a);
+
+/* read_matrix_market (matrix_market.cpp:10-65): coordinate real|integer,
+ * general|symmetric (lower triangle mirrored), duplicates summed as in
+ * SparseMatrix::from_triplets; malformed input -> HSSMF_ERR_SHAPE (IoError) */
+int hssmf_csr_read_mm(const char* path, hssmf_csr** out, hssmf_status* st);
+/* write_matrix_market (matrix_market.cpp:67-77): general, %.17g values */
+int hssmf_csr_write_mm(const hssmf_csr* a, const char* path, hssmf_status* st);
+/* equilibrate_and_permute (scaling.hpp:40-139): *out = Dr A Dc Qc with the
+ * ScalingState dr, dc (n doubles each), qc (n ints) and the sweep count;
+ * structurally singular input -> HSSMF_ERR_STRUCTURAL. A x = b is solved as
+ * (*out) xs = Dr b, x[qc[j]] = dc[qc[j]] xs[j]. */
+int hssmf_equilibrate(const hssmf_csr* a, hssmf_csr** out, double* dr, double* dc, int* qc,
+                      int* sweeps, hssmf_status* st);
 
 /* nested_dissection_geometric (ordering.cpp:213-222) followed by
  * EliminationTree::from_separators (elimination_tree.cpp:10-26); perm[old]=new */

@@ -61,6 +61,10 @@ def lib():
                                          _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
         "ref_ordered_graph": (vp, [C.c_int, _i32p, _i32p, _f64c, C.c_int, C.c_int, vp]),
         "ref_ordered_sep_clusters": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp]),
+        "ref_equilibrate": (C.c_int, [C.c_int, _i32p, _i32p, _f64c, _i32p, _f64c, _f64c, _f64c,
+                                      _i32p, C.POINTER(C.c_int)]),
+        "ref_read_mm": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_longlong), vp,
+                                  vp, vp]),
         "ref_ordered_free": (None, [vp]),
         "ref_ordered_n": (C.c_int, [vp]),
         "ref_ordered_nnz": (C.c_longlong, [vp]),
@@ -180,6 +184,39 @@ def ordered_csr_geom(ptr, ind, val, dims, ndims, nd_leaf) -> Ordered:
     return Ordered(lib().ref_ordered_csr_geom(
         n, np.ascontiguousarray(ptr, np.int32), np.ascontiguousarray(ind, np.int32),
         np.ascontiguousarray(val, np.float64), dims[0], dims[1], dims[2], ndims, nd_leaf))
+
+
+def equilibrate(ptr, ind, val):
+    """reference equilibrate_and_permute: (ind, val, dr, dc, qc, sweeps) or
+    raises RefError(9) when structurally singular"""
+    n = len(ptr) - 1
+    ptr = np.ascontiguousarray(ptr, np.int32)
+    oi = np.zeros(len(ind), np.int32)
+    ov = np.zeros(len(ind), np.float64)
+    dr, dc = np.zeros(n), np.zeros(n)
+    qc = np.zeros(n, np.int32)
+    sw = C.c_int()
+    rc = lib().ref_equilibrate(n, ptr, np.ascontiguousarray(ind, np.int32),
+                               np.ascontiguousarray(val, np.float64), oi, ov, dr, dc, qc,
+                               C.byref(sw))
+    if rc:
+        raise RefError(rc, -1, -1, lib().ref_last_error().decode())
+    return oi, ov, dr, dc, qc, sw.value
+
+
+def read_mm(path):
+    """reference read_matrix_market: (ptr, ind, val) or raises RefError(1)"""
+    L = lib()
+    n, nnz = C.c_int(), C.c_longlong()
+    rc = L.ref_read_mm(os.fsencode(path), C.byref(n), C.byref(nnz), None, None, None)
+    if rc:
+        raise RefError(rc, -1, -1, L.ref_last_error().decode())
+    ptr = np.zeros(n.value + 1, np.int32)
+    ind = np.zeros(nnz.value, np.int32)
+    val = np.zeros(nnz.value, np.float64)
+    L.ref_read_mm(os.fsencode(path), C.byref(n), C.byref(nnz), ptr.ctypes.data_as(C.c_void_p),
+                  ind.ctypes.data_as(C.c_void_p), val.ctypes.data_as(C.c_void_p))
+    return ptr, ind, val
 
 
 def ordered_graph(ptr, ind, val, nd_leaf, reorder_b=0, selected=None) -> Ordered:

@@ -67,6 +67,8 @@ namespace hssmf {
 #include "hssmf/random_sampler.hpp"
 #include "hssmf/rrqr.hpp"
 #include "hssmf/separator_reorder.hpp"
+#include "hssmf/matrix_market.hpp"
+#include "hssmf/scaling.hpp"
 #include "hssmf/lu.hpp"
 #include "hssmf/solver_options.hpp"
 #include "hssmf/sparse_matrix.hpp"
@@ -254,6 +256,47 @@ int ref_ordered_sep_clusters(void* h, int front, int* begin, int* end, int* c0, 
     if (parent) parent[i] = x.parent;
   }
   return c.size();
+}
+
+// equilibrate_and_permute (scaling.hpp:40-139); the output keeps a's row
+// pointers. returns 0, or 9 when structurally singular (message in
+// ref_last_error)
+int ref_equilibrate(int n, const int* ptr, const int* ind, const double* val, int* oind,
+                    double* oval, double* dr, double* dc, int* qc, int* sweeps) {
+  auto a = csr_copy(n, ptr, ind, val);
+  ScalingState<double> st;
+  try {
+    auto s = equilibrate_and_permute(a, st);
+    std::copy(s.ind().begin(), s.ind().end(), oind);
+    std::copy(s.val().begin(), s.val().end(), oval);
+  } catch (const StructuralSingularError& e) {
+    g_err = e.what();
+    return 9;
+  }
+  std::copy(st.dr.begin(), st.dr.end(), dr);
+  std::copy(st.dc.begin(), st.dc.end(), dc);
+  std::copy(st.qc.begin(), st.qc.end(), qc);
+  *sweeps = st.sweeps;
+  return 0;
+}
+
+// read_matrix_market (matrix_market.cpp:10-65): sizes when ptr is NULL;
+// returns 0, or 1 on IoError
+int ref_read_mm(const char* path, int* n, long long* nnz, int* ptr, int* ind, double* val) {
+  try {
+    auto a = read_matrix_market(path);
+    *n = a.size();
+    *nnz = a.nnz();
+    if (ptr) {
+      std::copy(a.ptr().begin(), a.ptr().end(), ptr);
+      std::copy(a.ind().begin(), a.ind().end(), ind);
+      std::copy(a.val().begin(), a.val().end(), val);
+    }
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 1;
+  }
+  return 0;
 }
 
 void ref_ordered_free(void* h) { delete static_cast<Ordered*>(h); }

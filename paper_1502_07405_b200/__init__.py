@@ -10,5 +10,6 @@ from .api import (  # noqa: F401
     generate_convdiff3d, generate_grid_problem, gmres, hss_compress, iterative_refinement,
     mf_factor, mf_solve, mf_solve_new, nested_dissection_geometric, ordered_grid,
     ordered_problem, symbolic_factorization, nested_dissection_graph, reorder_tree_separators,
-    ordered_graph,
+    ordered_graph, read_matrix_market, write_matrix_market, equilibrate_and_permute,
+    ScalingState, StructuralSingularError,
 )

@@ -59,6 +59,10 @@ _SIGS = {
                                C.POINTER(C.c_longlong)]),
     "hssmf_tree_get": (None, [vp, i32p, i32p, i32p, i32p, i32p, i32p, i32p, i32p]),
     "hssmf_tree_free": (None, [vp]),
+    "hssmf_csr_read_mm": (C.c_int, [C.c_char_p, C.POINTER(vp), C.POINTER(Status)]),
+    "hssmf_csr_write_mm": (C.c_int, [vp, C.c_char_p, C.POINTER(Status)]),
+    "hssmf_equilibrate": (C.c_int, [vp, C.POINTER(vp), vp, vp, vp, C.POINTER(C.c_int),
+                                    C.POINTER(Status)]),
     "hssmf_nd_graph": (C.c_int, [vp, C.c_int, i32p, C.POINTER(vp), C.POINTER(Status)]),
     "hssmf_reorder_separators": (C.c_int, [vp, vp, vp, C.c_int, i32p, C.POINTER(Status)]),
     "hssmf_tree_sep_clusters": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp]),

@@ -10,6 +10,7 @@ numerics run in sm_100a kernels. There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -42,6 +43,10 @@ class HssRankExceeded(SolverError):
     pass
 
 
+class StructuralSingularError(SolverError):
+    """errors.hpp:32-35"""
+
+
 class KrylovDivergenceError(SolverError):
     pass
 
@@ -66,6 +71,8 @@ def _check(rc, st: N.Status):
         raise HssRankExceeded(msg)
     if rc == 8:
         raise KrylovDivergenceError(msg)
+    if rc == 9:
+        raise StructuralSingularError(msg)
     raise SolverError(msg)
 
 
@@ -161,6 +168,52 @@ def generate_convdiff3d(k: int, scale: float = 0.1) -> GridProblem:
     h = C.c_void_p()
     _call("hssmf_csr_convdiff3d", int(k), float(scale), C.byref(h))
     return GridProblem(SparseMatrix(h), GridGeometry((k, k, k), 3), "cd3d", k, scale)
+
+
+# ---- Matrix Market I/O and equilibration (matrix_market.cpp, scaling.hpp) ----
+def read_matrix_market(path) -> SparseMatrix:
+    """matrix_market.cpp:10-65"""
+    h = C.c_void_p()
+    _call("hssmf_csr_read_mm", os.fsencode(path), C.byref(h))
+    return SparseMatrix(h)
+
+
+def write_matrix_market(a: SparseMatrix, path):
+    """matrix_market.cpp:67-77"""
+    _call("hssmf_csr_write_mm", a._h, os.fsencode(path))
+
+
+@dataclass
+class ScalingState:
+    """scaling.hpp:15-32: As = Dr A Dc Qc"""
+    dr: np.ndarray
+    dc: np.ndarray
+    qc: np.ndarray
+    sweeps: int
+
+    def apply_scaling(self, b):
+        """b -> Dr b"""
+        b = np.asarray(b, np.float64)
+        return b * (self.dr if b.ndim == 1 else self.dr[:, None])
+
+    def undo_scaling(self, xs):
+        """xs -> x with x[qc[j]] = dc[qc[j]] xs[j]"""
+        xs = np.asarray(xs, np.float64)
+        x = np.empty_like(xs)
+        x[self.qc] = (self.dc[self.qc] * xs) if xs.ndim == 1 else self.dc[self.qc][:, None] * xs
+        return x
+
+
+def equilibrate_and_permute(a: SparseMatrix):
+    """scaling.hpp:40-139; returns (As, ScalingState)"""
+    n = a.size()
+    dr, dc = np.zeros(n), np.zeros(n)
+    qc = np.zeros(n, np.int32)
+    sw = C.c_int()
+    h = C.c_void_p()
+    _call("hssmf_equilibrate", a._h, C.byref(h), dr.ctypes.data_as(C.c_void_p),
+          dc.ctypes.data_as(C.c_void_p), qc.ctypes.data_as(C.c_void_p), C.byref(sw))
+    return SparseMatrix(h), ScalingState(dr, dc, qc, sw.value)
 
 
 # ---- elimination tree (elimination_tree.hpp) --------------------------------

@@ -249,6 +249,41 @@ int hssmf_symbolic(const hssmf_csr* a, hssmf_tree* t, hssmf_status* st) {
   });
 }
 
+int hssmf_csr_read_mm(const char* path, hssmf_csr** out, hssmf_status* st) {
+  return guard(st, [&] {
+    auto* c = new hssmf_csr;
+    try {
+      c->a = read_matrix_market(path);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int hssmf_csr_write_mm(const hssmf_csr* a, const char* path, hssmf_status* st) {
+  return guard(st, [&] { write_matrix_market(a->a, path); });
+}
+
+int hssmf_equilibrate(const hssmf_csr* a, hssmf_csr** out, double* dr, double* dc, int* qc,
+                      int* sweeps, hssmf_status* st) {
+  return guard(st, [&] {
+    Scaling sc;
+    Csr s = equilibrate_and_permute(a->a, sc);
+    auto* c = new hssmf_csr;
+    c->a = std::move(s);
+    const size_t n = (size_t)a->a.n;
+    if (n) {
+      std::memcpy(dr, sc.dr.data(), n * sizeof(double));
+      std::memcpy(dc, sc.dc.data(), n * sizeof(double));
+      std::memcpy(qc, sc.qc.data(), n * sizeof(int));
+    }
+    *sweeps = sc.sweeps;
+    *out = c;
+  });
+}
+
 int hssmf_nd_graph(const hssmf_csr* a, int leaf, int* perm, hssmf_tree** out, hssmf_status* st) {
   return guard(st, [&] {
     std::vector<int> gptr, gind, p;

@@ -35,11 +35,7 @@ namespace hssmf_b200 {
     long long flops = 0;
   };
 
-  struct SolverFailure : std::runtime_error {
-    int code, front, column;
-    SolverFailure(int c, int f, int col, const std::string& m)
-        : std::runtime_error(m), code(c), front(f), column(col) {}
-  };
+
 
   // per-kernel-class device time + algorithmic work, for the roofline
   struct KernelStat {

@@ -13,10 +13,20 @@
 
 #include <array>
 #include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <tuple>
 #include <vector>
 
 namespace hssmf_b200 {
 
+  // error with a C-ABI status code (include/hssmf_b200.h), the failing front
+  // and column where they apply
+  struct SolverFailure : std::runtime_error {
+    int code, front, column;
+    SolverFailure(int c, int f, int col, const std::string& m)
+        : std::runtime_error(m), code(c), front(f), column(col) {}
+  };
   // square CSR, sorted duplicate-free rows (sparse_matrix.hpp:14-47)
   struct Csr {
     int n = 0;
@@ -26,9 +36,29 @@ namespace hssmf_b200 {
     double get(int i, int j) const;
     // symmetric permutation B[p[i]][p[j]] = A[i][j]
     Csr permuted(const std::vector<int>& p) const;
+    // column permutation B[i][j] = A[i][q[j]] (sparse_matrix.hpp:104-124)
+    Csr col_permuted(const std::vector<int>& q) const;
     // structurally symmetrized adjacency without the diagonal
     void symmetric_graph(std::vector<int>& gptr, std::vector<int>& gind) const;
   };
+
+  // SparseMatrix::from_triplets (sparse_matrix.hpp:25-47): rows sorted,
+  // duplicates summed; t is sorted in place
+  Csr csr_from_triplets(int n, std::vector<std::tuple<int, int, double>>& t);
+
+  // ScalingState (scaling.hpp:15-32): As = Dr A Dc Qc; xs[j] = x[qc[j]] / dc[qc[j]]
+  struct Scaling {
+    std::vector<double> dr, dc;
+    std::vector<int> qc;
+    int sweeps = 0;
+  };
+  // equilibrate_and_permute (scaling.hpp:40-139); throws code 9 (structurally
+  // singular) on an empty row / column or when no zero-free diagonal exists
+  Csr equilibrate_and_permute(const Csr& a, Scaling& sc);
+  // read_matrix_market / write_matrix_market (matrix_market.cpp:10-77):
+  // coordinate real|integer, general|symmetric; errors are code 1 (IoError)
+  Csr read_matrix_market(const std::string& path);
+  void write_matrix_market(const Csr& a, const std::string& path);
 
   struct Geometry {
     std::array<int, 3> dims{1, 1, 1};

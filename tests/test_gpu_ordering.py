@@ -80,3 +80,49 @@ def test_reordered_separator_hss_matches_reference(oracle, k, b_sep, eps):
         assert len(u) == len(ru)
         assert close(u, ru, slack=10)
     assert res <= 10 * rres
+
+
+@pytest.mark.parametrize("hss", [False, True])
+def test_matrix_market_equilibrated_pipeline_matches_reference(oracle, tmp_path, hss):
+    # general nonsymmetric input end to end: Matrix Market file -> equilibration
+    # and static pivoting -> graph ND (+ separator reordering) -> factor/solve
+    # on the device -> unscaled solution; the reference runs the identical
+    # pipeline on its own host code
+    a0 = P.generate_convdiff3d(16, 0.1).A
+    ptr, ind, val = a0.arrays()
+    rng = np.random.default_rng(11)
+    rs = 10.0 ** rng.uniform(-3, 3, a0.size())
+    val = val * rs[np.repeat(np.arange(a0.size()), np.diff(ptr))]
+    path = str(tmp_path / "cd16.mtx")
+    P.write_matrix_market(P.SparseMatrix.from_csr(a0.size(), ptr, ind, val), path)
+    a = P.read_matrix_market(path)
+    s, st = P.equilibrate_and_permute(a)
+    op = P.ordered_graph(s, 16, reorder_b=32 if hss else 0)
+    xt = x_true(a.size(), 3)
+    b = a.matvec(xt)
+    bs = st.apply_scaling(b)[np.argsort(op.perm)]  # into tree order
+    so = dict(ls=64, min_hss=200, eps=1e-8, leaf=32) if hss else dict(mode="mf")
+    m = P.mf_factor(op.a, op.t, P.SolverOptions(nd_leaf=16, **so))
+    xs = P.mf_solve_new(m, bs)[op.perm]
+    x = st.undo_scaling(xs)
+    # reference pipeline on the same file
+    rptr, rind, rval = oracle.read_mm(path)
+    oi, ov, dr, dc, qc, sw = oracle.equilibrate(rptr, rind, rval)
+    assert np.array_equal(qc, st.qc) and dr.tobytes() == st.dr.tobytes()
+    o = oracle.ordered_graph(rptr, oi, ov, 16, reorder_b=32 if hss else 0)
+    assert np.array_equal(o.perm, op.perm)
+    if hss:
+        F = oracle.Factors(o, eps=1e-8, ls=64, min_hss=200, leaf=32)
+        assert (F.type == 1).sum() > 0 and np.array_equal(F.type, m.type)
+    else:
+        F = oracle.Factors(o, mode=1)
+    xr = st.undo_scaling(F.solve(np.asfortranarray(bs))[:, 0][op.perm])
+    if hss:
+        res = np.linalg.norm(a.matvec(x) - b) / np.linalg.norm(b)
+        rres = np.linalg.norm(a.matvec(xr) - b) / np.linalg.norm(b)
+        assert res <= 10 * max(rres, 1e-15)
+        hs = np.nonzero(F.type == 1)[0]
+        assert close(m.rank[hs], F.rank[hs])
+    else:
+        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-10
+        assert np.linalg.norm(x - xt) / np.linalg.norm(xt) <= 1e-8
