@@ -169,6 +169,27 @@ namespace hssmf_b200 {
       hssmf_csr_free(c);
       detail::raise(rc, st);
     }
+    // separator clusters from the reference's reorder_tree_separators
+    // (FrontNode::sep_clusters) travel with the tree
+    for (int i = 0; i < nn && rc == HSSMF_OK; i++) {
+      const auto& sc = t.nodes[i].sep_clusters;
+      if (sc.empty()) continue;
+      const int cn = sc.size();
+      std::vector<int> cb(cn), ce(cn), cc0(cn), cc1(cn);
+      for (int k = 0; k < cn; k++) {
+        cb[k] = sc.node(k).begin;
+        ce[k] = sc.node(k).end;
+        cc0[k] = sc.node(k).child0;
+        cc1[k] = sc.node(k).child1;
+      }
+      rc = hssmf_tree_set_sep_clusters(tr, i, cn, cb.data(), ce.data(), cc0.data(), cc1.data(),
+                                       &st);
+    }
+    if (rc != HSSMF_OK) {
+      hssmf_tree_free(tr);
+      hssmf_csr_free(c);
+      detail::raise(rc, st);
+    }
     hssmf_options o{opts.ls, opts.eps, opts.leaf, opts.d0, opts.dd, opts.p, opts.min_hss,
                     opts.max_rank, static_cast<int>(opts.mode)};
     hssmf_factors* h = nullptr;

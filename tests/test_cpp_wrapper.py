@@ -30,3 +30,6 @@ def test_wrapper_drop_in_factor_solve():
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["relres"] < 1e-12 and d["singular_col"] == 1 and d["front0"] == 1
     assert d["gmres_converged"] == 1 and d["gmres_iterations"] <= 2
+    # reordered separators forwarded through the drop-in: HSS ranks within
+    # +-10% of the reference's own mf_factor on the same tree
+    assert d["reorder_hss_fronts"] > 0 and d["reorder_ranks_close"] == 1
