@@ -211,6 +211,52 @@ namespace hssmf_b200 {
       std::string msg, error;
     };
     std::vector<cudaStream_t> hstreams;  // concurrent HSS fronts of one level
+    // solves: the HSS fronts of one tree level sweep concurrently on the
+    // worker streams (forked from / joined back into the engine stream)
+    std::vector<cudaStream_t> solve_st;
+    cudaEvent_t solve_fork = nullptr;
+    std::vector<cudaEvent_t> solve_join;
+    cudaStream_t solve_stream_of(int i) const { return solve_st[i]; }
+    template <class F>
+    void hss_level_concurrent(const std::vector<int>& lst, cudaStream_t main, F&& f) {
+      std::vector<int> L;
+      for (int i : lst)
+        if (i < (int)hss.size() && hss[i]) L.push_back(i);
+      if (L.empty()) return;
+      if (solve_st.size() != t.nodes.size()) solve_st.assign(t.nodes.size(), main);
+      const int nw = (int)std::min(L.size(), hstreams.size());
+      if (nw <= 1) {
+        for (int i : L) {
+          solve_st[i] = main;
+          hss[i]->set_solve_stream(main);
+          f(i);
+        }
+        return;
+      }
+      if (!solve_fork) HSSMF_CUDA(cudaEventCreateWithFlags(&solve_fork, cudaEventDisableTiming));
+      while ((int)solve_join.size() < nw) {
+        cudaEvent_t e;
+        HSSMF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        solve_join.push_back(e);
+      }
+      HSSMF_CUDA(cudaEventRecord(solve_fork, main));
+      for (int w = 0; w < nw; w++) HSSMF_CUDA(cudaStreamWaitEvent(hstreams[w], solve_fork, 0));
+      for (size_t q = 0; q < L.size(); q++) {
+        const int i = L[q];
+        cudaStream_t ws = hstreams[q % nw];
+        solve_st[i] = ws;
+        hss[i]->set_solve_stream(ws);
+        f(i);
+      }
+      for (int w = 0; w < nw; w++) {
+        HSSMF_CUDA(cudaEventRecord(solve_join[w], hstreams[w]));
+        HSSMF_CUDA(cudaStreamWaitEvent(main, solve_join[w], 0));
+      }
+      for (int i : L) {
+        solve_st[i] = main;
+        hss[i]->set_solve_stream(main);
+      }
+    }
     double* assemble_hss_front(int i, cudaStream_t st);
     void assemble_on(int i, const FrontDev& view, cudaStream_t st);
     void upload_front_on(int i, cudaStream_t st) {
@@ -1317,10 +1363,15 @@ namespace hssmf_b200 {
     if (nrhs <= 0) return;
     D.profile = profile_;
     if (nrhs > D.bupd_nr) D.set_bupd_capacity(nrhs);
-    int max_nu = 0;
-    for (const auto& f : D.t.nodes) max_nu = std::max(max_nu, f.nu());
-    if (D.x2buf.bytes < (size_t)max_nu * sizeof(double) + 8)
-      D.x2buf.alloc((size_t)max_nu * sizeof(double) + 8);
+    size_t max_nu = 0;
+    for (const auto& P : D.levels) {
+      size_t sum = 0;
+      for (int i : P.hss) sum += D.t.nodes[i].nu();
+      max_nu = std::max(max_nu, sum);
+    }
+    for (const auto& f : D.t.nodes) max_nu = std::max(max_nu, (size_t)f.nu());
+    if (D.x2buf.bytes < max_nu * sizeof(double) + 8)
+      D.x2buf.alloc(max_nu * sizeof(double) + 8);
     const FrontDev* F = D.d_fronts.as<FrontDev>();
     const int nlev = (int)D.levels.size();
     lo = std::max(lo, 0);
@@ -1343,15 +1394,14 @@ namespace hssmf_b200 {
             DenseKernels::fwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
             DenseKernels::fwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_nu, stream_);
           }
-          for (int i : P.hss) {
-            if (!D.hss[i]) continue;
+          D.hss_level_concurrent(P.hss, stream_, [&](int i) {
             const auto& h = D.hf[i];
             for (int r = 0; r < nrhs; r++) {
               double* xr = x + (size_t)r * ldx + h.sep_begin;
               if (h.nu) D.hss[i]->partial_forward(xr, h.bupd + (size_t)r * h.nu);
               else D.hss[i]->solve_full(xr);
             }
-          }
+          });
         });
       }
     } else {
@@ -1364,18 +1414,25 @@ namespace hssmf_b200 {
             DenseKernels::bwd_gemv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
             DenseKernels::bwd_trsv(F, sids, P.nsf, x, ldx, nrhs, P.max_ns, stream_);
           }
+          // x(upd) of every front of the level into its own slice of x2buf
+          std::vector<size_t> x2off(D.t.nodes.size(), 0);
+          size_t o2 = 0;
           for (int i : P.hss) {
-            if (!D.hss[i]) continue;
+            x2off[i] = o2;
+            o2 += D.t.nodes[i].nu();
+          }
+          D.hss_level_concurrent(P.hss, stream_, [&](int i) {
             const auto& h = D.hf[i];
-            if (!h.nu) continue;
+            if (!h.nu) return;
+            double* x2 = D.x2buf.as<double>() + x2off[i];
             for (int r = 0; r < nrhs; r++) {
               double* xr = x + (size_t)r * ldx;
-              CopyDesc g{xr, 1, 0, h.upd, nullptr, 0, 0, D.x2buf.as<double>(), h.nu, nullptr,
+              CopyDesc g{xr, 1, 0, h.upd, nullptr, 0, 0, x2, h.nu, nullptr,
                          nullptr, 0, 0, h.nu, 1, 1.0, 0, 0};
-              index_copy_run({g}, stream_);
-              D.hss[i]->partial_backward(xr + h.sep_begin, D.x2buf.as<double>());
+              index_copy_run({g}, D.solve_stream_of(i));
+              D.hss[i]->partial_backward(xr + h.sep_begin, x2);
             }
-          }
+          });
         });
       }
     }

@@ -224,6 +224,7 @@ namespace hssmf_b200 {
     DevArena arena;       // scratch blocks; first members: outlive every buffer below
     DevArena keep_arena;  // factor data
     cudaStream_t s;
+    cudaStream_t owner = nullptr;  // the arenas' stream once factored (set_stream)
     ClusterTree tree;
     int m = 0;
     const double* A = nullptr;
@@ -1429,11 +1430,23 @@ namespace hssmf_b200 {
   }
   void HssMatrixDev::set_stream(cudaStream_t s) {
     d_->collect_phases();
+    d_->owner = s;
     d_->arena.set_meter(nullptr);  // the compression is over: detach from the admission meter
     d_->keep_arena.set_meter(nullptr);
     d_->arena.rebind(s);
     d_->keep_arena.rebind(s);
     d_->s = s;
+  }
+  void HssMatrixDev::set_solve_stream(cudaStream_t w) {
+    if (!d_->owner) d_->owner = d_->s;
+    if (!d_->sbuf.p) {
+      cudaStream_t cur = d_->s;
+      d_->s = d_->owner;
+      ArenaScope as(&d_->arena, &d_->keep_arena);
+      d_->alloc_solve_scratch();
+      d_->s = cur;
+    }
+    d_->s = w;
   }
   void HssMatrixDev::solve_full(double* x) {
     StagingScope sc(staging_for(d_->s));

@@ -87,6 +87,10 @@ namespace hssmf_b200 {
     void drop_dense();
     // stream used by later solves (factorization ran on its own stream)
     void set_stream(cudaStream_t s);
+    // stream of the next solves only (no arena move; the solve scratch is
+    // allocated on the owning stream first): lets the fronts of one tree level
+    // run their ULV sweeps concurrently
+    void set_solve_stream(cudaStream_t s);
 
     // solves (single right-hand side, device vectors)
     void solve_full(double* x);  // in place, length m

@@ -73,6 +73,7 @@ namespace hssmf_b200 {
     const double* xkeep;
     double* out0;       // first n0 entries of x_local
     double* out1;       // remaining entries
+    double* scr;        // level scratch of the batched steps (set by the launcher)
   };
   void ulv_fwd_level(const std::vector<UlvSolveNode>& nodes, int nrhs_ld_unused, cudaStream_t s);
   void ulv_bwd_level(const std::vector<UlvSolveNode>& nodes, cudaStream_t s);
