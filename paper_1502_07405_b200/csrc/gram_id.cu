@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "gemm.cuh"
 #include "staging.cuh"
@@ -564,6 +565,89 @@ namespace hssmf_b200 {
           if (16 * a < im && b < jm && i0 + tx + 16 * a >= j0 + ty * 4 + b)
             G[16 * a + (size_t)b * n] = c[a][b] - acc[a][b];
     }
+
+    // the same trailing update on the FP64 tensor pipe (DMMA m8n8k4): 64 x 64
+    // lower tiles, 8 warps of 32 x 16, operands staged by cp.async into
+    // padded shared tiles (stride 68: a warp's fragment loads hit every bank
+    // pair exactly twice), the tile's G entries loaded into registers before
+    // the products. Two shared loads feed 256 FMAs instead of 32.
+    template <int NB>
+    __global__ void __launch_bounds__(256, 2)
+    gram_syrk_dmma_kernel(const GramTask* __restrict__ tasks, int k0,
+                          unsigned long long* probe_bytes) {
+      constexpr int SP = 68;
+      const GramTask Tk = tasks[blockIdx.y];
+      const int n = Tk.n;
+      const int nbt = (n + 63) >> 6;
+      const int t = blockIdx.x;
+      if (t >= nbt * (nbt + 1) / 2) return;
+      if (__ldcg(Tk.state + 1)) return;
+      if (probe_bytes && t == 0 && threadIdx.x == 0)
+        atomicAdd(probe_bytes, (unsigned long long)n * (n + 1) / 2 * 16ull);
+      // column-major order of the lower tiles: CTAs running together sweep
+      // long contiguous column strips of G (DRAM page locality)
+      auto before = [&](int c) { return c * nbt - c * (c - 1) / 2; };
+      const double bb = 2.0 * nbt + 1.0;
+      int tj = (int)((bb - sqrt(fmax(bb * bb - 8.0 * t, 0.0))) * 0.5);
+      tj = max(0, min(tj, nbt - 1));
+      while (tj > 0 && before(tj) > t) tj--;
+      while (tj + 1 < nbt && before(tj + 1) <= t) tj++;
+      const int ti = tj + (t - before(tj));
+      const int i0 = ti * 64, j0 = tj * 64;
+      extern __shared__ __align__(16) double sm5[];
+      double* As = sm5;            // [NB][SP]: As[q][r] = L(i0 + r, k0 + q)
+      double* Bs = sm5 + NB * SP;  // [NB][SP]: Bs[q][r] = L(j0 + r, k0 + q)
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      const double* Lk = Tk.L + (size_t)k0 * n;
+      for (int e = tid; e < NB * 64; e += 256) {
+        const int q = e >> 6, r = e & 63;
+        const bool va = i0 + r < n, vb = j0 + r < n;
+        cp_async8(As + q * SP + r, va ? Lk + i0 + r + (size_t)q * n : Lk, va);
+        cp_async8(Bs + q * SP + r, vb ? Lk + j0 + r + (size_t)q * n : Lk, vb);
+      }
+      cp_async_commit();
+      const int wm = warp & 1, wn = warp >> 1;  // warp tile rows 32 wm, cols 16 wn
+      const int lr = lane >> 2, lc = lane & 3;
+      double* G = Tk.G;
+      double c[4][2][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            const int i = i0 + 32 * wm + 8 * mi + lr, j = j0 + 16 * wn + 8 * ni + 2 * lc + v;
+            c[mi][ni][v] = (i < n && j < n && i >= j) ? G[i + (size_t)j * n] : 0.0;
+          }
+      cp_async_wait<0>();
+      __syncthreads();
+      double acc[4][2][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NB; kk += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++) a[mi] = As[(kk + lc) * SP + 32 * wm + 8 * mi + lr];
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) b[ni] = Bs[(kk + lc) * SP + 16 * wn + 8 * ni + lr];
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+          for (int ni = 0; ni < 2; ni++) dmma8x8x4(acc[mi][ni], a[mi], b[ni]);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            const int i = i0 + 32 * wm + 8 * mi + lr, j = j0 + 16 * wn + 8 * ni + 2 * lc + v;
+            if (i < n && j < n && i >= j) G[i + (size_t)j * n] = c[mi][ni][v] - acc[mi][ni][v];
+          }
+    }
   }  // namespace
 
   void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
@@ -628,11 +712,16 @@ namespace hssmf_b200 {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * NB2 * 8));
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 64 * 8));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_dmma_kernel<NB2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
         attr2 = true;
       }
       CL = CL2;
       nb = NB2;
     }
+    // trailing update on the FP64 tensor pipe unless HSSMF_GRAM_SYRK=fma
+    const char* esy = getenv("HSSMF_GRAM_SYRK");
+    const bool syrk_cuda_cores = esy && !strcmp(esy, "fma");
     // all panels are queued without host round trips: a finished task's
     // panel kernel returns at once and its trailing GEMM is skipped on device
     for (int k0 = 0; k0 <= kmax; k0 += nb) {
@@ -663,8 +752,13 @@ namespace hssmf_b200 {
         const int nbt = (max_n + 63) / 64;
         {
           ProbeScope prs(PROBE_GRAM_SYRK, s, 0.0, 0.0);
-          gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
-              (const GramTask*)d, k0, probe_enabled() ? probe_device_bytes() : nullptr);
+          unsigned long long* pb = probe_enabled() ? probe_device_bytes() : nullptr;
+          if (syrk_cuda_cores)
+            gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
+                (const GramTask*)d, k0, pb);
+          else
+            gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
+                (const GramTask*)d, k0, pb);
           HSSMF_LAUNCH_CHECK();
         }
         if (flops)
