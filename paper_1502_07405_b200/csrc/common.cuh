@@ -104,6 +104,7 @@ namespace hssmf_b200 {
     cudaStream_t s;
     double flops, bytes;
     cudaEvent_t a = nullptr;
+    int tiles = 0, kmax = 0, nprob = 0;  // GEMM shape summary (HSSMF_PROBE_DUMP)
     ProbeScope(int k, cudaStream_t st, double f, double b);
     ~ProbeScope();
   };

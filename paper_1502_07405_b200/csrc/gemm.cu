@@ -285,10 +285,16 @@ namespace hssmf_b200 {
       const int tiles = b.pre[b.nprob];
       if (tiles) {
         double fl = 0;
+        int km = 0;
         if (probe_enabled())
-          for (int q = 0; q < b.nprob; q++)
+          for (int q = 0; q < b.nprob; q++) {
             fl += (b.p[q].lower ? 1.0 : 2.0) * b.p[q].m * b.p[q].n * b.p[q].k;
+            km = std::max(km, b.p[q].k);
+          }
         ProbeScope pr(PROBE_GEMM, s, fl, 0.0);
+        pr.tiles = tiles;
+        pr.kmax = km;
+        pr.nprob = b.nprob;
         gemm_param_kernel<<<tiles, THREADS, SMEM, s>>>(b);
         HSSMF_LAUNCH_CHECK();
       }

@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -10,6 +12,7 @@ namespace hssmf_b200 {
       int kind;
       cudaEvent_t a, b;
       double flops, bytes;
+      int tiles, kmax, nprob;
     };
     std::mutex g_mu;
     std::vector<Rec> g_recs;
@@ -37,9 +40,16 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaDeviceSynchronize());
     std::lock_guard<std::mutex> l(g_mu);
     for (int k = 0; k < PROBE_KINDS; k++) out[k] = {0, 0.0, 0.0, 0.0};
+    // HSSMF_PROBE_DUMP=<path>: one CSV line per probed launch (shape study)
+    FILE* dump = nullptr;
+    if (const char* pth = getenv("HSSMF_PROBE_DUMP")) dump = fopen(pth, "w");
+    if (dump) fprintf(dump, "kind,ms,flops,bytes,tiles,kmax,nprob\n");
     for (auto& r : g_recs) {
       float ms = 0;
       cudaEventElapsedTime(&ms, r.a, r.b);
+      if (dump)
+        fprintf(dump, "%d,%.4f,%.6g,%.6g,%d,%d,%d\n", r.kind, ms, r.flops, r.bytes, r.tiles, r.kmax,
+                r.nprob);
       auto& o = out[r.kind];
       o.launches++;
       o.ms += ms;
@@ -49,6 +59,7 @@ namespace hssmf_b200 {
       cudaEventDestroy(r.b);
     }
     g_recs.clear();
+    if (dump) fclose(dump);
     if (g_dev_bytes) {
       unsigned long long b = 0;
       HSSMF_CUDA(cudaMemcpy(&b, g_dev_bytes, sizeof(b), cudaMemcpyDeviceToHost));
@@ -69,7 +80,7 @@ namespace hssmf_b200 {
     cudaEvent_t b;
     if (cudaEventCreate(&b) != cudaSuccess || cudaEventRecord(b, s) != cudaSuccess) return;
     std::lock_guard<std::mutex> l(g_mu);
-    g_recs.push_back({kind, a, b, flops, bytes});
+    g_recs.push_back({kind, a, b, flops, bytes, tiles, kmax, nprob});
   }
 
 }  // namespace hssmf_b200
