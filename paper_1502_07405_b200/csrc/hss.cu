@@ -5,7 +5,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <functional>
 #include <numeric>
+#include <mutex>
+#include <memory>
+#include <map>
 
 #include "common.cuh"
 #include "cpqr.cuh"
@@ -99,6 +103,18 @@ namespace hssmf_b200 {
         HSSMF_CUDA(cudaStreamWaitEvent(s, fork, 0));
       }
     };
+
+    // one persistent side stream (and its staging ring) per main stream:
+    // creating a stream per front cost milliseconds of host time, and a new
+    // stream needed a new pinned staging ring
+    SideStream& side_for(cudaStream_t main) {
+      static std::mutex mu;
+      static auto* reg = new std::map<cudaStream_t, std::unique_ptr<SideStream>>();  // never destroyed
+      std::lock_guard<std::mutex> lk(mu);
+      auto& p = (*reg)[main];
+      if (!p) p.reset(new SideStream());
+      return *p;
+    }
 
     // rows x cols matrix (ld = rows) whose column count grows by appending
     struct Grow {
@@ -353,7 +369,12 @@ namespace hssmf_b200 {
       // side stream while this round's (latency-bound) IDs run; a round that
       // ends the compression wastes one round of sampling. The samples are
       // the same seeded columns and the same GEMMs, so results are unchanged.
-      SideStream side;
+      SideStream& side = side_for(s);
+      // speculative fold of next round's columns: opt-in (HSSMF_SPEC_FOLD=1);
+      // measured neutral on c5 (13.84 s vs 13.63 s per step), the IDs, not
+      // the folds, bound the rounds
+      static const bool no_spec_fold = getenv("HSSMF_SPEC_FOLD") == nullptr;
+      pending_spec = nullptr;
       DBuf<double> scale2;
       scale2.alloc_keep(1, s);
       int spec_d = -1;
@@ -403,8 +424,32 @@ namespace hssmf_b200 {
         const int cap_id = std::min(d - o.p, o.max_rank);
         const double abs_tol = o.eps * sc;
         int fail = -1;
+        fold_done_all();
+        // next round's columns of the nodes done now are folded on the side
+        // stream while this round's IDs run (same GEMMs on the same columns,
+        // so results are unchanged; wasted when this round ends the
+        // compression). Their buffers are grown first, on the main stream.
+        if (spec_d == d + o.dd && !no_spec_fold) {
+          const int dt = spec_d;
+          auto lists = done_by_level();
+          for (auto& l : lists)
+            for (int n : l)
+              for (Grow* g : {&nodes[n].sr, &nodes[n].sc, &nodes[n].rr, &nodes[n].rc}) g->ensure(dt);
+          HSSMF_CUDA(cudaEventRecord(side.fork, s));
+          pending_spec = [this, lists = std::move(lists), dt, &side] {
+            StagingScope ss(staging_for(side.s));
+            HSSMF_CUDA(cudaStreamWaitEvent(side.s, side.fork, 0));
+            for (int lv = maxdepth; lv >= 0; lv--)
+              if (!lists[lv].empty()) update_done(lists[lv], dt, side.s);
+            HSSMF_CUDA(cudaEventRecord(side.done, side.s));
+          };
+        }
         for (int lv = maxdepth; lv >= 0; lv--) pass_level(lv, cap_id, abs_tol, fail);
-        if (nodes[root].state == DONE) break;
+        if (nodes[root].state == DONE) {
+          pending_spec = nullptr;
+          break;
+        }
+        run_pending_spec();  // no ID ran this round
         if (d - o.p >= o.max_rank) throw HssRankError(fail, o.max_rank);
         d += o.dd;
       }
@@ -437,7 +482,7 @@ namespace hssmf_b200 {
       DBuf<double> Xp;
     };
 
-    void run_basis_apply(std::vector<BasisApplyJob>& jobs) {
+    void run_basis_apply(std::vector<BasisApplyJob>& jobs, cudaStream_t st) {
       if (jobs.empty()) return;
       IdxPool pool;
       struct Pend { size_t o0, o1, o2, o3; int n0, n1; };
@@ -462,9 +507,9 @@ namespace hssmf_b200 {
           pend[q].n0 = (int)st.d0.size();
           pend[q].n1 = (int)st.d1.size();
         }
-        J.Xp.alloc((size_t)N.mt * J.nc + 1, s);
+        J.Xp.alloc((size_t)N.mt * J.nc + 1, st);
       }
-      pool.upload(s);
+      pool.upload(st);
       std::vector<CopyDesc> c1, c2;
       for (size_t q = 0; q < jobs.size(); q++) {
         auto& J = jobs[q];
@@ -485,8 +530,8 @@ namespace hssmf_b200 {
         c2.push_back(cd(J.Xp.p, 1, N.mt, nullptr, 0, nullptr, 0, J.out, J.ldo, nullptr, 0, nullptr,
                         0, N.r, J.nc));
       }
-      index_copy_run(c1, s);
-      index_copy_run(c2, s);
+      index_copy_run(c1, st);
+      index_copy_run(c2, st);
       GemmGroups gg;
       for (auto& J : jobs) {
         HssNode& N = *J.N;
@@ -495,25 +540,48 @@ namespace hssmf_b200 {
           gg.tn_plus.push_back({(J.vside ? N.Ev : N.Eu).p, J.Xp.p + N.r, J.out, N.r, J.nc, k, k,
                                 N.mt, J.ldo});
       }
-      gg.run(s);
+      gg.run(st);
       flops += gg.flops;
       for (auto& J : jobs) J.Xp.free();
     }
 
+    // Done nodes of every level fold in this round's columns first, bottom-up
+    // (identical to folding each level just before its active nodes: a done
+    // node's children were done before this round, so their columns are
+    // folded first either way)
+    std::vector<std::vector<int>> done_by_level() const {
+      std::vector<std::vector<int>> out(maxdepth + 1);
+      for (int lv = maxdepth; lv >= 0; lv--)
+        for (int n : levels[lv])
+          if (nodes[n].state == DONE && n != root) out[lv].push_back(n);
+      return out;
+    }
+    void fold_done_all() {
+      const auto lists = done_by_level();
+      for (int lv = maxdepth; lv >= 0; lv--) {
+        if (lists[lv].empty()) continue;
+        Ph ph_(this, 5);
+        update_done(lists[lv], d, s);
+      }
+    }
+
+    // host work enqueued right before the next blocking readback (while the
+    // GPU runs the IDs): the speculative fold of next round's columns
+    std::function<void()> pending_spec;
+    void run_pending_spec() {
+      if (!pending_spec) return;
+      auto f = std::move(pending_spec);
+      pending_spec = nullptr;
+      f();
+    }
+
     void pass_level(int lv, int cap_id, double abs_tol, int& fail) {
-      std::vector<int> updl, act;
+      std::vector<int> act;
       for (int n : levels[lv]) {
         auto& N = nodes[n];
-        if (N.state == DONE) {
-          if (n != root) updl.push_back(n);
-          continue;
-        }
+        if (N.state == DONE) continue;
         if (!N.leaf && (nodes[N.c0].state != DONE || nodes[N.c1].state != DONE)) continue;
         act.push_back(n);
-      }
-      {
-        Ph ph_(this, 5);
-        update_done(updl);
       }
       if (act.empty()) return;
       auto* ph1 = new Ph(this, 1);
@@ -692,8 +760,10 @@ namespace hssmf_b200 {
       PermReadback prb;
       {
         Ph ph_(this, 3);
-        gram_cholesky_run(gt, o.eps, abs_tol, s, rk, ce, &flops,
-                          [&] { prb.enqueue(perm, nt, s); });
+        gram_cholesky_run(gt, o.eps, abs_tol, s, rk, ce, &flops, [&] {
+          prb.enqueue(perm, nt, s);
+          run_pending_spec();
+        });
       }
       prb.unpack(hp);
       ho.assign(2 * nt, 0);
@@ -756,6 +826,7 @@ namespace hssmf_b200 {
       d2h(ho.data(), outs.p, ho.size() * sizeof(int), s);
       PermReadback prb;
       prb.enqueue(perm, 2 * na, s);
+      run_pending_spec();
       stream_sync(s);
       prb.unpack(hp);
       for (int q = 0; q < 2 * na; q++) {
@@ -890,7 +961,7 @@ namespace hssmf_b200 {
       }
       index_copy_run(ce, s);
       index_copy_run(cg, s);
-      run_basis_apply(jobs);
+      run_basis_apply(jobs, s);
       for (int q : okq) {
         auto& N = nodes[act[q]];
         N.slr.release();
@@ -902,10 +973,12 @@ namespace hssmf_b200 {
     }
 
     // Done nodes fold in only the new columns (update_done, hss_compress.hpp:148-206)
-    void update_done(const std::vector<int>& lst) {
+    // (target column count dt, on stream st: the main stream, or the side
+    // stream when next round's columns are folded speculatively)
+    void update_done(const std::vector<int>& lst, int dt, cudaStream_t st) {
       std::vector<int> todo;
       for (int n : lst)
-        if (d - nodes[n].cols_built > 0) todo.push_back(n);
+        if (dt - nodes[n].cols_built > 0) todo.push_back(n);
       if (todo.empty()) return;
       std::vector<CopyDesc> c1, c3;
       GemmGroups gg;
@@ -913,10 +986,10 @@ namespace hssmf_b200 {
       std::vector<BasisApplyJob> jobs;
       for (size_t q = 0; q < todo.size(); q++) {
         auto& N = nodes[todo[q]];
-        const int cb = N.cols_built, nc = d - cb, r = N.r, mt = N.mt;
+        const int cb = N.cols_built, nc = dt - cb, r = N.r, mt = N.mt;
         for (Grow* g : {&N.sr, &N.sc, &N.rr, &N.rc}) {
-          g->ensure(d, &c1, &grave);
-          g->cols = d;
+          g->ensure(dt, &c1, &grave);
+          g->cols = dt;
         }
         if (N.leaf) {
           c1.push_back(cd(Sr.b.p, 1, m, N.d_ir.p, 0, nullptr, cb, N.sr.col(cb), r, nullptr, 0,
@@ -929,8 +1002,8 @@ namespace hssmf_b200 {
           auto& a = nodes[N.c0];
           auto& b = nodes[N.c1];
           const int ra = a.r, rb = b.r;
-          tr[q].alloc((size_t)mt * nc + 1, s);
-          tc[q].alloc((size_t)mt * nc + 1, s);
+          tr[q].alloc((size_t)mt * nc + 1, st);
+          tc[q].alloc((size_t)mt * nc + 1, st);
           c1.push_back(copy_block(a.sr.col(cb), ra, tr[q].p, mt, ra, nc));
           c1.push_back(copy_block(b.sr.col(cb), rb, tr[q].p + ra, mt, rb, nc));
           c1.push_back(copy_block(a.sc.col(cb), ra, tc[q].p, mt, ra, nc));
@@ -947,12 +1020,12 @@ namespace hssmf_b200 {
         jobs.push_back({&N, true, cb, nc, N.rr.col(cb), r, {}});
         jobs.push_back({&N, false, cb, nc, N.rc.col(cb), r, {}});
       }
-      index_copy_run(c1, s);
-      gg.run(s);
+      index_copy_run(c1, st);
+      gg.run(st);
       flops += gg.flops;
-      index_copy_run(c3, s);
-      run_basis_apply(jobs);
-      for (int n : todo) nodes[n].cols_built = d;
+      index_copy_run(c3, st);
+      run_basis_apply(jobs, st);
+      for (int n : todo) nodes[n].cols_built = dt;
     }
 
     // ------------------------------------------------------------------ ULV
