@@ -255,6 +255,12 @@ namespace hssmf_b200 {
     int d = 0, rounds = 0;
     double flops = 0;
     bool gram = false;  // ID route: Gram / pivoted Cholesky (eps >= 5e-5) or Householder
+    // numerically symmetric front (|F - F^T| <= 1e-10 max|F|, far below any
+    // compression tolerance of the Gram route): S_c = F^T R equals S_r = F R
+    // up to that perturbation, so the column-side IDs are taken from the
+    // row-side ones (V = U, ic = ir), computed once. Bitwise-symmetric fronts
+    // give exactly the two-sided result.
+    bool sym = false;
     // top factorization
     bool partial = false;
     DBuf<double> Z;
@@ -364,6 +370,16 @@ namespace hssmf_b200 {
       if (m == 0) {
         nodes[root].state = DONE;
         return;
+      }
+      sym = false;
+      if (gram && !getenv("HSSMF_NO_SYM")) {
+        DBuf<double> sf;
+        sf.alloc(2, s);
+        asymmetry_async(A, lda, m, sf.p, s);
+        double hs[2] = {1.0, 0.0};
+        d2h(hs, sf.p, 2 * sizeof(double), s);
+        stream_sync(s);
+        sym = hs[0] <= 1e-10 * hs[1];
       }
       // the next round's sampling products are computed speculatively on a
       // side stream while this round's (latency-bound) IDs run; a round that
@@ -674,13 +690,16 @@ namespace hssmf_b200 {
         const bool first = !N.G0r.p;
         if (first) {
           N.G0r.alloc((size_t)mt * mt, s);
-          N.G0c.alloc((size_t)mt * mt, s);
+          if (!sym) N.G0c.alloc((size_t)mt * mt, s);
         }
         GemmProblem gr{N.slr.col(cb0), N.slr.col(cb0), N.G0r.p, mt, mt, nc, mt, mt, mt};
-        GemmProblem gc{N.slc.col(cb0), N.slc.col(cb0), N.G0c.p, mt, mt, nc, mt, mt, mt};
-        gr.lower = gc.lower = 1;
+        gr.lower = 1;
         (first ? gp0 : gp).push_back(gr);
-        (first ? gp0 : gp).push_back(gc);
+        if (!sym) {
+          GemmProblem gc{N.slc.col(cb0), N.slc.col(cb0), N.G0c.p, mt, mt, nc, mt, mt, mt};
+          gc.lower = 1;
+          (first ? gp0 : gp).push_back(gc);
+        }
         N.gram_cols = d;
       }
       flops += gemm_flops(gp) + gemm_flops(gp0);
@@ -741,29 +760,56 @@ namespace hssmf_b200 {
         const int mt = N.mt;
         for (int side = 0; side < 2; side++) {
           const int t = 2 * q + side;
-          const DBuf<double>& G0 = side ? N.G0c : N.G0r;
           const int kdim = std::min(d, mt), kmax = std::min(kdim, std::max(cap_id, 0));
           const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
+          perm[t].alloc_keep(mt + 1, s);
+          if (sym && side == 1) {  // the row-side task's twin
+            gt[t] = gt[t - 1];
+            gt[t].orig_at = perm[t].p;
+            continue;
+          }
+          const DBuf<double>& G0 = side ? N.G0c : N.G0r;
           Gw[t].alloc((size_t)mt * mt + 1, s);
           if (mt) gcp.push_back(copy_block(G0.p, mt, Gw[t].p, mt, mt, mt));
           L[t].alloc((size_t)mt * kcap + 1, s);
           dg[t].alloc(mt + 1, s);
           flag[t].alloc(mt + 1, s);
           pos[t].alloc(mt + 1, s);
-          perm[t].alloc_keep(mt + 1, s);
-          gt[t] = {Gw[t].p, L[t].p, dg[t].p, flag[t].p, perm[t].p, pos[t].p, st.p + 3 * t,
-                   r11.p + t, mt, kdim, kmax, kcap};
+          const int ti = sym ? t / 2 : t;  // run tasks keep their states packed
+          gt[t] = {Gw[t].p, L[t].p, dg[t].p, flag[t].p, perm[t].p, pos[t].p, st.p + 3 * ti,
+                   r11.p + ti, mt, kdim, kmax, kcap};
         }
       }
       index_copy_run(gcp, s);
-      std::vector<int> rk, ce;
+      std::vector<GramTask> run;
+      std::vector<int> run_t;
+      for (int t = 0; t < nt; t++)
+        if (!sym || t % 2 == 0) {
+          run.push_back(gt[t]);
+          run_t.push_back(t);
+        }
+      std::vector<int> rk1, ce1, rk(nt), ce(nt);
       PermReadback prb;
       {
         Ph ph_(this, 3);
-        gram_cholesky_run(gt, o.eps, abs_tol, s, rk, ce, &flops, [&] {
+        gram_cholesky_run(run, o.eps, abs_tol, s, rk1, ce1, &flops, [&] {
+          if (sym)
+            for (int q = 0; q < na; q++)
+              if (gt[2 * q].n)
+                HSSMF_CUDA(cudaMemcpyAsync(perm[2 * q + 1].p, perm[2 * q].p,
+                                           (size_t)gt[2 * q].n * sizeof(int),
+                                           cudaMemcpyDeviceToDevice, s));
           prb.enqueue(perm, nt, s);
           run_pending_spec();
         });
+      }
+      for (size_t i = 0; i < run_t.size(); i++) {
+        rk[run_t[i]] = rk1[i];
+        ce[run_t[i]] = ce1[i];
+        if (sym) {
+          rk[run_t[i] + 1] = rk1[i];
+          ce[run_t[i] + 1] = ce1[i];
+        }
       }
       prb.unpack(hp);
       ho.assign(2 * nt, 0);
@@ -772,9 +818,10 @@ namespace hssmf_b200 {
         ho[2 * t] = rk[t];
         ho[2 * t + 1] = ce[t];
         const int mt = gt[t].n, k = rk[t];
+        const double* Lt = (sym && t % 2) ? L[t - 1].p : L[t].p;
         Y[t].alloc((size_t)std::max(k, 1) * mt + 1, s);
         X[t].alloc((size_t)k * std::max(mt - k, 0) + 1, s);
-        if (k) rc.push_back(cd(L[t].p, mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
+        if (k) rc.push_back(cd(Lt, mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
                                nullptr, 0, k, mt));
         tasks[t] = {Y[t].p, k, mt, std::max(k, 1), std::max(cap_id, 0), perm[t].p, X[t].p,
                     outs.p + 2 * t};

@@ -72,6 +72,29 @@ namespace hssmf_b200 {
       }
     }
 
+    // asymmetry of a dense front: out[0] = max_{i>j} |a(i,j) - a(j,i)|,
+    // out[1] = max |a(i,j)| (non-negative doubles compare as their bits)
+    __global__ void asymmetry_kernel(const double* __restrict__ a, long long lda, int m,
+                                     unsigned long long* out) {
+      const long long tot = (long long)m * m;
+      double da = 0.0, mx = 0.0;
+      for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
+           e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % m), j = (int)(e / m);
+        const double x = a[i + j * lda];
+        mx = fmax(mx, fabs(x));
+        if (i > j) da = fmax(da, fabs(x - a[j + i * lda]));
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        da = fmax(da, __shfl_xor_sync(0xffffffffu, da, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, (unsigned long long)__double_as_longlong(da));
+        atomicMax(out + 1, (unsigned long long)__double_as_longlong(mx));
+      }
+    }
+
     constexpr int UT = 256;
 
     // ---- batched ULV sweep phases (see ulv_fwd_level / ulv_bwd_level) -------
@@ -605,6 +628,15 @@ namespace hssmf_b200 {
     }
     release_async(d, s);
     HSSMF_CUDA(cudaFreeAsync(scr, s));
+  }
+
+  void asymmetry_async(const double* a, long long lda, int m, double* dout, cudaStream_t s) {
+    HSSMF_CUDA(cudaMemsetAsync(dout, 0, 2 * sizeof(double), s));
+    if (m > 0) {
+      asymmetry_kernel<<<std::min(ceil_div((long long)m * m, 256), 148 * 8), 256, 0, s>>>(
+          a, lda, m, reinterpret_cast<unsigned long long*>(dout));
+      HSSMF_LAUNCH_CHECK();
+    }
   }
 
   void lu_solve_vec(const double* lu, int ld, const int* perm, int n, double* x, cudaStream_t s) {

@@ -80,6 +80,9 @@ namespace hssmf_b200 {
 
   // small dense LU solve (n x n factored in place, ld, composed row perm) of a
   // single vector: x <- U^-1 L^-1 P x ; run on one CTA
+  // dout[0] = max_{i>j} |a(i,j) - a(j,i)|, dout[1] = max |a| of the m x m
+  // matrix a (ld lda), stream-ordered (the caller reads them back)
+  void asymmetry_async(const double* a, long long lda, int m, double* dout, cudaStream_t s);
   void lu_solve_vec(const double* lu, int ld, const int* perm, int n, double* x, cudaStream_t s);
   // y (+)= alpha op(A) x for one small dense matrix (one launch)
   void gemv_run(char ta, int m, int n, double alpha, const double* A, int lda, const double* x,
