@@ -400,9 +400,13 @@ namespace hssmf_b200 {
         // sampling: Sr = A R, Sc = A^T R on the new columns (dense_oracles,
         // hss_compress.hpp:359-363)
         gemm_run_splitk({A, R.col(c0), Sr.col(c0), m, dn, m, (int)lda, m, m}, 'N', 'N', 1.0, 0.0, st);
-        gemm_run_splitk({A, R.col(c0), Sc.col(c0), m, dn, m, (int)lda, m, m}, 'T', 'N', 1.0, 0.0, st);
+        // (symmetric fronts: the column side feeds only column IDs, which are
+        // taken from the row side, so S_c and every column-side sample are
+        // not formed)
+        if (!sym)
+          gemm_run_splitk({A, R.col(c0), Sc.col(c0), m, dn, m, (int)lda, m, m}, 'T', 'N', 1.0, 0.0, st);
         maxabs_run(Sr.col(c0), m, m, dn, sc_acc, st);
-        maxabs_run(Sc.col(c0), m, m, dn, sc_acc, st);
+        if (!sym) maxabs_run(Sc.col(c0), m, m, dn, sc_acc, st);
       };
       while (true) {
         rounds++;
@@ -416,17 +420,17 @@ namespace hssmf_b200 {
           } else {
             R.ensure(d);
             Sr.ensure(d);
-            Sc.ensure(d);
+            if (!sym) Sc.ensure(d);
             sample(dold, d, s, scale.p);
           }
-          flops += 4.0 * m * m * dn;
+          flops += (sym ? 2.0 : 4.0) * m * m * dn;
           R.cols = Sr.cols = Sc.cols = d;
           spec_d = -1;
           if (d - o.p < o.max_rank && !getenv("HSSMF_NO_SPEC_SAMPLING")) {
             const int d2 = d + o.dd;
             R.ensure(d2);
             Sr.ensure(d2);
-            Sc.ensure(d2);
+            if (!sym) Sc.ensure(d2);
             side.follow(s);  // buffers (re)allocated on s: the side stream starts after them
             scale2.zero_on(side.s);
             sample(d, d2, side.s, scale2.p);
@@ -450,7 +454,8 @@ namespace hssmf_b200 {
           auto lists = done_by_level();
           for (auto& l : lists)
             for (int n : l)
-              for (Grow* g : {&nodes[n].sr, &nodes[n].sc, &nodes[n].rr, &nodes[n].rc}) g->ensure(dt);
+              for (Grow* g : {&nodes[n].sr, &nodes[n].sc, &nodes[n].rr, &nodes[n].rc})
+                if (!sym || g == &nodes[n].sr || g == &nodes[n].rr) g->ensure(dt);
           HSSMF_CUDA(cudaEventRecord(side.fork, s));
           pending_spec = [this, lists = std::move(lists), dt, &side] {
             StagingScope ss(staging_for(side.s));
@@ -652,25 +657,29 @@ namespace hssmf_b200 {
         const int cb = N.cols_built, nc = d - cb;
         if (nc <= 0) continue;
         N.slr.ensure(d, &cp, &grave);
-        N.slc.ensure(d, &cp, &grave);
+        if (!sym) N.slc.ensure(d, &cp, &grave);
         const int mt = N.mt;
         if (N.leaf) {
           cp.push_back(copy_block(Sr.col(cb) + N.begin, m, N.slr.col(cb), mt, mt, nc));
-          cp.push_back(copy_block(Sc.col(cb) + N.begin, m, N.slc.col(cb), mt, mt, nc));
           gg.nn.push_back({N.D, R.col(cb) + N.begin, N.slr.col(cb), mt, nc, mt, (int)N.ldD, m, mt});
-          gg.tn.push_back({N.D, R.col(cb) + N.begin, N.slc.col(cb), mt, nc, mt, (int)N.ldD, m, mt});
+          if (!sym) {
+            cp.push_back(copy_block(Sc.col(cb) + N.begin, m, N.slc.col(cb), mt, mt, nc));
+            gg.tn.push_back({N.D, R.col(cb) + N.begin, N.slc.col(cb), mt, nc, mt, (int)N.ldD, m, mt});
+          }
         } else {
           auto& a = nodes[N.c0];
           auto& b = nodes[N.c1];
           const int ra = a.r, rb = b.r;
           cp.push_back(copy_block(a.sr.col(cb), ra, N.slr.col(cb), mt, ra, nc));
           cp.push_back(copy_block(b.sr.col(cb), rb, N.slr.col(cb) + ra, mt, rb, nc));
-          cp.push_back(copy_block(a.sc.col(cb), ra, N.slc.col(cb), mt, ra, nc));
-          cp.push_back(copy_block(b.sc.col(cb), rb, N.slc.col(cb) + ra, mt, rb, nc));
           if (rb) gg.nn.push_back({N.B12.p, b.rr.col(cb), N.slr.col(cb), ra, nc, rb, ra, rb, mt});
           if (ra) gg.nn.push_back({N.B21.p, a.rr.col(cb), N.slr.col(cb) + ra, rb, nc, ra, rb, ra, mt});
-          if (rb) gg.tn.push_back({N.B21.p, b.rc.col(cb), N.slc.col(cb), ra, nc, rb, rb, rb, mt});
-          if (ra) gg.tn.push_back({N.B12.p, a.rc.col(cb), N.slc.col(cb) + ra, rb, nc, ra, ra, ra, mt});
+          if (!sym) {
+            cp.push_back(copy_block(a.sc.col(cb), ra, N.slc.col(cb), mt, ra, nc));
+            cp.push_back(copy_block(b.sc.col(cb), rb, N.slc.col(cb) + ra, mt, rb, nc));
+            if (rb) gg.tn.push_back({N.B21.p, b.rc.col(cb), N.slc.col(cb), ra, nc, rb, rb, rb, mt});
+            if (ra) gg.tn.push_back({N.B12.p, a.rc.col(cb), N.slc.col(cb) + ra, rb, nc, ra, ra, ra, mt});
+          }
         }
         N.cols_built = d;
         N.slr.cols = N.slc.cols = d;
@@ -987,24 +996,29 @@ namespace hssmf_b200 {
         N.rr.init(r, s);
         N.rc.init(r, s);
         N.sr.ensure(d);
-        N.sc.ensure(d);
         N.rr.ensure(d);
-        N.rc.ensure(d);
+        if (!sym) {
+          N.sc.ensure(d);
+          N.rc.ensure(d);
+        }
         N.sr.cols = N.sc.cols = N.rr.cols = N.rc.cols = d;
         cg.push_back(cd(N.slr.b.p, 1, mt, N.d_up.p, 0, nullptr, 0, N.sr.b.p, r, nullptr, 0, nullptr,
                         0, r, d));
-        cg.push_back(cd(N.slc.b.p, 1, mt, N.d_vp.p, 0, nullptr, 0, N.sc.b.p, r, nullptr, 0, nullptr,
-                        0, r, d));
+        if (!sym)
+          cg.push_back(cd(N.slc.b.p, 1, mt, N.d_vp.p, 0, nullptr, 0, N.sc.b.p, r, nullptr, 0,
+                          nullptr, 0, r, d));
         if (N.leaf) {
           N.dr.alloc((size_t)r * mt + 1, s);
-          N.dc.alloc((size_t)mt * r + 1, s);
           cg.push_back(cd(N.D, 1, N.ldD, N.d_up.p, 0, nullptr, 0, N.dr.p, r, nullptr, 0, nullptr, 0,
                           r, mt));
-          cg.push_back(cd(N.D, 1, N.ldD, nullptr, 0, N.d_vp.p, 0, N.dc.p, mt, nullptr, 0, nullptr,
-                          0, mt, r));
+          if (!sym) {
+            N.dc.alloc((size_t)mt * r + 1, s);
+            cg.push_back(cd(N.D, 1, N.ldD, nullptr, 0, N.d_vp.p, 0, N.dc.p, mt, nullptr, 0, nullptr,
+                            0, mt, r));
+          }
         }
         jobs.push_back({&N, true, 0, d, N.rr.b.p, r, {}});
-        jobs.push_back({&N, false, 0, d, N.rc.b.p, r, {}});
+        if (!sym) jobs.push_back({&N, false, 0, d, N.rc.b.p, r, {}});
       }
       index_copy_run(ce, s);
       index_copy_run(cg, s);
@@ -1035,37 +1049,41 @@ namespace hssmf_b200 {
         auto& N = nodes[todo[q]];
         const int cb = N.cols_built, nc = dt - cb, r = N.r, mt = N.mt;
         for (Grow* g : {&N.sr, &N.sc, &N.rr, &N.rc}) {
-          g->ensure(dt, &c1, &grave);
+          if (!sym || g == &N.sr || g == &N.rr) g->ensure(dt, &c1, &grave);
           g->cols = dt;
         }
         if (N.leaf) {
           c1.push_back(cd(Sr.b.p, 1, m, N.d_ir.p, 0, nullptr, cb, N.sr.col(cb), r, nullptr, 0,
                           nullptr, 0, r, nc));
-          c1.push_back(cd(Sc.b.p, 1, m, N.d_ic.p, 0, nullptr, cb, N.sc.col(cb), r, nullptr, 0,
-                          nullptr, 0, r, nc));
           gg.nn.push_back({N.dr.p, R.col(cb) + N.begin, N.sr.col(cb), r, nc, mt, r, m, r});
-          gg.tn.push_back({N.dc.p, R.col(cb) + N.begin, N.sc.col(cb), r, nc, mt, mt, m, r});
+          if (!sym) {
+            c1.push_back(cd(Sc.b.p, 1, m, N.d_ic.p, 0, nullptr, cb, N.sc.col(cb), r, nullptr, 0,
+                            nullptr, 0, r, nc));
+            gg.tn.push_back({N.dc.p, R.col(cb) + N.begin, N.sc.col(cb), r, nc, mt, mt, m, r});
+          }
         } else {
           auto& a = nodes[N.c0];
           auto& b = nodes[N.c1];
           const int ra = a.r, rb = b.r;
           tr[q].alloc((size_t)mt * nc + 1, st);
-          tc[q].alloc((size_t)mt * nc + 1, st);
           c1.push_back(copy_block(a.sr.col(cb), ra, tr[q].p, mt, ra, nc));
           c1.push_back(copy_block(b.sr.col(cb), rb, tr[q].p + ra, mt, rb, nc));
-          c1.push_back(copy_block(a.sc.col(cb), ra, tc[q].p, mt, ra, nc));
-          c1.push_back(copy_block(b.sc.col(cb), rb, tc[q].p + ra, mt, rb, nc));
           if (rb) gg.nn.push_back({N.B12.p, b.rr.col(cb), tr[q].p, ra, nc, rb, ra, rb, mt});
           if (ra) gg.nn.push_back({N.B21.p, a.rr.col(cb), tr[q].p + ra, rb, nc, ra, rb, ra, mt});
-          if (rb) gg.tn.push_back({N.B21.p, b.rc.col(cb), tc[q].p, ra, nc, rb, rb, rb, mt});
-          if (ra) gg.tn.push_back({N.B12.p, a.rc.col(cb), tc[q].p + ra, rb, nc, ra, ra, ra, mt});
           c3.push_back(cd(tr[q].p, 1, mt, N.d_up.p, 0, nullptr, 0, N.sr.col(cb), r, nullptr, 0,
                           nullptr, 0, r, nc));
-          c3.push_back(cd(tc[q].p, 1, mt, N.d_vp.p, 0, nullptr, 0, N.sc.col(cb), r, nullptr, 0,
-                          nullptr, 0, r, nc));
+          if (!sym) {
+            tc[q].alloc((size_t)mt * nc + 1, st);
+            c1.push_back(copy_block(a.sc.col(cb), ra, tc[q].p, mt, ra, nc));
+            c1.push_back(copy_block(b.sc.col(cb), rb, tc[q].p + ra, mt, rb, nc));
+            if (rb) gg.tn.push_back({N.B21.p, b.rc.col(cb), tc[q].p, ra, nc, rb, rb, rb, mt});
+            if (ra) gg.tn.push_back({N.B12.p, a.rc.col(cb), tc[q].p + ra, rb, nc, ra, ra, ra, mt});
+            c3.push_back(cd(tc[q].p, 1, mt, N.d_vp.p, 0, nullptr, 0, N.sc.col(cb), r, nullptr, 0,
+                            nullptr, 0, r, nc));
+          }
         }
         jobs.push_back({&N, true, cb, nc, N.rr.col(cb), r, {}});
-        jobs.push_back({&N, false, cb, nc, N.rc.col(cb), r, {}});
+        if (!sym) jobs.push_back({&N, false, cb, nc, N.rc.col(cb), r, {}});
       }
       index_copy_run(c1, st);
       gg.run(st);
