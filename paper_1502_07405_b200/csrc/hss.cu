@@ -1283,20 +1283,21 @@ namespace hssmf_b200 {
           DBuf<double>& u = N.leaf ? N.Ub : dU[q];
           DBuf<double>& v = N.leaf ? N.Vb : dV[q];
           u.alloc((size_t)mt * r + 1, s);
-          v.alloc((size_t)mt * r + 1, s);
           u.zero();
-          v.zero();
           CopyDesc e1 = cd(one.p, 0, 0, nullptr, 0, nullptr, 0, u.p, mt, N.d_up.p, 0, nullptr, 0, r, r);
           e1.diag = 1;
+          c.push_back(e1);
+          if (k && r)
+            c.push_back(cd(N.Eu.p, 1, k, nullptr, 0, nullptr, 0, u.p, mt, N.d_up.p + r, 0, nullptr, 0, k, r));
+          if (sym) continue;  // V = U: the column bases are never formed
+          v.alloc((size_t)mt * r + 1, s);
+          v.zero();
           CopyDesc e2 = e1;
           e2.dst = v.p;
           e2.dr = N.d_vp.p;
-          c.push_back(e1);
           c.push_back(e2);
-          if (k && r) {
-            c.push_back(cd(N.Eu.p, 1, k, nullptr, 0, nullptr, 0, u.p, mt, N.d_up.p + r, 0, nullptr, 0, k, r));
+          if (k && r)
             c.push_back(cd(N.Ev.p, 1, k, nullptr, 0, nullptr, 0, v.p, mt, N.d_vp.p + r, 0, nullptr, 0, k, r));
-          }
         }
         index_copy_run(c, s);
         std::vector<GemmProblem> pp;
@@ -1307,10 +1308,11 @@ namespace hssmf_b200 {
           auto& b = nodes[N.c1];
           const int ma = a.size(), mb = b.size(), r = N.r;
           N.Ub.alloc((size_t)N.size() * r + 1, s);
-          N.Vb.alloc((size_t)N.size() * r + 1, s);
+          if (!sym) N.Vb.alloc((size_t)N.size() * r + 1, s);
           if (!r) continue;
           pp.push_back({a.Ub.p, dU[q].p, N.Ub.p, ma, r, a.r, ma, N.mt, N.size()});
           pp.push_back({b.Ub.p, dU[q].p + a.r, N.Ub.p + ma, mb, r, b.r, mb, N.mt, N.size()});
+          if (sym) continue;
           pp.push_back({a.Vb.p, dV[q].p, N.Vb.p, ma, r, a.r, ma, N.mt, N.size()});
           pp.push_back({b.Vb.p, dV[q].p + a.r, N.Vb.p + ma, mb, r, b.r, mb, N.mt, N.size()});
         }
@@ -1355,16 +1357,18 @@ namespace hssmf_b200 {
         const auto& b = nodes[N.c1];
         const int ma = a.size(), mb = b.size();
         DBuf<double> t1, t2;
-        t1.alloc((size_t)ma * b.r + 1, s);
         t2.alloc((size_t)mb * a.r + 1, s);
+        if (!sym) t1.alloc((size_t)ma * b.r + 1, s);
         if (a.r && b.r) {
-          p1.push_back({a.Ub.p, N.B12.p, t1.p, ma, b.r, a.r, ma, a.r, ma});
+          if (!sym) p1.push_back({a.Ub.p, N.B12.p, t1.p, ma, b.r, a.r, ma, a.r, ma});
           p1.push_back({b.Ub.p, N.B21.p, t2.p, mb, a.r, b.r, mb, b.r, mb});
         }
         double* o_ab = upd + (a.begin - nsep) + (size_t)(b.begin - nsep) * ldu;
         double* o_ba = upd + (b.begin - nsep) + (size_t)(a.begin - nsep) * ldu;
-        p2.push_back({t1.p, b.Vb.p, o_ab, ma, mb, b.r, ma, mb, (int)ldu});
-        p2.push_back({t2.p, a.Vb.p, o_ba, mb, ma, a.r, mb, ma, (int)ldu});
+        // symmetric front: only the blocks of the lower triangle are formed,
+        // the strict upper triangle is mirrored from them at the end
+        if (!sym) p2.push_back({t1.p, b.Vb.p, o_ab, ma, mb, b.r, ma, mb, (int)ldu});
+        p2.push_back({t2.p, sym ? a.Ub.p : a.Vb.p, o_ba, mb, ma, a.r, mb, ma, (int)ldu});
         T.push_back(std::move(t1));
         T.push_back(std::move(t2));
       }
@@ -1377,12 +1381,20 @@ namespace hssmf_b200 {
         t.alloc((size_t)nu * r1 + 1, s);
         std::vector<GemmProblem> q1{{N1.Ub.p, Z.p + r0 + (size_t)r0 * zn, t.p, nu, r1, r1, nu, zn, nu}};
         gemm_run_host(q1, 'N', 'N', 1.0, 0.0, s);
-        std::vector<GemmProblem> q2{{t.p, N1.Vb.p, upd, nu, nu, r1, nu, nu, (int)ldu}};
+        std::vector<GemmProblem> q2{{t.p, sym ? N1.Ub.p : N1.Vb.p, upd, nu, nu, r1, nu, nu, (int)ldu}};
+        q2[0].lower = sym ? 1 : 0;
         gemm_run_host(q2, 'N', 'T', 1.0, 1.0, s);
-        flops += gemm_flops(q1) + gemm_flops(q2);
+        flops += gemm_flops(q1) + (sym ? 0.5 : 1.0) * gemm_flops(q2);
       }
+      if (sym) mirror_lower_run(upd, ldu, nu, s);
       Ubig1 = std::move(N1.Ub);
-      Vbig1 = std::move(N1.Vb);
+      if (sym) {  // the solves read Vbig1 = Ubig1
+        Vbig1.alloc_keep(Ubig1.n, s);
+        HSSMF_CUDA(cudaMemcpyAsync(Vbig1.p, Ubig1.p, Ubig1.n * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, s));
+      } else {
+        Vbig1 = std::move(N1.Vb);
+      }
       for (int n : set1) {
         nodes[n].Ub.free();
         nodes[n].Vb.free();

@@ -95,6 +95,25 @@ namespace hssmf_b200 {
       }
     }
 
+    // strict upper triangle of the n x n matrix a (ld) := transpose of its
+    // strict lower triangle, 32 x 32 tiles through shared memory
+    __global__ void mirror_lower_kernel(double* a, long long ld, int n) {
+      __shared__ double t[32][33];
+      const int bi = blockIdx.y, bj = blockIdx.x;  // destination tile (bi < bj or diagonal)
+      if (bi > bj) return;
+      const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+      // source tile (bj, bi) of the lower triangle
+      for (int r = ty; r < 32; r += 8) {
+        const int i = bj * 32 + tx, j = bi * 32 + r;
+        t[r][tx] = (i < n && j < n) ? a[i + (size_t)j * ld] : 0.0;
+      }
+      __syncthreads();
+      for (int r = ty; r < 32; r += 8) {
+        const int i = bi * 32 + tx, j = bj * 32 + r;  // destination (i, j), i < j
+        if (i < n && j < n && i < j) a[i + (size_t)j * ld] = t[tx][r];
+      }
+    }
+
     constexpr int UT = 256;
 
     // ---- batched ULV sweep phases (see ulv_fwd_level / ulv_bwd_level) -------
@@ -637,6 +656,13 @@ namespace hssmf_b200 {
           a, lda, m, reinterpret_cast<unsigned long long*>(dout));
       HSSMF_LAUNCH_CHECK();
     }
+  }
+
+  void mirror_lower_run(double* a, long long ld, int n, cudaStream_t s) {
+    if (n <= 1) return;
+    const int nb = ceil_div(n, 32);
+    mirror_lower_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(a, ld, n);
+    HSSMF_LAUNCH_CHECK();
   }
 
   void lu_solve_vec(const double* lu, int ld, const int* perm, int n, double* x, cudaStream_t s) {

@@ -83,6 +83,8 @@ namespace hssmf_b200 {
   // dout[0] = max_{i>j} |a(i,j) - a(j,i)|, dout[1] = max |a| of the m x m
   // matrix a (ld lda), stream-ordered (the caller reads them back)
   void asymmetry_async(const double* a, long long lda, int m, double* dout, cudaStream_t s);
+  // a(i, j) = a(j, i) for i < j (n x n, ld): symmetrizes from the lower triangle
+  void mirror_lower_run(double* a, long long ld, int n, cudaStream_t s);
   void lu_solve_vec(const double* lu, int ld, const int* perm, int n, double* x, cudaStream_t s);
   // y (+)= alpha op(A) x for one small dense matrix (one launch)
   void gemv_run(char ta, int m, int n, double alpha, const double* A, int lda, const double* x,
