@@ -827,10 +827,13 @@ namespace hssmf_b200 {
         ho[2 * t] = rk[t];
         ho[2 * t + 1] = ce[t];
         const int mt = gt[t].n, k = rk[t];
-        const double* Lt = (sym && t % 2) ? L[t - 1].p : L[t].p;
+        if (sym && t % 2) {  // the row side's twin: its coefficients are reused
+          tasks[t] = tasks[t - 1];
+          continue;
+        }
         Y[t].alloc((size_t)std::max(k, 1) * mt + 1, s);
         X[t].alloc((size_t)k * std::max(mt - k, 0) + 1, s);
-        if (k) rc.push_back(cd(Lt, mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
+        if (k) rc.push_back(cd(L[t].p, mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
                                nullptr, 0, k, mt));
         tasks[t] = {Y[t].p, k, mt, std::max(k, 1), std::max(cap_id, 0), perm[t].p, X[t].p,
                     outs.p + 2 * t};
@@ -912,6 +915,7 @@ namespace hssmf_b200 {
         }
         okq.push_back(q);
         for (int side = 0; side < 2; side++) {
+          if (sym && side == 1) continue;  // the column-side coefficients are the row side's
           const int t = 2 * q + side, k = ho[2 * t];
           if (k > 0 && tasks[t].n > k) {
             if (k > 128) {  // GEMM-blocked triangular solve for large ranks
@@ -960,8 +964,8 @@ namespace hssmf_b200 {
           const int kid = side ? kc : kr, t = r - kid;
           DBuf<double>& E = side ? N.Ev : N.Eu;
           if (kid && kk)
-            ce.push_back(cd(X[2 * q + side].p + (size_t)t * kid, kid, 1, nullptr, 0, nullptr, 0,
-                            E.p, kk, nullptr, 0, nullptr, 0, kk, kid));
+            ce.push_back(cd(X[2 * q + (sym ? 0 : side)].p + (size_t)t * kid, kid, 1, nullptr, 0,
+                            nullptr, 0, E.p, kk, nullptr, 0, nullptr, 0, kk, kid));
           // zero padding columns [kid, r) only
           if (kk && r > kid)
             HSSMF_CUDA(cudaMemsetAsync(E.p + (size_t)kk * kid, 0, (size_t)kk * (r - kid) * sizeof(double), s));
