@@ -314,42 +314,47 @@ namespace hssmf_b200 {
       }
     }
 
-    template <int T, int NB>
-    __global__ void __launch_bounds__(T, 1)
+    template <int R, int NB>
+    __global__ void __launch_bounds__(512, 1)
     gram_panel2_kernel(const GramTask* __restrict__ tasks, int k0, double eps, double abs_tol,
                        int CL, int init) {
-      constexpr int NW = T / 32;
+      // T threads (a multiple of 32, <= 512, sized to the rows on the host)
+      const int T = blockDim.x, NW = T / 32, RPC = T * R;  // rows per CTA
       cg::cluster_group cl = cg::this_cluster();
       const int rank = (int)cl.block_rank();
       const GramTask Tk = tasks[blockIdx.x / CL];
       const int n = Tk.n;
       const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-      const int i = rank * T + tid;
-      const bool have = i < n;
+      const int row0 = rank * RPC + tid;  // own rows row0 + a T, a < R
       extern __shared__ __align__(16) double sm2[];
-      double* Lp = sm2;  // [NB][T]: own rows' panel columns (push source)
+      double* Lp = sm2;  // [NB][RPC]: own rows' panel columns (pivoted rows stay 0)
       __shared__ __align__(16) Cand stc[2][16];
       __shared__ __align__(16) double strow[2][16][NB];
       __shared__ __align__(8) unsigned long long mbar[2];
-      __shared__ Cand wred[2][NW];
+      __shared__ Cand wred[2][16];
 
       if (__ldcg(Tk.state + 1) && !init) return;  // finished in an earlier panel (uniform)
-      double dg = 0.0;
-      int pos = INT_MAX, flg = 1;
-      if (have) {
-        if (init) {
-          dg = Tk.G[i + (size_t)i * n];
-          pos = i;
-          flg = 0;
-        } else {
-          dg = __ldcg(Tk.dg + i);
-          pos = __ldcg(Tk.pos_of + i);
-          flg = __ldcg(Tk.flag + i);
+      double dg[R];
+      int pos[R], flg[R];
+#pragma unroll
+      for (int a = 0; a < R; a++) {
+        const int i = row0 + a * T;
+        dg[a] = 0.0;
+        pos[a] = INT_MAX;
+        flg[a] = 1;
+        if (i < n) {
+          if (init) {
+            dg[a] = Tk.G[i + (size_t)i * n];
+            pos[a] = i;
+            flg[a] = 0;
+          } else {
+            dg[a] = __ldcg(Tk.dg + i);
+            pos[a] = __ldcg(Tk.pos_of + i);
+            flg[a] = __ldcg(Tk.flag + i);
+          }
         }
       }
-      // own row's panel columns (zero until set; pivoted rows stay 0)
-#pragma unroll
-      for (int q = 0; q < NB; q++) Lp[q * T + tid] = 0.0;
+      for (int e = tid; e < NB * RPC; e += T) Lp[e] = 0.0;
       double r11 = init ? 0.0 : __ldcg(Tk.r11);
       if (tid == 0) {
         mbar_init(smem_u32(&mbar[0]), 1);
@@ -357,10 +362,17 @@ namespace hssmf_b200 {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       }
       // candidate of this CTA for the step whose buffer is b; the panel row
-      // carries nv values. Warp w sends it to peer w.
+      // carries nv values; warp w pushes it to peers w, w + NW, ...
       auto propose = [&](int b, int nv) {
-        double v = (have && !flg) ? dg : -1.0;
-        int p = (have && !flg) ? pos : INT_MAX, ix = (have && !flg) ? i : -1;
+        double v = -1.0;
+        int p = INT_MAX, ix = -1;
+#pragma unroll
+        for (int a = 0; a < R; a++)
+          if (!flg[a] && better(dg[a], pos[a], v, p)) {
+            v = dg[a];
+            p = pos[a];
+            ix = row0 + a * T;
+          }
         warp_best(v, p, ix);
         if (lane == 0) wred[b][warp] = {v, p, ix};
         __syncthreads();
@@ -376,15 +388,17 @@ namespace hssmf_b200 {
           ix = -1;
         }
         warp_best(v, p, ix);
-        const int peer = warp;
-        const uint32_t rbar = mapa(smem_u32(&mbar[b]), peer);
-        if (lane == 0)
-          st_async_v2(mapa(smem_u32(&stc[b][rank]), peer), (unsigned long long)__double_as_longlong(v),
-                      (unsigned long long)(unsigned)p | ((unsigned long long)(unsigned)ix << 32), rbar);
-        if (lane < nv) {
-          const double rv = ix >= 0 ? Lp[lane * T + (ix - rank * T)] : 0.0;
-          st_async_b64(mapa(smem_u32(&strow[b][rank][lane]), peer),
-                       (unsigned long long)__double_as_longlong(rv), rbar);
+        const double rv = (lane < nv && ix >= 0) ? Lp[lane * RPC + (ix - rank * RPC)] : 0.0;
+        for (int peer = warp; peer < CL; peer += NW) {
+          const uint32_t rbar = mapa(smem_u32(&mbar[b]), peer);
+          if (lane == 0)
+            st_async_v2(mapa(smem_u32(&stc[b][rank]), peer),
+                        (unsigned long long)__double_as_longlong(v),
+                        (unsigned long long)(unsigned)p | ((unsigned long long)(unsigned)ix << 32),
+                        rbar);
+          if (lane < nv)
+            st_async_b64(mapa(smem_u32(&strow[b][rank][lane]), peer),
+                         (unsigned long long)__double_as_longlong(rv), rbar);
         }
       };
       int stopped = 0, cert = 0, jend = k0;
@@ -397,90 +411,108 @@ namespace hssmf_b200 {
       // rolled step loop: an unrolled one overflows the instruction cache
 #pragma unroll 1
       for (int jj = 0; jj < NB; jj++) {
-        if (!stopped) {
-          const int j = k0 + jj, buf = jj & 1;
-          if (tid == 0) mbar_arrive_expect(smem_u32(&mbar[buf]), (uint32_t)(CL * (16 + 8 * jj)));
-          mbar_wait(smem_u32(&mbar[buf]), (jj >> 1) & 1);
-          // decision (rrqr.hpp:62-77: largest residual norm, lowest position on ties)
-          double bv = -1.0;
-          int bp = INT_MAX, bi = -1;
-          if (lane < CL) {
-            const Cand c = stc[buf][lane];
-            bv = c.v;
-            bp = c.pos;
-            bi = c.idx;
-          }
-          warp_best(bv, bp, bi);
-          const double pv = bv > 0.0 ? sqrt(bv) : 0.0;
-          int stop = 0, ct = 0;
-          if (j == 0) {
-            r11 = pv;
-            if (pv == 0.0 || pv <= abs_tol) { stop = 1; ct = 1; }
-          } else if (pv <= eps * r11 || pv <= abs_tol) {
-            stop = 1;
-            ct = 1;
-          }
-          if (!stop && j == Tk.kmax) {
-            stop = 1;
-            ct = (j == Tk.kmax_dim);
-          }
-          if (stop) {
-            stopped = 1;
-            cert = ct;
-            jend = j;
-          } else {
-            const int pj = bi, pp = bp;
-            const double ljj = pv;
-            const bool act = have && !flg;
-            double gv = 0.0;
-            if (act && i != pj) gv = i >= pj ? Tk.G[i + (size_t)pj * n] : Tk.G[pj + (size_t)i * n];
-            const double* prow = strow[buf][pj / T];
-            double t0 = 0.0, t1 = 0.0;
-            const double* lrow = Lp + tid;
-            int q = 0;
-#pragma unroll 4
-            for (; q + 1 < jj; q += 2) {
-              t0 += lrow[q * T] * prow[q];
-              t1 += lrow[(q + 1) * T] * prow[q + 1];
-            }
-            if (q < jj) t0 += lrow[q * T] * prow[q];
-            if (act) {
-              double lo;
-              if (i == pj) {
-                flg = 1;
-                lo = ljj;
-              } else {
-                lo = (gv - (t0 + t1)) / ljj;
-                double dd = dg - lo * lo;
-                if (dd < 0.0) dd = 0.0;
-                dg = dd;
-              }
-              Lp[jj * T + tid] = lo;
-            }
-            if (have) {
-              if (i == pj) pos = j;
-              else if (pos == j) pos = pp;
-            }
-            if (j + 1 == Tk.kmax_dim) {  // factorization exhausted exactly
-              stopped = 1;
-              cert = 1;
-              jend = j + 1;
-            } else {
-              propose(buf ^ 1, jj + 1);
-              jend = j + 1;
-            }
+        if (stopped) break;
+        const int j = k0 + jj, buf = jj & 1;
+        if (tid == 0) mbar_arrive_expect(smem_u32(&mbar[buf]), (uint32_t)(CL * (16 + 8 * jj)));
+        mbar_wait(smem_u32(&mbar[buf]), (jj >> 1) & 1);
+        // decision (rrqr.hpp:62-77: largest residual norm, lowest position on ties)
+        double bv = -1.0;
+        int bp = INT_MAX, bi = -1;
+        if (lane < CL) {
+          const Cand c = stc[buf][lane];
+          bv = c.v;
+          bp = c.pos;
+          bi = c.idx;
+        }
+        warp_best(bv, bp, bi);
+        const double pv = bv > 0.0 ? sqrt(bv) : 0.0;
+        int stop = 0, ct = 0;
+        if (j == 0) {
+          r11 = pv;
+          if (pv == 0.0 || pv <= abs_tol) { stop = 1; ct = 1; }
+        } else if (pv <= eps * r11 || pv <= abs_tol) {
+          stop = 1;
+          ct = 1;
+        }
+        if (!stop && j == Tk.kmax) {
+          stop = 1;
+          ct = (j == Tk.kmax_dim);
+        }
+        if (stop) {
+          stopped = 1;
+          cert = ct;
+          jend = j;
+          break;
+        }
+        const int pj = bi, pp = bp;
+        const double ljj = pv;
+        double gv[R];
+#pragma unroll
+        for (int a = 0; a < R; a++) {
+          const int i = row0 + a * T;
+          gv[a] = 0.0;
+          if (i < n && !flg[a] && i != pj)
+            gv[a] = i >= pj ? Tk.G[i + (size_t)pj * n] : Tk.G[pj + (size_t)i * n];
+        }
+        const double* prow = strow[buf][pj / RPC];
+        double t0[R], t1[R];
+#pragma unroll
+        for (int a = 0; a < R; a++) t0[a] = t1[a] = 0.0;
+        const double* lrow = Lp + tid;
+        int q = 0;
+#pragma unroll 2
+        for (; q + 1 < jj; q += 2) {
+          const double p0 = prow[q], p1 = prow[q + 1];
+#pragma unroll
+          for (int a = 0; a < R; a++) {
+            t0[a] += lrow[q * RPC + a * T] * p0;
+            t1[a] += lrow[(q + 1) * RPC + a * T] * p1;
           }
         }
+        if (q < jj) {
+#pragma unroll
+          for (int a = 0; a < R; a++) t0[a] += lrow[q * RPC + a * T] * prow[q];
+        }
+#pragma unroll
+        for (int a = 0; a < R; a++) {
+          const int i = row0 + a * T;
+          if (i >= n) continue;
+          if (!flg[a]) {
+            double lo;
+            if (i == pj) {
+              flg[a] = 1;
+              lo = ljj;
+            } else {
+              lo = (gv[a] - (t0[a] + t1[a])) / ljj;
+              double dd = dg[a] - lo * lo;
+              if (dd < 0.0) dd = 0.0;
+              dg[a] = dd;
+            }
+            Lp[jj * RPC + a * T + tid] = lo;
+          }
+          if (i == pj) pos[a] = j;
+          else if (pos[a] == j) pos[a] = pp;
+        }
+        jend = j + 1;
+        if (j + 1 == Tk.kmax_dim) {  // factorization exhausted exactly
+          stopped = 1;
+          cert = 1;
+          break;
+        }
+        propose(buf ^ 1, jj + 1);
       }
       // the panel's columns of L (pivoted rows hold 0), state for the next
       // panel / the host, the current ID permutation
       const int ncol = jend - k0;
-      if (have) {
-        for (int q = 0; q < ncol; q++) Tk.L[i + (size_t)(k0 + q) * n] = Lp[q * T + tid];
-        __stcg(Tk.dg + i, dg);
-        __stcg(Tk.flag + i, flg);
-        __stcg(Tk.pos_of + i, pos);
-        __stcg(Tk.orig_at + pos, i);
+#pragma unroll
+      for (int a = 0; a < R; a++) {
+        const int i = row0 + a * T;
+        if (i >= n) continue;
+        for (int q = 0; q < ncol; q++) Tk.L[i + (size_t)(k0 + q) * n] = Lp[q * RPC + a * T + tid];
+        __stcg(Tk.dg + i, dg[a]);
+        __stcg(Tk.flag + i, flg[a]);
+        __stcg(Tk.pos_of + i, pos[a]);
+        __stcg(Tk.orig_at + pos[a], i);
       }
       if (rank == 0 && tid == 0) {
         if (k0 == 0) __stcg(Tk.r11, r11);
@@ -693,29 +725,29 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaMemcpyAsync(d, tasks.data(), nt * sizeof(GramTask), cudaMemcpyHostToDevice, s));
     }
     std::vector<int> hst(3 * nt);
-    // v2 panel (one row per thread) up to 16 x 512 rows; HSSMF_GRAM_V1=1 keeps
-    // the shared-memory panel kernel (measurement knob)
+    // v2 panel: one row per thread, up to 512 rows per CTA in clusters of up
+    // to 16, the CTA sized to its rows (no idle warps in the per-step
+    // decision work); HSSMF_GRAM_V1=1 keeps the older shared-memory kernel
     const bool force_v1 = getenv("HSSMF_GRAM_V1") != nullptr;
-    constexpr int NB2 = 32;
-    const bool v2 = !force_v1 && max_n <= 16 * 512;
-    int T2 = 512, CL2 = 1;
+    constexpr int NB2 = 32, RPC_MAX = 512;
+    const bool v2 = !force_v1 && max_n <= 16 * RPC_MAX;
+    int T2 = 32, CL2 = 1;
     if (v2) {
-      if (max_n <= 256) T2 = 256;
-      while (CL2 * T2 < max_n) CL2 *= 2;
       static bool attr2 = false;
       if (!attr2) {
-        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<512, NB2>,
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<1, NB2>,
                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<512, NB2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 512 * NB2 * 8));
-        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<256, NB2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * NB2 * 8));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<1, NB2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        RPC_MAX * NB2 * 8));
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 64 * 8));
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_dmma_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
         attr2 = true;
       }
+      while (CL2 * RPC_MAX < max_n) CL2 *= 2;
+      T2 = std::max(32, ((max_n + CL2 - 1) / CL2 + 31) / 32 * 32);
       CL = CL2;
       nb = NB2;
     }
@@ -740,12 +772,11 @@ namespace hssmf_b200 {
         cfg.numAttrs = 1;
         {
           ProbeScope prp(PROBE_GRAM_PANEL, s, 0.0, 0.0);
-          if (T2 == 512)
-            HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<512, NB2>, (const GramTask*)d,
-                                          k0, eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
-          else
-            HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<256, NB2>, (const GramTask*)d,
-                                          k0, eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
+          prp.tiles = CL2;
+          prp.kmax = max_n;
+          prp.nprob = nt;
+          HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<1, NB2>, (const GramTask*)d, k0,
+                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
           HSSMF_LAUNCH_CHECK();
         }
         if (k0 + nb > kmax) break;

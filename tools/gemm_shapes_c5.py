@@ -38,3 +38,14 @@ tot = sum(v[1] for v in agg.values())
 for key, (c, ms, fl) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"tiles {key[0]:>6} K {key[1]:>6}: {c:6d} launches {ms:9.1f} ms ({100 * ms / tot:5.1f}%) "
           f"{fl / max(ms, 1e-9) / 1e9:6.2f} TF/s")
+
+# Gram panel launches by cluster size (rows per task up to 512 * CL)
+pan = collections.defaultdict(lambda: [0, 0.0])
+for kind, ms, fl, by, tiles, kmax, npb in rows:
+    if kind == "1":
+        pan[int(tiles)][0] += 1
+        pan[int(tiles)][1] += float(ms)
+ptot = sum(v[1] for v in pan.values()) or 1.0
+for cl, (c, ms) in sorted(pan.items()):
+    print(f"gram panel CL {cl:2d}: {c:6d} launches {ms:9.1f} ms ({100 * ms / ptot:5.1f}%) "
+          f"{1e3 * ms / max(c, 1):7.1f} us/launch")
