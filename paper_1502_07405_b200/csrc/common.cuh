@@ -99,12 +99,15 @@ namespace hssmf_b200 {
   // device counter the Gram SYRK kernel adds its live tasks' algorithmic bytes
   // to (stopped tasks are skipped on the device, so the host cannot count them)
   unsigned long long* probe_device_bytes();
+  // HSS phase tag of the calling thread (recorded with each probed launch)
+  int& probe_phase();
   struct ProbeScope {
     int kind;
     cudaStream_t s;
     double flops, bytes;
     cudaEvent_t a = nullptr;
     int tiles = 0, kmax = 0, nprob = 0;  // GEMM shape summary (HSSMF_PROBE_DUMP)
+    int phase = -1;                      // HSS phase of the launching thread
     ProbeScope(int k, cudaStream_t st, double f, double b);
     ~ProbeScope();
   };

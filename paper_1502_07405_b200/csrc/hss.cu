@@ -283,13 +283,17 @@ namespace hssmf_b200 {
       cudaEvent_t a = nullptr;
       double f0;
       std::chrono::steady_clock::time_point t0;
+      int prev_phase;
       Ph(HssImpl* hh, int i) : h(hh), id(i), f0(hh->flops) {
+        prev_phase = probe_phase();
+        probe_phase() = i;
         if (!g_phase_timing) return;
         t0 = std::chrono::steady_clock::now();
         HSSMF_CUDA(cudaEventCreate(&a));
         HSSMF_CUDA(cudaEventRecord(a, h->s));
       }
       ~Ph() {
+        probe_phase() = prev_phase;
         if (!a) return;
         h->ph_host[id] +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

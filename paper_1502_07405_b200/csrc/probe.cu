@@ -12,7 +12,7 @@ namespace hssmf_b200 {
       int kind;
       cudaEvent_t a, b;
       double flops, bytes;
-      int tiles, kmax, nprob;
+      int tiles, kmax, nprob, phase;
     };
     std::mutex g_mu;
     std::vector<Rec> g_recs;
@@ -21,6 +21,10 @@ namespace hssmf_b200 {
   }  // namespace
 
   bool probe_enabled() { return g_on.load(std::memory_order_relaxed); }
+  int& probe_phase() {
+    static thread_local int ph = -1;
+    return ph;
+  }
 
   unsigned long long* probe_device_bytes() {
     std::lock_guard<std::mutex> l(g_mu);
@@ -43,13 +47,13 @@ namespace hssmf_b200 {
     // HSSMF_PROBE_DUMP=<path>: one CSV line per probed launch (shape study)
     FILE* dump = nullptr;
     if (const char* pth = getenv("HSSMF_PROBE_DUMP")) dump = fopen(pth, "w");
-    if (dump) fprintf(dump, "kind,ms,flops,bytes,tiles,kmax,nprob\n");
+    if (dump) fprintf(dump, "kind,ms,flops,bytes,tiles,kmax,nprob,phase\n");
     for (auto& r : g_recs) {
       float ms = 0;
       cudaEventElapsedTime(&ms, r.a, r.b);
       if (dump)
-        fprintf(dump, "%d,%.4f,%.6g,%.6g,%d,%d,%d\n", r.kind, ms, r.flops, r.bytes, r.tiles, r.kmax,
-                r.nprob);
+        fprintf(dump, "%d,%.4f,%.6g,%.6g,%d,%d,%d,%d\n", r.kind, ms, r.flops, r.bytes, r.tiles,
+                r.kmax, r.nprob, r.phase);
       auto& o = out[r.kind];
       o.launches++;
       o.ms += ms;
@@ -80,7 +84,7 @@ namespace hssmf_b200 {
     cudaEvent_t b;
     if (cudaEventCreate(&b) != cudaSuccess || cudaEventRecord(b, s) != cudaSuccess) return;
     std::lock_guard<std::mutex> l(g_mu);
-    g_recs.push_back({kind, a, b, flops, bytes, tiles, kmax, nprob});
+    g_recs.push_back({kind, a, b, flops, bytes, tiles, kmax, nprob, probe_phase()});
   }
 
 }  // namespace hssmf_b200

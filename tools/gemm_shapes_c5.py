@@ -24,7 +24,17 @@ P.api.probe_read()
 P.api.probe_enable(False)
 rows = [l.strip().split(",") for l in open(os.environ["HSSMF_PROBE_DUMP"])][1:]
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-for kind, ms, fl, by, tiles, kmax, npb in rows:
+PH = ["sample", "extract", "local", "cpqr", "finalize", "update_done", "ulv_elim", "ulv_top",
+      "densify"]
+byph = collections.defaultdict(lambda: [0, 0.0])
+for kind, ms, fl, by, tiles, kmax, npb, ph in rows:
+    k = ("gemm" if kind == "0" else "panel" if kind == "1" else "syrk") + "/" + \
+        (PH[int(ph)] if 0 <= int(ph) < len(PH) else "dense")
+    byph[k][0] += 1
+    byph[k][1] += float(ms)
+for k, (c, ms) in sorted(byph.items(), key=lambda x: -x[1][1]):
+    print(f"{k:24s} {c:7d} launches {ms:9.1f} ms")
+for kind, ms, fl, by, tiles, kmax, npb, ph in rows:
     if kind != "0":
         continue
     t, k = int(tiles), int(kmax)
@@ -41,7 +51,7 @@ for key, (c, ms, fl) in sorted(agg.items(), key=lambda x: -x[1][1]):
 
 # Gram panel launches by cluster size (rows per task up to 512 * CL)
 pan = collections.defaultdict(lambda: [0, 0.0])
-for kind, ms, fl, by, tiles, kmax, npb in rows:
+for kind, ms, fl, by, tiles, kmax, npb, ph in rows:
     if kind == "1":
         pan[int(tiles)][0] += 1
         pan[int(tiles)][1] += float(ms)
