@@ -215,6 +215,11 @@ namespace hssmf_b200 {
     Grow slr, slc, sr, sc, rr, rc;
     DBuf<double> G0r, G0c;  // Gram matrices of the local samples (Gram ID route)
     int gram_cols = 0;      // sample columns folded into G0r/G0c
+    // speculative next-round ID (Gram route, symmetric fronts): the local
+    // samples already hold [.., spec_cols); the ID result at d = spec_d
+    int fails = 0, spec_cols = 0, spec_d = 0, spec_rank = 0, spec_cert = 0;
+    DBuf<int> spec_perm;
+    DBuf<double> spec_L;
     DBuf<double> dr, dc;
     // ULV
     DBuf<double> G;
@@ -447,6 +452,10 @@ namespace hssmf_b200 {
         stream_sync(s);
         const int cap_id = std::min(d - o.p, o.max_rank);
         const double abs_tol = o.eps * sc;
+        next_d = spec_d;
+        side_ = &side;
+        cur_scale = sc;
+        next_scale = &scale2;
         int fail = -1;
         fold_done_all();
         // next round's columns of the nodes done now are folded on the side
@@ -481,6 +490,11 @@ namespace hssmf_b200 {
       // a speculative round may still run: the main stream waits for it
       // before anything reuses its buffers
       if (spec_d >= 0) HSSMF_CUDA(cudaStreamWaitEvent(s, side.done, 0));
+      HSSMF_CUDA(cudaStreamWaitEvent(s, side.done, 0));
+      for (auto& N : nodes)
+        if (N.spec_perm.p || N.spec_L.p) drop_spec(N);
+      side_ = nullptr;
+      next_scale = nullptr;
     }
 
     // index lists for the permuted gather of a stacked pair of r-row blocks
@@ -593,6 +607,11 @@ namespace hssmf_b200 {
     // host work enqueued right before the next blocking readback (while the
     // GPU runs the IDs): the speculative fold of next round's columns
     std::function<void()> pending_spec;
+    // next round's speculative samples (columns [d, next_d) on the side stream)
+    int next_d = -1;
+    SideStream* side_ = nullptr;
+    double cur_scale = 0;
+    DBuf<double>* next_scale = nullptr;  // max |S| of the speculative columns (device)
     void run_pending_spec() {
       if (!pending_spec) return;
       auto f = std::move(pending_spec);
@@ -658,6 +677,10 @@ namespace hssmf_b200 {
       GemmGroups gg;
       for (int n : act) {
         auto& N = nodes[n];
+        if (N.spec_cols > N.cols_built && N.spec_cols <= d) {  // formed by the speculation
+          N.cols_built = N.spec_cols;
+          N.slr.cols = N.cols_built;
+        }
         const int cb = N.cols_built, nc = d - cb;
         if (nc <= 0) continue;
         N.slr.ensure(d, &cp, &grave);
@@ -755,6 +778,122 @@ namespace hssmf_b200 {
     // Gram route (gram_id.cuh): residual norms / pivots from the pivoted
     // Cholesky of the incrementally accumulated Gram matrices; R = L^T is
     // scattered into position order for the common ID-coefficient solve
+    // ---- speculative next-round IDs (Gram route, symmetric fronts) ----------
+    // A node that already failed certification will most likely fail again;
+    // while its ID at d runs on the main stream, the ID at d + dd is computed
+    // on the side stream from next round's (speculatively sampled) columns:
+    // the subtree's folds and the node's local samples for [d, d + dd), the
+    // Gram matrix G(d) + S_new S_new^T and its pivoted Cholesky -- the same
+    // operations on the same values the next round would perform, so results
+    // are unchanged; the next round adopts the result instead of recomputing
+    // it (wasted when the node certifies at d).
+    // opt-in (HSSMF_SPEC_ID=1): measured on c5 at 9.23 s (nodes >= 3000 rows)
+    // and 9.98 s (>= 6000) against 9.00 s without -- the speculative rounds
+    // compete with the other fronts' work and their host-side setup delays the
+    // pair, so the adopted rounds do not pay for it yet
+    static bool spec_id_enabled() {
+      static const bool on = getenv("HSSMF_SPEC_ID") != nullptr;
+      return on;
+    }
+    // large IDs only: below this the device is busy with other fronts' work
+    // and the speculation competes with it instead of filling idle SMs
+    static int spec_min_rows() {
+      static const int v = getenv("HSSMF_SPEC_ID_ROWS") ? atoi(getenv("HSSMF_SPEC_ID_ROWS")) : 3000;
+      return v;
+    }
+    void subtree_done(int n, std::vector<std::vector<int>>& byd) {
+      const auto& N = nodes[n];
+      if (N.leaf) return;
+      for (int c : {N.c0, N.c1}) {
+        subtree_done(c, byd);
+        byd[nodes[c].depth].push_back(c);
+      }
+    }
+    void launch_spec_ids(const std::vector<int>& spec_nodes, int dt) {
+      SideStream& side = *side_;
+      const cudaStream_t ss = side.s;
+      StagingScope stg(staging_for(ss));
+      HSSMF_CUDA(cudaStreamWaitEvent(ss, side.fork, 0));
+      // the next round's tolerance: max |S| over every column up to dt
+      double nsc = 0;
+      d2h(&nsc, next_scale->p, sizeof(double), ss);
+      stream_sync(ss);
+      const double abs_tol_n = o.eps * std::max(cur_scale, nsc);
+      const int cap_n = std::min(dt - o.p, o.max_rank);
+      std::vector<GramTask> gts;
+      std::vector<DBuf<double>> Gs(spec_nodes.size()), Ls(spec_nodes.size()), dgs(spec_nodes.size());
+      std::vector<DBuf<int>> fls(spec_nodes.size()), poss(spec_nodes.size()), perms(spec_nodes.size());
+      DBuf<int> stt;
+      DBuf<double> r11s;
+      stt.alloc(3 * spec_nodes.size(), ss);
+      r11s.alloc(spec_nodes.size(), ss);
+      for (size_t q = 0; q < spec_nodes.size(); q++) {
+        auto& N = nodes[spec_nodes[q]];
+        const int mt = N.mt, cb = d, nc = dt - d;
+        // folds of the (done) subtree, bottom-up
+        std::vector<std::vector<int>> byd(maxdepth + 1);
+        subtree_done(spec_nodes[q], byd);
+        for (int lv = maxdepth; lv >= 0; lv--)
+          if (!byd[lv].empty()) update_done(byd[lv], dt, ss);
+        // the node's local samples for [d, dt) (row side)
+        std::vector<CopyDesc> cp;
+        GemmGroups gg;
+        if (N.leaf) {
+          cp.push_back(copy_block(Sr.col(cb) + N.begin, m, N.slr.col(cb), mt, mt, nc));
+          gg.nn.push_back({N.D, R.col(cb) + N.begin, N.slr.col(cb), mt, nc, mt, (int)N.ldD, m, mt});
+        } else {
+          auto& A0 = nodes[N.c0];
+          auto& A1 = nodes[N.c1];
+          const int ra = A0.r, rb = A1.r;
+          cp.push_back(copy_block(A0.sr.col(cb), ra, N.slr.col(cb), mt, ra, nc));
+          cp.push_back(copy_block(A1.sr.col(cb), rb, N.slr.col(cb) + ra, mt, rb, nc));
+          if (rb) gg.nn.push_back({N.B12.p, A1.rr.col(cb), N.slr.col(cb), ra, nc, rb, ra, rb, mt});
+          if (ra) gg.nn.push_back({N.B21.p, A0.rr.col(cb), N.slr.col(cb) + ra, rb, nc, ra, rb, ra, mt});
+        }
+        index_copy_run(cp, ss);
+        gg.run(ss);
+        flops += gg.flops;
+        N.spec_cols = dt;
+        // G(dt) = G(d) + S_new S_new^T on a copy
+        Gs[q].alloc((size_t)mt * mt + 1, ss);
+        if (mt) index_copy_run({copy_block(N.G0r.p, mt, Gs[q].p, mt, mt, mt)}, ss);
+        GemmProblem g{N.slr.col(cb), N.slr.col(cb), Gs[q].p, mt, mt, nc, mt, mt, mt};
+        g.lower = 1;
+        gemm_set_op(g, 'N', 'T', 1.0, 1.0);
+        gemm_run_mixed({g}, ss);
+        flops += gemm_flops({g});
+        const int kdim = std::min(dt, mt), kmax = std::min(kdim, std::max(cap_n, 0));
+        const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
+        Ls[q].alloc((size_t)mt * kcap + 1, ss);
+        dgs[q].alloc(mt + 1, ss);
+        fls[q].alloc(mt + 1, ss);
+        poss[q].alloc(mt + 1, ss);
+        perms[q].alloc(mt + 1, ss);
+        gts.push_back({Gs[q].p, Ls[q].p, dgs[q].p, fls[q].p, perms[q].p, poss[q].p,
+                       stt.p + 3 * q, r11s.p + q, mt, kdim, kmax, kcap});
+      }
+      std::vector<int> rk, ce;
+      gram_cholesky_run(gts, o.eps, abs_tol_n, ss, rk, ce, &flops);
+      for (size_t q = 0; q < spec_nodes.size(); q++) {
+        auto& N = nodes[spec_nodes[q]];
+        N.spec_d = dt;
+        N.spec_rank = rk[q];
+        N.spec_cert = ce[q];
+        N.spec_L = std::move(Ls[q]);
+        N.spec_perm = std::move(perms[q]);
+      }
+      HSSMF_CUDA(cudaEventRecord(side.done, ss));
+    }
+    // release a node's speculative buffers on the main stream (ordered after
+    // every main-stream use)
+    void drop_spec(HssNode& N) {
+      N.spec_L.s = s;
+      N.spec_L.free();
+      N.spec_perm.s = s;
+      N.spec_perm.free();
+      N.spec_d = 0;
+    }
+
     void gram_ids(const std::vector<int>& act, int cap_id, double abs_tol,
                   std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
                   std::vector<DBuf<int>>& perm, DBuf<int>& outs, std::vector<CpqrTask>& tasks,
@@ -762,6 +901,8 @@ namespace hssmf_b200 {
       const int na = (int)act.size(), nt = 2 * na;
       std::vector<DBuf<double>> Gw(nt), L(nt), dg(nt);
       std::vector<DBuf<int>> flag(nt), pos(nt);
+      std::vector<const double*> Luse(nt, nullptr);
+      std::vector<char> adopt(na, 0);
       DBuf<int> st;
       DBuf<double> r11;
       st.alloc(3 * nt, s);
@@ -771,10 +912,19 @@ namespace hssmf_b200 {
       for (int q = 0; q < na; q++) {
         auto& N = nodes[act[q]];
         const int mt = N.mt;
+        adopt[q] = sym && N.spec_d == d && N.spec_perm.p;
         for (int side = 0; side < 2; side++) {
           const int t = 2 * q + side;
           const int kdim = std::min(d, mt), kmax = std::min(kdim, std::max(cap_id, 0));
           const int kcap = ((kmax + kGramNB - 1) / kGramNB) * kGramNB + kGramNB;
+          if (adopt[q] && side == 0) {  // last round's speculation computed this ID
+            perm[t] = std::move(N.spec_perm);
+            perm[t].s = s;
+            gt[t] = {nullptr, nullptr, nullptr, nullptr, perm[t].p, nullptr, nullptr, nullptr, mt,
+                     kdim, kmax, kcap};
+            Luse[t] = N.spec_L.p;
+            continue;
+          }
           perm[t].alloc_keep(mt + 1, s);
           if (sym && side == 1) {  // the row-side task's twin
             gt[t] = gt[t - 1];
@@ -785,6 +935,7 @@ namespace hssmf_b200 {
           Gw[t].alloc((size_t)mt * mt + 1, s);
           if (mt) gcp.push_back(copy_block(G0.p, mt, Gw[t].p, mt, mt, mt));
           L[t].alloc((size_t)mt * kcap + 1, s);
+          Luse[t] = L[t].p;
           dg[t].alloc(mt + 1, s);
           flag[t].alloc(mt + 1, s);
           pos[t].alloc(mt + 1, s);
@@ -794,27 +945,54 @@ namespace hssmf_b200 {
         }
       }
       index_copy_run(gcp, s);
+      // nodes whose next-round ID is speculated now: failed before, next
+      // round's samples already on the way
+      std::vector<int> spec_nodes;
+      const int dt = d + o.dd;
+      if (sym && spec_id_enabled() && side_ && next_d == dt && next_scale)
+        for (int q = 0; q < na; q++) {
+          auto& N = nodes[act[q]];
+          // only next to an ID that runs now (an adopted round has nothing to
+          // overlap with): pairs of rounds share one ID's latency
+          if (adopt[q] || N.fails < 1 || N.mt < spec_min_rows() || N.spec_d == dt) continue;
+          spec_nodes.push_back(act[q]);
+          // buffers the side stream appends to are grown here, on the main stream
+          N.slr.ensure(dt);
+          std::vector<std::vector<int>> byd(maxdepth + 1);
+          subtree_done(act[q], byd);
+          for (auto& l : byd)
+            for (int c : l)
+              for (Grow* g : {&nodes[c].sr, &nodes[c].rr}) g->ensure(dt);
+        }
+      if (!spec_nodes.empty()) HSSMF_CUDA(cudaEventRecord(side_->fork, s));
       std::vector<GramTask> run;
       std::vector<int> run_t;
       for (int t = 0; t < nt; t++)
-        if (!sym || t % 2 == 0) {
+        if ((!sym || t % 2 == 0) && !adopt[t / 2]) {
           run.push_back(gt[t]);
           run_t.push_back(t);
         }
       std::vector<int> rk1, ce1, rk(nt), ce(nt);
       PermReadback prb;
+      auto hook = [&] {
+        if (sym)
+          for (int q = 0; q < na; q++)
+            if (gt[2 * q].n)
+              HSSMF_CUDA(cudaMemcpyAsync(perm[2 * q + 1].p, perm[2 * q].p,
+                                         (size_t)gt[2 * q].n * sizeof(int),
+                                         cudaMemcpyDeviceToDevice, s));
+        prb.enqueue(perm, nt, s);
+        run_pending_spec();
+        if (!spec_nodes.empty()) launch_spec_ids(spec_nodes, dt);
+      };
       {
         Ph ph_(this, 3);
-        gram_cholesky_run(run, o.eps, abs_tol, s, rk1, ce1, &flops, [&] {
-          if (sym)
-            for (int q = 0; q < na; q++)
-              if (gt[2 * q].n)
-                HSSMF_CUDA(cudaMemcpyAsync(perm[2 * q + 1].p, perm[2 * q].p,
-                                           (size_t)gt[2 * q].n * sizeof(int),
-                                           cudaMemcpyDeviceToDevice, s));
-          prb.enqueue(perm, nt, s);
-          run_pending_spec();
-        });
+        if (!run.empty()) {
+          gram_cholesky_run(run, o.eps, abs_tol, s, rk1, ce1, &flops, hook);
+        } else {
+          hook();
+          stream_sync(s);
+        }
       }
       for (size_t i = 0; i < run_t.size(); i++) {
         rk[run_t[i]] = rk1[i];
@@ -824,6 +1002,12 @@ namespace hssmf_b200 {
           ce[run_t[i] + 1] = ce1[i];
         }
       }
+      for (int q = 0; q < na; q++)
+        if (adopt[q]) {
+          const auto& N = nodes[act[q]];
+          rk[2 * q] = rk[2 * q + 1] = N.spec_rank;
+          ce[2 * q] = ce[2 * q + 1] = N.spec_cert;
+        }
       prb.unpack(hp);
       ho.assign(2 * nt, 0);
       std::vector<CopyDesc> rc;
@@ -837,13 +1021,15 @@ namespace hssmf_b200 {
         }
         Y[t].alloc((size_t)std::max(k, 1) * mt + 1, s);
         X[t].alloc((size_t)k * std::max(mt - k, 0) + 1, s);
-        if (k) rc.push_back(cd(L[t].p, mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
+        if (k) rc.push_back(cd(Luse[t], mt, 1, nullptr, 0, perm[t].p, 0, Y[t].p, k, nullptr, 0,
                                nullptr, 0, k, mt));
         tasks[t] = {Y[t].p, k, mt, std::max(k, 1), std::max(cap_id, 0), perm[t].p, X[t].p,
                     outs.p + 2 * t};
       }
       index_copy_run(rc, s);
       h2d(outs.p, ho.data(), ho.size() * sizeof(int), s);
+      for (int q = 0; q < na; q++)
+        if (adopt[q]) drop_spec(nodes[act[q]]);
     }
 
     void id_batch(const std::vector<int>& act, int cap_id, double abs_tol, int& fail) {
@@ -915,6 +1101,7 @@ namespace hssmf_b200 {
         const int kr = ho[4 * q], cr = ho[4 * q + 1], kc = ho[4 * q + 2], cc = ho[4 * q + 3];
         if (!cr || kr > cap_id || !cc || kc > cap_id) {
           fail = act[q];
+          nodes[act[q]].fails++;
           continue;
         }
         okq.push_back(q);

@@ -30,7 +30,8 @@ print(json.dumps({"x": hashlib.sha256(x.tobytes()).hexdigest(), "rank": m.rank.t
 
 def run(env_extra):
     env = {k: v for k, v in os.environ.items()
-           if k not in ("HSSMF_SPEC_FOLD", "HSSMF_NO_SPEC_SAMPLING", "HSSMF_NO_SYM")}
+           if k not in ("HSSMF_SPEC_FOLD", "HSSMF_NO_SPEC_SAMPLING", "HSSMF_NO_SYM",
+                        "HSSMF_SPEC_ID", "HSSMF_SPEC_ID_ROWS")}
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], capture_output=True, text=True,
                          env=env, timeout=600)
@@ -57,3 +58,12 @@ def test_symmetric_front_shortcut_matches_two_sided():
     rb, ro = np.array(both["rank"], float), np.array(once["rank"], float)
     assert np.all(np.abs(rb - ro) <= np.maximum(2, 0.1 * rb))
     assert once["relres"] <= 10 * both["relres"]
+
+
+def test_speculative_ids_are_bitwise_neutral():
+    # next-round IDs computed on the side stream and adopted by the next round
+    base = run({})
+    spec = run({"HSSMF_SPEC_ID": "1", "HSSMF_SPEC_ID_ROWS": "0"})
+    assert base["hss"] > 0
+    assert base["rank"] == spec["rank"]
+    assert base["x"] == spec["x"]
