@@ -534,7 +534,11 @@ def main():
                      frac=ach / peaks["hbm_gbs"], peak_src=peaks["hbm_src"],
                      algorithmic="16 B per lower-triangle Gram element per panel (read + write)")
         else:
-            e.update(bound="latency", note="pivot chain: one cluster-wide argmax per elimination step")
+            # a panel launch runs at most 32 dependent pivot steps
+            e.update(bound="latency", us_per_pivot_step=round(e["avg_launch_us"] / 32, 3),
+                     note="pivot chain: one cluster-wide argmax per elimination step; "
+                          "us_per_pivot_step = avg launch / 32 steps (an upper bound when "
+                          "tasks stop inside a panel)")
         e["traffic"] = TRAFFIC.get(name)
         roofs.append(e)
     roofs.sort(key=lambda e: -e["ms"])
