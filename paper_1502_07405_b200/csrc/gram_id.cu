@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -314,10 +315,47 @@ namespace hssmf_b200 {
       }
     }
 
+    // best of the first cnt (<= 32) candidates in shared memory, returned to
+    // every lane: a short sequential scan for a few entries, otherwise a
+    // log2(cnt)-level butterfly over the low lanes and a broadcast
+    __device__ __forceinline__ void best_of(const Cand* c, int cnt, double& v, int& p, int& ix) {
+      if (cnt <= 4) {
+        v = c[0].v;
+        p = c[0].pos;
+        ix = c[0].idx;
+        for (int q = 1; q < cnt; q++) {
+          const Cand x = c[q];
+          if (better(x.v, x.pos, v, p)) { v = x.v; p = x.pos; ix = x.idx; }
+        }
+        return;
+      }
+      const int lane = threadIdx.x & 31;
+      if (lane < cnt) {
+        const Cand x = c[lane];
+        v = x.v;
+        p = x.pos;
+        ix = x.idx;
+      } else {
+        v = -1.0;
+        p = INT_MAX;
+        ix = -1;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        if (o >= cnt) continue;  // uniform: lanes >= cnt hold no candidate
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (better(v2, p2, v, p)) { v = v2; p = p2; ix = i2; }
+      }
+      v = __shfl_sync(0xffffffffu, v, 0);
+      p = __shfl_sync(0xffffffffu, p, 0);
+      ix = __shfl_sync(0xffffffffu, ix, 0);
+    }
+
     template <int R, int NB>
     __global__ void __launch_bounds__(512, 1)
     gram_panel2_kernel(const GramTask* __restrict__ tasks, int k0, double eps, double abs_tol,
-                       int CL, int init) {
+                       int CL, int init, unsigned long long* tprobe) {
       // T threads (a multiple of 32, <= 512, sized to the rows on the host)
       const int T = blockDim.x, NW = T / 32, RPC = T * R;  // rows per CTA
       cg::cluster_group cl = cg::this_cluster();
@@ -377,17 +415,7 @@ namespace hssmf_b200 {
         if (lane == 0) wred[b][warp] = {v, p, ix};
         __syncthreads();
         if (warp >= CL) return;
-        if (lane < NW) {
-          const Cand c = wred[b][lane];
-          v = c.v;
-          p = c.pos;
-          ix = c.idx;
-        } else {
-          v = -1.0;
-          p = INT_MAX;
-          ix = -1;
-        }
-        warp_best(v, p, ix);
+        best_of(wred[b], NW, v, p, ix);
         const double rv = (lane < nv && ix >= 0) ? Lp[lane * RPC + (ix - rank * RPC)] : 0.0;
         for (int peer = warp; peer < CL; peer += NW) {
           const uint32_t rbar = mapa(smem_u32(&mbar[b]), peer);
@@ -413,18 +441,27 @@ namespace hssmf_b200 {
       for (int jj = 0; jj < NB; jj++) {
         if (stopped) break;
         const int j = k0 + jj, buf = jj & 1;
+        // per-step segment timing of CTA 0 / thread 0 (HSSMF_GRAM_TPROBE)
+        const bool tp = tprobe && blockIdx.x == 0 && tid == 0;
+        long long c_a = tp ? clock64() : 0;
         if (tid == 0) mbar_arrive_expect(smem_u32(&mbar[buf]), (uint32_t)(CL * (16 + 8 * jj)));
         mbar_wait(smem_u32(&mbar[buf]), (jj >> 1) & 1);
-        // decision (rrqr.hpp:62-77: largest residual norm, lowest position on ties)
-        double bv = -1.0;
-        int bp = INT_MAX, bi = -1;
-        if (lane < CL) {
-          const Cand c = stc[buf][lane];
-          bv = c.v;
-          bp = c.pos;
-          bi = c.idx;
+        long long c_b = tp ? clock64() : 0;
+        // decision (rrqr.hpp:62-77: largest residual norm, lowest position on
+        // ties): every lane scans the CL candidates itself
+        double bv;
+        int bp, bi;
+        best_of(stc[buf], CL, bv, bp, bi);
+        // the pivot's G column is requested before the stop tests (a stopped
+        // step discards the values)
+        double gv[R];
+#pragma unroll
+        for (int a = 0; a < R; a++) {
+          const int i = row0 + a * T;
+          gv[a] = 0.0;
+          if (bi >= 0 && i < n && !flg[a] && i != bi)
+            gv[a] = i >= bi ? Tk.G[i + (size_t)bi * n] : Tk.G[bi + (size_t)i * n];
         }
-        warp_best(bv, bp, bi);
         const double pv = bv > 0.0 ? sqrt(bv) : 0.0;
         int stop = 0, ct = 0;
         if (j == 0) {
@@ -446,14 +483,7 @@ namespace hssmf_b200 {
         }
         const int pj = bi, pp = bp;
         const double ljj = pv;
-        double gv[R];
-#pragma unroll
-        for (int a = 0; a < R; a++) {
-          const int i = row0 + a * T;
-          gv[a] = 0.0;
-          if (i < n && !flg[a] && i != pj)
-            gv[a] = i >= pj ? Tk.G[i + (size_t)pj * n] : Tk.G[pj + (size_t)i * n];
-        }
+        long long c_c = tp ? clock64() : 0;
         const double* prow = strow[buf][pj / RPC];
         double t0[R], t1[R];
 #pragma unroll
@@ -499,7 +529,16 @@ namespace hssmf_b200 {
           cert = 1;
           break;
         }
+        long long c_d = tp ? clock64() : 0;
         propose(buf ^ 1, jj + 1);
+        if (tp) {
+          const long long c_e = clock64();
+          atomicAdd(tprobe + 0, (unsigned long long)(c_b - c_a));
+          atomicAdd(tprobe + 1, (unsigned long long)(c_c - c_b));
+          atomicAdd(tprobe + 2, (unsigned long long)(c_d - c_c));
+          atomicAdd(tprobe + 3, (unsigned long long)(c_e - c_d));
+          atomicAdd(tprobe + 4, 1ull);
+        }
       }
       // the panel's columns of L (pivoted rows hold 0), state for the next
       // panel / the host, the current ID permutation
@@ -682,6 +721,30 @@ namespace hssmf_b200 {
     }
   }  // namespace
 
+  // per-step segment cycles of the panel kernel (measurement knob): wait,
+  // decision, row update, propose + push; printed by gram_tprobe_report()
+  unsigned long long* gram_tprobe() {
+    static unsigned long long* p = [] {
+      unsigned long long* q = nullptr;
+      if (getenv("HSSMF_GRAM_TPROBE")) {
+        HSSMF_CUDA(cudaMalloc(&q, 8 * sizeof(unsigned long long)));
+        HSSMF_CUDA(cudaMemset(q, 0, 8 * sizeof(unsigned long long)));
+      }
+      return q;
+    }();
+    return p;
+  }
+  void gram_tprobe_report() {
+    unsigned long long* p = gram_tprobe();
+    if (!p) return;
+    unsigned long long h[8];
+    HSSMF_CUDA(cudaMemcpy(h, p, sizeof(h), cudaMemcpyDeviceToHost));
+    const double n = h[4] ? (double)h[4] : 1.0;
+    fprintf(stderr, "[gram] steps %llu  cycles/step: wait %.0f decide %.0f update %.0f propose %.0f\n",
+            h[4], h[0] / n, h[1] / n, h[2] / n, h[3] / n);
+    HSSMF_CUDA(cudaMemset(p, 0, sizeof(h)));
+  }
+
   void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
                          cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
                          double* flops, const std::function<void()>& before_sync) {
@@ -776,7 +839,7 @@ namespace hssmf_b200 {
           prp.kmax = max_n;
           prp.nprob = nt;
           HSSMF_CUDA(cudaLaunchKernelEx(&cfg, gram_panel2_kernel<1, NB2>, (const GramTask*)d, k0,
-                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0));
+                                        eps, abs_tol, CL2, k0 == 0 ? 1 : 0, gram_tprobe()));
           HSSMF_LAUNCH_CHECK();
         }
         if (k0 + nb > kmax) break;

@@ -43,6 +43,10 @@ namespace hssmf_b200 {
   // runs the factorization of all tasks; returns per task (rank, certified)
   // after ONE host sync; before_sync may enqueue more device->host reads
   // that the same sync then covers
+  // HSSMF_GRAM_TPROBE=1: per-step segment cycles of the panel kernel
+  unsigned long long* gram_tprobe();
+  void gram_tprobe_report();
+
   void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
                          cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
                          double* flops = nullptr,

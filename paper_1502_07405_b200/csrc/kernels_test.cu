@@ -223,6 +223,7 @@ namespace hssmf_b200 {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *steps = rk.empty() ? 0 : rk[0];
+    gram_tprobe_report();
     return ms / iters;
   }
 
