@@ -20,6 +20,7 @@
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+#include <map>
 
 #include "common.cuh"
 #include "front.cuh"
@@ -29,6 +30,8 @@
 #include "hss_kernels.cuh"
 
 namespace hssmf_b200 {
+  cudaStream_t worker_stream_take(int device);
+  void worker_stream_give(int device, cudaStream_t st);
 
   namespace {
     constexpr int NB = 32;  // LU panel width (reference lu_recursive base, lu.hpp:51)
@@ -279,7 +282,7 @@ namespace hssmf_b200 {
 
   Engine::Engine(int device) : d_(new Impl), device_(device) {
     HSSMF_CUDA(cudaSetDevice(device));
-    HSSMF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    stream_ = worker_stream_take(device);
     d_->s = stream_;
     for (int k = 0; k < K_NCLASS; k++)
       d_->kstat[k].name = k < K_HSS_PH ? kclass_name[k] : hss_phase_name(k - K_HSS_PH);
@@ -290,22 +293,47 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
     int nw = 8;
     if (const char* e = getenv("HSSMF_HSS_STREAMS")) nw = std::max(1, atoi(e));
-    for (int w = 0; w < nw; w++) {
-      cudaStream_t st;
-      HSSMF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-      d_->hstreams.push_back(st);
+    for (int w = 0; w < nw; w++) d_->hstreams.push_back(worker_stream_take(device));
+  }
+
+  // worker streams outlive the engines that use them (a per-device free
+  // list): an engine created after another one reuses its streams, hence
+  // their side streams and pinned staging rings, instead of creating them
+  // again (stream creation and cudaHostAlloc cost milliseconds and the latter
+  // synchronizes)
+  namespace {
+    std::mutex g_ws_mu;
+    std::map<int, std::vector<cudaStream_t>>& worker_free() {
+      static auto* m = new std::map<int, std::vector<cudaStream_t>>();  // never destroyed
+      return *m;
     }
+  }  // namespace
+  cudaStream_t worker_stream_take(int device) {
+    {
+      std::lock_guard<std::mutex> lk(g_ws_mu);
+      auto& f = worker_free()[device];
+      if (!f.empty()) {
+        cudaStream_t st = f.back();
+        f.pop_back();
+        return st;
+      }
+    }
+    cudaStream_t st;
+    HSSMF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    return st;
+  }
+  void worker_stream_give(int device, cudaStream_t st) {
+    cudaStreamSynchronize(st);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    worker_free()[device].push_back(st);
   }
 
   Engine::~Engine() {
     cudaSetDevice(device_);
     auto hs = d_->hstreams;
     d_.reset();
-    for (auto st : hs) {
-      cudaStreamSynchronize(st);
-      cudaStreamDestroy(st);
-    }
-    if (stream_) cudaStreamDestroy(stream_);
+    for (auto st : hs) worker_stream_give(device_, st);
+    if (stream_) worker_stream_give(device_, stream_);
   }
 
   void Engine::analyze(const Csr& a, const Etree& t, const Options& o, const char* owned) {
