@@ -528,6 +528,11 @@ def main():
             e.update(bound="tensor", achieved=ach, peak=peaks["fp64_tflops"], unit="TFLOP/s",
                      frac=ach / peaks["fp64_tflops"], peak_src=peaks["fp64_src"],
                      algorithmic="2mnk per GEMM (mnk for lower-triangle SYRK updates)")
+            if pr["bytes"] > 0:
+                # A and B read once, C written (beta 0) or read + written
+                e.update(algorithmic_bytes_per_launch=pr["bytes"] / pr["launches"],
+                         flop_per_byte=pr["flops"] / pr["bytes"],
+                         hbm_gbs_at_algorithmic_bytes=pr["bytes"] / (pr["ms"] * 1e-3) / 1e9)
         elif pr["bytes"] > 0:
             ach = pr["bytes"] / (pr["ms"] * 1e-3) / 1e9
             e.update(bound="hbm", achieved=ach, peak=peaks["hbm_gbs"], unit="GB/s",

@@ -524,6 +524,8 @@ namespace hssmf_b200 {
       b.nprob = (int)probs.size();
       b.tiles = pre.back();
       b.flops = gemm_flops(probs);
+      b.ab_bytes = gemm_ab_bytes(probs);
+      b.c_elems = gemm_c_elems(probs);
       gp.insert(gp.end(), probs.begin(), probs.end());
       gpre.insert(gpre.end(), pre.begin(), pre.end());
       return b;

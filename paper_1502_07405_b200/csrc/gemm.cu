@@ -199,13 +199,26 @@ namespace hssmf_b200 {
     return f;
   }
 
+  double gemm_ab_bytes(const std::vector<GemmProblem>& p) {
+    double f = 0;
+    for (const auto& q : p) f += 8.0 * ((double)q.m * q.k + (double)q.k * q.n);
+    return f;
+  }
+
+  double gemm_c_elems(const std::vector<GemmProblem>& p) {
+    double f = 0;
+    for (const auto& q : p) f += (q.lower ? 0.5 : 1.0) * q.m * q.n;
+    return f;
+  }
+
   void gemm_run(const GemmBatchDev& b, char ta, char tb, double alpha, double beta,
                 cudaStream_t s) {
     if (b.nprob == 0 || b.tiles == 0) return;
     const bool TA = ta != 'N', TB = tb != 'N';
     set_gemm_attrs();
     dim3 grid(b.tiles), block(THREADS);
-    ProbeScope pr(PROBE_GEMM, s, probe_enabled() ? b.flops : 0.0, 0.0);
+    ProbeScope pr(PROBE_GEMM, s, probe_enabled() ? b.flops : 0.0,
+                  probe_enabled() ? gemm_bytes(b.ab_bytes, b.c_elems, beta) : 0.0);
     if (!TA && !TB) gemm_grouped_kernel<false, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
     else if (TA && !TB) gemm_grouped_kernel<true, false><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
     else if (!TA && TB) gemm_grouped_kernel<false, true><<<grid, block, SMEM, s>>>(b.probs, b.prefix, b.nprob, alpha, beta);
@@ -284,14 +297,17 @@ namespace hssmf_b200 {
       if (!b.nprob) return;
       const int tiles = b.pre[b.nprob];
       if (tiles) {
-        double fl = 0;
+        double fl = 0, by = 0;
         int km = 0;
         if (probe_enabled())
           for (int q = 0; q < b.nprob; q++) {
-            fl += (b.p[q].lower ? 1.0 : 2.0) * b.p[q].m * b.p[q].n * b.p[q].k;
-            km = std::max(km, b.p[q].k);
+            const GemmProblem& g = b.p[q];
+            fl += (g.lower ? 1.0 : 2.0) * g.m * g.n * g.k;
+            by += gemm_bytes(8.0 * ((double)g.m * g.k + (double)g.k * g.n),
+                             (g.lower ? 0.5 : 1.0) * g.m * g.n, g.beta);
+            km = std::max(km, g.k);
           }
-        ProbeScope pr(PROBE_GEMM, s, fl, 0.0);
+        ProbeScope pr(PROBE_GEMM, s, fl, by);
         pr.tiles = tiles;
         pr.kmax = km;
         pr.nprob = b.nprob;

@@ -41,6 +41,8 @@ namespace hssmf_b200 {
     int nprob = 0;
     int tiles = 0;
     double flops = 0;  // 2 m n k summed (probe accounting)
+    double ab_bytes = 0;  // 8 (mk + kn) summed: A and B read once (probe accounting)
+    double c_elems = 0;   // C elements touched (lower triangle only for SYRK-like problems)
   };
 
   constexpr int kGemmBM = 64, kGemmBN = 64;
@@ -48,6 +50,13 @@ namespace hssmf_b200 {
   // tile prefix for the batched tile shape
   std::vector<int> gemm_tile_prefix(const std::vector<GemmProblem>& p);
   double gemm_flops(const std::vector<GemmProblem>& p);
+  // algorithmic bytes of a batch: A and B read once, C written (beta == 0) or
+  // read and written; the probe's GEMM traffic denominator
+  double gemm_ab_bytes(const std::vector<GemmProblem>& p);
+  double gemm_c_elems(const std::vector<GemmProblem>& p);
+  inline double gemm_bytes(double ab_bytes, double c_elems, double beta) {
+    return ab_bytes + c_elems * (beta == 0.0 ? 8.0 : 16.0);
+  }
 
   // ta/tb: 'N' or 'T'. beta == 0 never reads C.
   void gemm_run(const GemmBatchDev& b, char ta, char tb, double alpha, double beta,
