@@ -335,6 +335,52 @@ def config_json(cfg, op, args):
             "l2": "inputs > L2 (factor storage tens of GB), no flush needed"}
 
 
+def spawn_ranks(n, dry):
+    """re-exec this command under torch.distributed.run with n local ranks;
+    returns the launcher's exit code"""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    env = dict(os.environ)
+    if not dry:
+        env.setdefault("NCCL_DEBUG", "INFO")  # NVLS / transport choice on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, cfg, world, rank):
+    """gloo, CPU: the ranks the GPU run would launch, the subtree partition of
+    the workload and the phased factor/solve protocol (parallel.protocol_check)
+    with a stand-in engine; prints the JSON line shape with n_gpus = world"""
+    import torch.distributed as dist
+    from paper_1502_07405_b200.parallel import TorchTransport, protocol_check, subtree_partition
+    if world > 1:
+        dist.init_process_group("gloo")
+    op = build_problem(cfg)
+    part = subtree_partition(op.t, world)
+    ok = protocol_check(op.t, part, rank, TorchTransport(None)) if world > 1 else True
+    oks = [ok]
+    if world > 1:
+        import torch
+        tt = torch.tensor([1 if ok else 0])
+        dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+        oks = [bool(tt.item())]
+    if rank == 0:
+        cj = config_json(cfg, op, args)
+        cj["parallelism"] = f"subtree{world}" if world > 1 else "single"
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "s", "n_gpus": world,
+                          "dry_run": True, "protocol_ok": oks[0], "steps": args.steps,
+                          "warmup": args.warmup, "config": cj,
+                          "partition": {"level": part.level, "edges": len(part.edges),
+                                        "update_bytes": part.factor_bytes()}}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -346,8 +392,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gmres", action="store_true",
                     help="also run GMRES(30) preconditioned by the timed factors (informational)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: launch the ranks over gloo and run the phased multi-GPU "
+                         "protocol with a stand-in engine (no GPU work, no timing)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # `python bench.py --gpus N` outside torchrun: launch the N ranks here
+        # (one process per GPU, the driver's own torchrun command line)
+        sys.exit(spawn_ranks(args.gpus, args.dry_run))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -357,8 +410,10 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        op = build_problem(cfg)
-        reference_arm(args, cfg, op)
+        reference_arm(args, cfg)
+        return
+    if args.dry_run:
+        dry_run(args, cfg, world, rank)
         return
 
     import torch
@@ -551,18 +606,21 @@ def main():
     roof = dict(dom[0]) if dom else {"kernel": None}
     flops_total = sum(k["flops"] for k in ks)
 
-    # the solve's HBM roofline: each sweep reads the stored factors once
-    # (factor_nnz doubles, the reference's own count) -> 2 * 8 * factor_nnz
-    # algorithmic bytes per solve (vectors are negligible beside them)
+    # the solve's HBM roofline: every stored factor scalar is read once per
+    # solve (the forward sweep reads L / L21 and the ULV lower factors, the
+    # backward sweep U / U12 and the upper ones): 8 B x factor_nnz (the
+    # reference's own count, multifrontal.hpp:463-467), plus the solution
+    # vector read and written once per sweep (2 x 16 B x n)
     solve_entry = None
     if not dist_mode and solve_ms:
-        fb = 16.0 * factor_nnz_val
+        fb = 8.0 * factor_nnz_val + 32.0 * n
         sm = float(np.median(solve_ms))
         if fb > 0 and sm > 0:
             ach = fb / (sm * 1e-3) / 1e9
             solve_entry = {"ms": round(sm, 3), "algorithmic_bytes": fb, "achieved": ach,
                            "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"],
-                           "note": "forward + backward sweeps, 2 x 8 B x factor_nnz"}
+                           "note": "8 B x factor_nnz (each stored scalar read once over the "
+                                   "two sweeps) + 32 B x n (x read + written per sweep)"}
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,

@@ -33,6 +33,20 @@ namespace hssmf_b200 {
 
   inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+  // Runs f once per CUDA device for one call site (`done` is that site's device
+  // bitmask). Function attributes (dynamic shared memory, non-portable cluster
+  // sizes) are per device, and the factor entry points run on worker threads,
+  // so a plain static flag is both racy and wrong for a second device.
+  template <class F>
+  void once_per_device(std::atomic<unsigned long long>& done, F&& f) {
+    int dev = 0;
+    HSSMF_CUDA(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();  // idempotent: two threads racing here both set the same attributes
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+
   // host time the calling thread spent blocked in stream_sync (seconds) and the
   // number of such waits: HSSMF_DEBUG splits a front's wall time into host work
   // and GPU waits with it

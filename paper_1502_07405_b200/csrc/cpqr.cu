@@ -418,8 +418,8 @@ namespace hssmf_b200 {
     }
 
     void set_attr() {
-      static bool done = false;
-      if (done) return;
+      static std::atomic<unsigned long long> done{0};
+      once_per_device(done, [] {
       HSSMF_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       220 * 1024));
       HSSMF_CUDA(cudaFuncSetAttribute(cpqr_cluster_kernel,
@@ -428,7 +428,7 @@ namespace hssmf_b200 {
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       HSSMF_CUDA(cudaFuncSetAttribute(id_solve_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      done = true;
+      });
     }
   }  // namespace
 

@@ -536,10 +536,23 @@ namespace hssmf_b200 {
       for (int i : lv[L])
         if (!D.want_hss[i]) dl.push_back(i);
       int dmax_ns = 0;
+      // K_ASM algorithmic bytes: the zeroing memsets of the level (bracketed
+      // with the kernel) write p_bytes + c_bytes; each owned CSR entry reads
+      // val + ind (12 B) and read-modify-writes its front element (16 B)
+      // (ownership rule for_front_entries, multifrontal.hpp:99-119)
+      P.bytes_asm = (double)P.p_bytes + (double)P.c_bytes;
       for (int i : dl) {
         dmax_ns = std::max(dmax_ns, D.hf[i].ns);
-        P.bytes_asm += 8.0 * ((double)D.hf[i].m * D.hf[i].ns + (double)D.hf[i].ns * D.hf[i].nu +
-                              (double)D.hf[i].nu * D.hf[i].nu);
+        const auto& f = D.t.nodes[i];
+        long long ent = 0;
+        for (int g = f.sep_begin; g < f.sep_end; g++)
+          ent += a.ptr[g + 1] - (std::lower_bound(a.ind.begin() + a.ptr[g], a.ind.begin() + a.ptr[g + 1],
+                                                  f.sep_begin) - a.ind.begin());
+        for (int g : f.upd) {
+          auto b0 = a.ind.begin() + a.ptr[g], b1 = a.ind.begin() + a.ptr[g + 1];
+          ent += std::lower_bound(b0, b1, f.sep_end) - std::lower_bound(b0, b1, f.sep_begin);
+        }
+        P.bytes_asm += 28.0 * (double)ent;
       }
       for (int slot = 0; slot < 2; slot++) {
         P.colpre_off[slot] = colpre.size();
@@ -1196,14 +1209,17 @@ namespace hssmf_b200 {
       if (Lh >= 0 && L < Lh) break;
       auto& P = D.levels[L];
       const int* ids = D.d_ids.as<int>() + P.dids_off;
-      if (P.p_bytes)
-        HSSMF_CUDA(cudaMemsetAsync(D.persist.as<char>(P.p_off), 0, P.p_bytes, stream_));
-      if (P.c_bytes) HSSMF_CUDA(cudaMemsetAsync(D.trans[L % 2].p, 0, P.c_bytes, stream_));
-      if (P.ndf) {
-        D.launch(K_ASM, 0, P.bytes_asm, [&] {
+      // the level's zeroing is part of assembly: timed in the same bracket
+      // as the scatter kernel, whose bytes count it (bytes_asm)
+      D.launch(K_ASM, 0, P.bytes_asm, [&] {
+        if (P.p_bytes)
+          HSSMF_CUDA(cudaMemsetAsync(D.persist.as<char>(P.p_off), 0, P.p_bytes, stream_));
+        if (P.c_bytes) HSSMF_CUDA(cudaMemsetAsync(D.trans[L % 2].p, 0, P.c_bytes, stream_));
+        if (P.ndf)
           DenseKernels::assemble_sparse(F, ids, P.ndf, D.d_ptr.as<int>(), D.d_ind.as<int>(),
                                         D.d_val.as<double>(), stream_);
-        });
+      });
+      if (P.ndf) {
         for (int slot = 0; slot < 2; slot++)
           D.launch(K_EXTADD, 0, P.bytes_ea[slot], [&] {
             DenseKernels::extend_add(F, ids, P.ndf, slot,

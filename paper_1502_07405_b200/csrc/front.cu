@@ -371,13 +371,13 @@ namespace hssmf_b200 {
     constexpr int kMaxTrsvSmem = 200 * 1024;
 
     void set_smem_attr() {
-      static bool done = false;
-      if (done) return;
+      static std::atomic<unsigned long long> done{0};
+      once_per_device(done, [] {
       HSSMF_CUDA(cudaFuncSetAttribute(fwd_trsv_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxTrsvSmem));
       HSSMF_CUDA(cudaFuncSetAttribute(bwd_trsv_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxTrsvSmem));
-      done = true;
+      });
     }
 
   }  // namespace

@@ -175,14 +175,14 @@ namespace hssmf_b200 {
     }
 
     void set_gemm_attrs() {
-      static bool attr = false;
-      if (attr) return;
+      static std::atomic<unsigned long long> done{0};
+      once_per_device(done, [] {
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      attr = true;
+      });
     }
   }  // namespace
 

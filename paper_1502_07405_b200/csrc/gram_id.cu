@@ -261,8 +261,11 @@ namespace hssmf_b200 {
           j++;
           break;
         }
-        // push the candidate for step j + 1 with its panel row (q <= jj)
-        push(buf ^ 1, c, jj + 1);
+        // push the candidate for step j + 1 with its panel row (q <= jj); not
+        // after the panel's last step: no peer waits on that phase, and an
+        // st.async still in flight when a peer exits could land in a later
+        // cluster's shared memory
+        if (jj + 1 < nb) push(buf ^ 1, c, jj + 1);
       }
       __syncthreads();
       // the panel's columns of L, written once from shared memory (no global
@@ -530,7 +533,7 @@ namespace hssmf_b200 {
           break;
         }
         long long c_d = tp ? clock64() : 0;
-        propose(buf ^ 1, jj + 1);
+        if (jj + 1 < NB) propose(buf ^ 1, jj + 1);  // (no peer waits after the last step)
         if (tp) {
           const long long c_e = clock64();
           atomicAdd(tprobe + 0, (unsigned long long)(c_b - c_a));
@@ -752,14 +755,13 @@ namespace hssmf_b200 {
     rank.assign(nt, 0);
     cert.assign(nt, 0);
     if (!nt) return;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    once_per_device(attr, [] {
       HSSMF_CUDA(cudaFuncSetAttribute(gram_panel_kernel,
                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       HSSMF_CUDA(cudaFuncSetAttribute(gram_panel_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap));
-      attr = true;
-    }
+    });
     int max_n = 0, kmax = 0;
     for (const auto& t : tasks) {
       max_n = std::max(max_n, t.n);
@@ -796,8 +798,8 @@ namespace hssmf_b200 {
     const bool v2 = !force_v1 && max_n <= 16 * RPC_MAX;
     int T2 = 32, CL2 = 1;
     if (v2) {
-      static bool attr2 = false;
-      if (!attr2) {
+      static std::atomic<unsigned long long> attr2{0};
+      once_per_device(attr2, [] {
         HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<1, NB2>,
                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         HSSMF_CUDA(cudaFuncSetAttribute(gram_panel2_kernel<1, NB2>,
@@ -807,8 +809,7 @@ namespace hssmf_b200 {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 64 * 8));
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_dmma_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
-        attr2 = true;
-      }
+      });
       while (CL2 * RPC_MAX < max_n) CL2 *= 2;
       T2 = std::max(32, ((max_n + CL2 - 1) / CL2 + 31) / 32 * 32);
       CL = CL2;

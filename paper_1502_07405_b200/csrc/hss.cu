@@ -17,6 +17,7 @@
 #include "gemm.cuh"
 #include "hss_kernels.cuh"
 #include "gram_id.cuh"
+#include <exception>
 #include "rng.cuh"
 #include "staging.cuh"
 #include "arena.cuh"
@@ -402,6 +403,17 @@ namespace hssmf_b200 {
       pending_spec = nullptr;
       DBuf<double> scale2;
       scale2.alloc_keep(1, s);
+      // on every exit by an exception (out of memory, rank guard) the side
+      // stream may still be writing R / Sr / Sc / scale2: wait for it before
+      // those buffers go back to the arena or the pool (declared after
+      // scale2, so it runs before scale2 is released)
+      struct SideDrain {
+        cudaStream_t st;
+        int exc;
+        ~SideDrain() {
+          if (std::uncaught_exceptions() > exc) cudaStreamSynchronize(st);
+        }
+      } side_drain{side.s, std::uncaught_exceptions()};
       int spec_d = -1;
       auto sample = [&](int c0, int c1, cudaStream_t st, double* sc_acc) {
         const int dn = c1 - c0;
@@ -435,7 +447,9 @@ namespace hssmf_b200 {
           flops += (sym ? 2.0 : 4.0) * m * m * dn;
           R.cols = Sr.cols = Sc.cols = d;
           spec_d = -1;
-          if (d - o.p < o.max_rank && !getenv("HSSMF_NO_SPEC_SAMPLING")) {
+          // (not in the profiled pass: its phase timers bracket the main
+          // stream only, so every sampling product must run there)
+          if (d - o.p < o.max_rank && !g_phase_timing && !getenv("HSSMF_NO_SPEC_SAMPLING")) {
             const int d2 = d + o.dd;
             R.ensure(d2);
             Sr.ensure(d2);

@@ -467,12 +467,12 @@ namespace hssmf_b200 {
     }
 
     void set_attr() {
-      static bool done = false;
-      if (done) return;
+      static std::atomic<unsigned long long> done{0};
+      once_per_device(done, [] {
       HSSMF_CUDA(cudaFuncSetAttribute(ulv_fwd_lsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       HSSMF_CUDA(cudaFuncSetAttribute(ulv_bwd_usolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       HSSMF_CUDA(cudaFuncSetAttribute(lu_solve_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      done = true;
+      });
     }
 
     // device copy of a host array: through the thread's staging ring when it

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -43,6 +44,12 @@ namespace hssmf_b200 {
 
   void Staging::complete() {
     for (const auto& p : pend_) std::memcpy(p.dst, hr_ + p.off, p.n);
+    pend_.clear();
+    hr_used_ = 0;
+  }
+
+  void Staging::discard() {
+    cudaStreamSynchronize(s_);  // no throw: may run during unwinding
     pend_.clear();
     hr_used_ = 0;
   }
@@ -112,7 +119,13 @@ namespace hssmf_b200 {
     return (g_cur && g_cur->stream() == s) ? g_cur : nullptr;
   }
 
-  StagingScope::StagingScope(Staging* st) : prev(g_cur) { g_cur = st; }
-  StagingScope::~StagingScope() { g_cur = prev; }
+  StagingScope::StagingScope(Staging* st)
+      : prev(g_cur), cur(st), exc(std::uncaught_exceptions()) {
+    g_cur = st;
+  }
+  StagingScope::~StagingScope() {
+    if (cur && std::uncaught_exceptions() > exc) cur->discard();
+    g_cur = prev;
+  }
 
 }  // namespace hssmf_b200

@@ -32,6 +32,9 @@ namespace hssmf_b200 {
     // pinned buffer cannot take it now
     bool d2h(void* dst, const void* src, size_t n);
     void complete();
+    // drop the pending reads without delivering them (their destinations may
+    // be gone): waits for the stream, then clears the landing area
+    void discard();
 
    private:
     char* stage(const void* src, size_t n, char** dev);
@@ -65,8 +68,14 @@ namespace hssmf_b200 {
   Staging* staging_for(cudaStream_t s);
   // thread-local current staging ring
   Staging* current_staging(cudaStream_t s);
+  // Binds st for the calling thread. Leaving the scope by an exception
+  // discards st's pending device -> host reads: their destinations are stack or
+  // local buffers of the unwound frames, and the ring is pooled with its stream,
+  // so the next stream_sync would otherwise write into freed memory.
   struct StagingScope {
     Staging* prev;
+    Staging* cur;
+    int exc;
     explicit StagingScope(Staging* st);
     ~StagingScope();
   };

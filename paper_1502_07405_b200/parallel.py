@@ -196,6 +196,11 @@ class TorchTransport:
         buf = self.torch.empty(shape[::-1] if len(shape) == 2 else shape, dtype=self.torch.float64,
                                device=self.device)
         self.torch.distributed.recv(buf, src)
+        # NCCL's recv only orders torch's current stream after the transfer;
+        # the engine reads `buf` on its own stream, so the host waits here
+        # until the data has landed (the import copies are host-ordered after)
+        if buf.is_cuda:
+            self.torch.cuda.current_stream(buf.device).synchronize()
         return buf
 
 
@@ -258,10 +263,102 @@ class PartFactors:
                    int(lo), int(hi), 1 if forward else 0)
 
     def gather_x(self, x, rows):
+        # solve_levels synchronised the engine stream before returning
         return x[:, rows].contiguous()
 
     def scatter_x(self, x, rows, vals):
         x[:, rows] = vals
+        # the next solve_levels reads x on the engine's stream, not torch's
+        self.torch.cuda.current_stream(self.dev).synchronize()
+
+
+class ProtocolEngine:
+    """Stand-in for PartFactors (CPU tests and `bench.py --dry-run`): 'factoring' front f gives val[f] = f + sum of
+    the children's vals (a child's val must be local or imported), the forward
+    sweep fwd[f] = val[f] + sum of the children's fwd, the backward sweep
+    x[f] = fwd[f] + x[parent]. Checks that every phase finds its inputs."""
+
+    def __init__(self, t, part, rank):
+        import torch
+        self.torch = torch
+        self.t, self.part, self.rank = t, part, rank
+        self.own = np.asarray(part.owner) == rank
+        self.val, self.fwd = {}, {}
+
+    def _kids(self, f):
+        return [c for c in (self.t.child0[f], self.t.child1[f]) if c >= 0]
+
+    def _at(self, lo, hi):
+        return [f for f in range(len(self.own)) if self.own[f] and lo <= self.t.level[f] <= hi]
+
+    def factor_levels(self, lo, hi):
+        for f in sorted(self._at(lo, hi), key=lambda f: -self.t.level[f]):
+            self.val[f] = float(f) + sum(self.val[c] for c in self._kids(f))
+
+    def _nu(self, f):
+        return int(self.t.upd_ptr[f + 1] - self.t.upd_ptr[f])
+
+    def export_update(self, f):  # nu x nu, like the real update block
+        nu = self._nu(f)
+        return self.torch.full((nu, nu), self.val[f], dtype=self.torch.float64)
+
+    def import_update(self, f, buf):
+        self.val[f] = float(buf[0, 0])
+
+    def export_bupd(self, f, nrhs):
+        return self.torch.full((nrhs, self._nu(f)), self.fwd[f], dtype=self.torch.float64)
+
+    def import_bupd(self, f, buf, nrhs):
+        self.fwd[f] = float(buf[0, 0])
+
+    def solve_levels(self, x, lo, hi, forward):
+        fs = self._at(lo, hi)
+        if forward:
+            for f in sorted(fs, key=lambda f: -self.t.level[f]):
+                self.fwd[f] = self.val[f] + sum(self.fwd[c] for c in self._kids(f))
+        else:
+            for f in sorted(fs, key=lambda f: self.t.level[f]):
+                p = self.t.parent[f]
+                x[0, f] = self.fwd[f] + (float(x[0, p]) if p >= 0 else 0.0)
+
+    def gather_x(self, x, rows):
+        return x[:, rows].clone()
+
+    def scatter_x(self, x, rows, vals):
+        x[:, rows] = vals
+
+
+def protocol_expected(t):
+    nn = len(t.child0)
+    val, fwd, x = np.zeros(nn), np.zeros(nn), np.zeros(nn)
+    for f in range(nn):  # postorder
+        kids = [c for c in (t.child0[f], t.child1[f]) if c >= 0]
+        val[f] = f + sum(val[c] for c in kids)
+        fwd[f] = val[f] + sum(fwd[c] for c in kids)
+    for f in range(nn - 1, -1, -1):
+        p = t.parent[f]
+        x[f] = fwd[f] + (x[p] if p >= 0 else 0.0)
+    return val, x
+
+
+def protocol_check(t, part, rank, transport):
+    """Run the phased factor + solve protocol of `rank` with ProtocolEngine
+    over `transport`; True when every owned front saw the inputs the
+    sequential schedule would give it"""
+    import torch
+    eng = ProtocolEngine(t, part, rank)
+    nlev = int(np.asarray(t.level).max()) + 1
+    phased_factor(part, t.level, nlev, {rank: eng}, transport)
+    x = torch.zeros((1, len(t.child0)), dtype=torch.float64)
+
+    def upd_of(c):  # nu_c copies of the parent's slot in this stand-in x
+        return torch.full((int(t.upd_ptr[c + 1] - t.upd_ptr[c]),), int(t.parent[c]),
+                          dtype=torch.long)
+    phased_solve(part, t.level, nlev, upd_of, {rank: eng}, {rank: x}, 1, transport)
+    val, xe = protocol_expected(t)
+    own = np.nonzero(eng.own)[0]
+    return (all(abs(eng.val[f] - val[f]) < 1e-9 for f in own)
+            and all(abs(float(x[0, f]) - xe[f]) < 1e-9 for f in own))
 
 
 class DistributedMf:
@@ -297,6 +394,8 @@ class DistributedMf:
         """xs: {rank: (nrhs, n) float64 device tensor}, solved in place; each
         rank's x is correct on its own separators"""
         nrhs = next(iter(xs.values())).shape[0]
+        # xs may have been written on torch's stream; the engines use their own
+        self.torch.cuda.current_stream(self.dev).synchronize()
         phased_solve(self.part, self.t.level, self.nlev, self.upd_of, self.engines, xs, nrhs,
                      self.transport)
 

@@ -4,10 +4,14 @@ smaller configs) the solution. Runs in the build container, where
 /root/reference exists; the .npz files are committed so the GPU box needs no
 reference at run time.
 
-usage: python tests/golden/make_golden.py c1 c1_mf c3 c4 c5 [--threads N]
+usage: python tests/golden/make_golden.py c1 c1_mf c3 c4 c5 [--threads N] [--out-dir D]
+
+c5 (P3D 128^3) needs more host RAM than the build container has (OOM at 65 GB);
+it is run on the GPU-box host (tools/ref_c5_box.sh) and the .npz brought back.
 """
 import argparse
 import os
+import resource
 import sys
 import time
 
@@ -28,7 +32,22 @@ def ordered(cfg):
     return ref.ordered_grid(cfg.kind, cfg.k, cfg.nd_leaf)
 
 
-def run(name, threads):
+def host_info():
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            info["mem_total_kb"] = int(f.readline().split()[1])
+    except OSError:
+        pass
+    return info
+
+
+def run(name, threads, out_dir):
     cfg = CONFIGS[name]
     ref.set_threads(threads)
     t0 = time.time()
@@ -64,10 +83,12 @@ def run(name, threads):
         node_v=np.concatenate(node_v) if node_v else np.zeros(0, np.int32),
         rounds=np.array(rounds, np.int32), d_final=np.array(dfin, np.int32),
         perm_sum=np.int64((o.perm.astype(np.int64) * np.arange(o.n)).sum()),
+        peak_rss_kb=resource.getrusage(resource.RUSAGE_SELF).ru_maxrss,
+        host=str(host_info()),
     )
     if o.n <= 300000:
         out["x"] = x
-    path = os.path.join(ROOT, "tests", "golden", f"ref_{name}.npz")
+    path = os.path.join(out_dir, f"ref_{name}.npz")
     np.savez_compressed(path, **out)
     print(f"{name}: factor {F.factor_seconds:.2f}s solve {F.solve_seconds:.3f}s relres "
           f"{relres:.3e} hss {F.hss_fronts} maxrank {F.max_front_rank} flops {flops:.3e}",
@@ -78,6 +99,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--out-dir", default=os.path.join(ROOT, "tests", "golden"))
     a = ap.parse_args()
+    print(host_info(), flush=True)
     for c in a.configs:
-        run(c, a.threads)
+        run(c, a.threads, a.out_dir)

@@ -103,71 +103,8 @@ def test_update_exchange_gloo_world2():
 
 
 # ---- the phased factor / solve protocol, with a recording stand-in engine ----
-class FakeEngine:
-    """Stand-in for PartFactors: 'factoring' front f gives val[f] = f + sum of
-    the children's vals (a child's val must be local or imported), the forward
-    sweep fwd[f] = val[f] + sum of the children's fwd, the backward sweep
-    x[f] = fwd[f] + x[parent]. Checks that every phase finds its inputs."""
-
-    def __init__(self, t, part, rank):
-        self.t, self.part, self.rank = t, part, rank
-        self.own = np.asarray(part.owner) == rank
-        self.val, self.fwd = {}, {}
-
-    def _kids(self, f):
-        return [c for c in (self.t.child0[f], self.t.child1[f]) if c >= 0]
-
-    def _at(self, lo, hi):
-        return [f for f in range(len(self.own)) if self.own[f] and lo <= self.t.level[f] <= hi]
-
-    def factor_levels(self, lo, hi):
-        for f in sorted(self._at(lo, hi), key=lambda f: -self.t.level[f]):
-            self.val[f] = float(f) + sum(self.val[c] for c in self._kids(f))
-
-    def _nu(self, f):
-        return int(self.t.upd_ptr[f + 1] - self.t.upd_ptr[f])
-
-    def export_update(self, f):  # nu x nu, like the real update block
-        nu = self._nu(f)
-        return torch.full((nu, nu), self.val[f], dtype=torch.float64)
-
-    def import_update(self, f, buf):
-        self.val[f] = float(buf[0, 0])
-
-    def export_bupd(self, f, nrhs):
-        return torch.full((nrhs, self._nu(f)), self.fwd[f], dtype=torch.float64)
-
-    def import_bupd(self, f, buf, nrhs):
-        self.fwd[f] = float(buf[0, 0])
-
-    def solve_levels(self, x, lo, hi, forward):
-        fs = self._at(lo, hi)
-        if forward:
-            for f in sorted(fs, key=lambda f: -self.t.level[f]):
-                self.fwd[f] = self.val[f] + sum(self.fwd[c] for c in self._kids(f))
-        else:
-            for f in sorted(fs, key=lambda f: self.t.level[f]):
-                p = self.t.parent[f]
-                x[0, f] = self.fwd[f] + (float(x[0, p]) if p >= 0 else 0.0)
-
-    def gather_x(self, x, rows):
-        return x[:, rows].clone()
-
-    def scatter_x(self, x, rows, vals):
-        x[:, rows] = vals
-
-
-def _expected(t):
-    nn = len(t.child0)
-    val, fwd, x = np.zeros(nn), np.zeros(nn), np.zeros(nn)
-    for f in range(nn):  # postorder
-        kids = [c for c in (t.child0[f], t.child1[f]) if c >= 0]
-        val[f] = f + sum(val[c] for c in kids)
-        fwd[f] = val[f] + sum(fwd[c] for c in kids)
-    for f in range(nn - 1, -1, -1):
-        p = t.parent[f]
-        x[f] = fwd[f] + (x[p] if p >= 0 else 0.0)
-    return val, x
+from paper_1502_07405_b200.parallel import ProtocolEngine as FakeEngine  # noqa: E402
+from paper_1502_07405_b200.parallel import protocol_expected as _expected  # noqa: E402
 
 
 def _phased_worker(rank, world, port, q):
@@ -211,3 +148,20 @@ def test_phased_protocol_gloo(world):
     for p in ps:
         p.join(timeout=60)
     assert all(ok_v and ok_x for _, ok_v, ok_x in res), res
+
+
+def test_bench_spawns_ranks_dry_run():
+    # `python bench.py --gpus 4` outside torchrun launches 4 ranks itself; the
+    # CPU dry run (gloo) runs the phased protocol on the workload's partition
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4",
+                          "--dry-run", "--config", "c3"], capture_output=True, text=True,
+                         timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 4 and line["protocol_ok"] is True
+    assert line["config"]["parallelism"] == "subtree4" and line["partition"]["edges"] == 3
