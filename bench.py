@@ -148,71 +148,129 @@ def measured_peaks(torch, dev):
 
 
 # ------------------------------------------------------ reference sample ---
-def front_model_flops(op, cfg):
-    """per-front cost by the reference's own estimate (multifrontal.hpp:391-396:
-    dense 2ns^3/3 + 2ns^2 nu + 2 ns nu^2, HSS 4 m^2 d + 8 m r^2), with the HSS
-    fronts' (rank, d_final) from tests/golden/<workload>_front_model.npz (a
-    committed record of a full run) when the workload has HSS fronts"""
-    t = op.t
-    ns = (t.sep_end - t.sep_begin).astype(np.int64)
-    nu = np.diff(t.upd_ptr).astype(np.int64)
-    fl = dense_flops(ns, nu)
-    path = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_front_model.npz")
-    if os.path.exists(path):
-        g = np.load(path)
-        if len(g["rank"]) == len(fl):
-            h = g["type"] == 1
-            m = (ns + nu).astype(np.float64)
-            fl = np.where(h, 4 * m ** 2 * g["d_final"] + 8 * m * g["rank"].astype(np.float64) ** 2,
-                          fl)
-    return fl
+class TreeView:
+    """the arrays a sample needs, from the oracle's Ordered (reference arm: no
+    product library is loaded) or from the product's OrderedProblem"""
+
+    def __init__(self, ptr, ind, val, sep_begin, sep_end, child0, child1, parent, level,
+                 upd_ptr, upd_ind):
+        self.ptr, self.ind, self.val = ptr, ind, val
+        self.sep_begin, self.sep_end = np.asarray(sep_begin), np.asarray(sep_end)
+        self.child0, self.child1 = np.asarray(child0), np.asarray(child1)
+        self.parent, self.level = np.asarray(parent), np.asarray(level)
+        self.upd_ptr, self.upd_ind = np.asarray(upd_ptr), np.asarray(upd_ind)
+        self.nn = len(self.sep_begin)
+
+    def upd(self, i):
+        return self.upd_ind[self.upd_ptr[i]:self.upd_ptr[i + 1]]
+
+    @classmethod
+    def of_oracle(cls, o):
+        return cls(o.ptr, o.ind, o.val, o.sep_begin, o.sep_end, o.child0, o.child1, o.parent,
+                   o.level, o.upd_ptr, o.upd_ind)
+
+    @classmethod
+    def of_product(cls, op):
+        t = op.t
+        ptr, ind, val = op.a.arrays()
+        return cls(ptr, ind, val, t.sep_begin, t.sep_end, t.child0, t.child1, t.parent, t.level,
+                   t.upd_ptr, t.upd_ind)
 
 
-def subtree_sample(op, target_flops, cfg=None):
-    """A bounded, self-contained piece of the same workload for the CPU
-    reference: the subtree of one front s plus a synthetic root front whose
-    separator is upd(s), over the principal submatrix on those indices. Every
-    front of the subtree then has exactly the (ns, nu) it has in the full run
-    (so HSS fronts stay HSS). s = the first HSS front of the deepest HSS level
-    when the workload has HSS fronts (front model present), else the first
-    subtree along child0 under target_flops of dense-front cost.
-    Returns (pieces, total_model_flops, description)."""
-    t = op.t
-    ns = (t.sep_end - t.sep_begin).astype(np.int64)
-    nu = np.diff(t.upd_ptr).astype(np.int64)
+def oracle_ordered(cfg):
+    """the reference's own ordering / tree for the workload (oracle/_ref)"""
+    from oracle import ref
+    if cfg.kind == "cd3d":  # config 4 has no reference generator (SURVEY §8d)
+        import paper_1502_07405_b200 as P
+        ptr, ind, val = P.generate_convdiff3d(cfg.k, 0.1).A.arrays()
+        return ref.ordered_csr_geom(ptr, ind, val, (cfg.k,) * 3, 3, cfg.nd_leaf)
+    return ref.ordered_grid(cfg.kind, cfg.k, cfg.nd_leaf)
+
+
+def front_model(tv, cfg):
+    """per-front cost by the reference's own FrontStat.flops estimate
+    (multifrontal.hpp:389-396, 432-445: dense 2ns^3/3 + 2ns^2 nu + 2ns nu^2,
+    HSS 4 m^2 d_final + 8 m r^2) with the HSS fronts' (rank, d_final) of the
+    full reference run (tests/golden/ref_<config>.npz) when it exists, else of
+    the recorded product run (tests/golden/<workload>_front_model.npz).
+    Returns (flops per front, source)."""
+    ns = (tv.sep_end - tv.sep_begin).astype(np.float64)
+    nu = np.diff(tv.upd_ptr).astype(np.float64)
     fl = dense_flops(ns, nu)
-    nn = t.size()
-    s = None
-    if cfg is not None:
-        path = os.path.join(ROOT, "tests", "golden", f"{cfg.name}_front_model.npz")
-        if os.path.exists(path):
+    key = [k for k, v in __import__("paper_1502_07405_b200.problems",
+                                     fromlist=["CONFIGS"]).CONFIGS.items() if v is cfg]
+    for path, src in ((os.path.join(ROOT, "tests", "golden", f"ref_{key[0]}.npz") if key else "",
+                       "reference run"),
+                      (os.path.join(ROOT, "tests", "golden", f"{cfg.name}_front_model.npz"),
+                       "product run")):
+        if path and os.path.exists(path):
             g = np.load(path)
-            if len(g["rank"]) == len(fl):
-                fl = front_model_flops(op, cfg)
-                h = np.nonzero(g["type"] == 1)[0]
-                if len(h):
-                    deepest = t.level[h].max()
-                    s = int(h[t.level[h] == deepest].min())
+            if len(g["rank"]) != len(fl):
+                continue
+            h = np.asarray(g["type"]) == 1
+            m = ns + nu
+            if "d_final" in g and len(g["d_final"]) == len(fl):
+                dfin = g["d_final"].astype(np.float64)
+            else:  # per-HSS-front arrays (make_golden layout)
+                dfin = np.zeros(len(fl))
+                dfin[np.asarray(g["hss_ids"])] = g["d_final"]
+            fl = np.where(h, 4 * m ** 2 * dfin + 8 * m * g["rank"].astype(np.float64) ** 2, fl)
+            return fl, src + " " + os.path.basename(path)
+    return fl, "dense-front model only"
+
+
+def hss_wanted(tv, cfg):
+    """structural HSS selection (multifrontal.hpp:410-412)"""
+    ns = tv.sep_end - tv.sep_begin
+    m = ns + np.diff(tv.upd_ptr)
+    ls = 0 if cfg.mode == "mf" else cfg.ls
+    return (tv.level < ls) & (m >= cfg.min_hss) & (ns > 0)
+
+
+def sample_candidates(tv, cfg):
+    """HSS-rooted subtrees of the workload (front s with its whole subtree),
+    cheapest first: [(model cost, s)]; the model costs come from front_model"""
+    fl, _ = front_model(tv, cfg)
+    nn = tv.nn
+    want = hss_wanted(tv, cfg)
     sub = fl.copy()
-    lo = np.arange(nn)
     for i in range(nn):  # postorder: children first
-        for c in (t.child0[i], t.child1[i]):
+        for c in (tv.child0[i], tv.child1[i]):
             if c >= 0:
                 sub[i] += sub[c]
+    cand = np.nonzero(want & (tv.parent >= 0))[0]
+    if not len(cand):  # no HSS front: dense subtrees along the root's child0 chain
+        cand, s = [], int(tv.child0[nn - 1])
+        while s >= 0:
+            cand.append(s)
+            s = int(tv.child0[s])
+        cand = np.array(cand, np.int64)
+    order = cand[np.argsort(sub[cand])]
+    return [(float(sub[s]), int(s)) for s in order]
+
+
+def subtree_sample(tv, cfg, s):
+    """A bounded, self-contained piece of the same workload for the CPU
+    reference: the subtree of front s plus a synthetic root front whose
+    separator is upd(s), over the principal submatrix on those indices. Every
+    front of the subtree keeps the (ns, nu) it has in the full run, so HSS
+    fronts stay HSS. Returns (pieces, sample ids, description)."""
+    nn = tv.nn
+    ns = tv.sep_end - tv.sep_begin
+    m = ns + np.diff(tv.upd_ptr)
+    want = hss_wanted(tv, cfg)
+    lo = np.arange(nn)
+    for i in range(nn):  # postorder: children first
+        for c in (tv.child0[i], tv.child1[i]):
+            if c >= 0:
                 lo[i] = min(lo[i], lo[c])
-    if s is None:
-        s = t.root_id()
-        while sub[s] > target_flops and t.child0[s] >= 0:
-            s = t.child0[s]
     ids = np.arange(lo[s], s + 1)
-    start = int(t.sep_begin[lo[s]])
-    end = int(t.sep_end[s])
-    U = t.upd(s).astype(np.int64)
+    start = int(tv.sep_begin[lo[s]])
+    end = int(tv.sep_end[s])
+    U = tv.upd(s).astype(np.int64)
     nin = end - start
     n_s = nin + len(U)
-    gmap = {}
-    for k, g_ in enumerate(U):
-        gmap[int(g_)] = nin + k
+
     def loc(v):
         v = np.asarray(v, np.int64)
         out = np.where((v >= start) & (v < end), v - start, -1)
@@ -221,10 +279,9 @@ def subtree_sample(op, target_flops, cfg=None):
             hit = (pos < len(U)) & (U[np.minimum(pos, len(U) - 1)] == v)
             out = np.where(hit, nin + pos, out)
         return out
-    ptr, ind, val = op.a.arrays()
-    rows = list(range(start, end)) + [int(x) for x in U]
-    rows_ptr = [0]
-    sind, sval = [], []
+    ptr, ind, val = tv.ptr, tv.ind, tv.val
+    rows = np.concatenate([np.arange(start, end), U])
+    sind, sval, rows_ptr = [], [], [0]
     for r in rows:
         cols = ind[ptr[r]:ptr[r + 1]]
         lc = loc(cols)
@@ -238,25 +295,23 @@ def subtree_sample(op, target_flops, cfg=None):
     off = lo[s]
     m_ids = len(ids)
     remap = lambda v: np.where(v >= 0, v - off, -1).astype(np.int32)  # noqa: E731
-    par = remap(t.parent[ids])
+    par = remap(tv.parent[ids])
     par[-1] = m_ids + 1  # the synthetic root; an empty leaf is its second child
-    upd = [loc(t.upd(i)).astype(np.int32) for i in ids] + [np.zeros(0, np.int32)] * 2
+    upd = [loc(tv.upd(i)).astype(np.int32) for i in ids] + [np.zeros(0, np.int32)] * 2
     up = np.zeros(m_ids + 3, np.int32)
     for q, u in enumerate(upd):
         up[q + 1] = up[q] + len(u)
     pieces = dict(n=n_s, ptr=sptr, ind=sind, val=sval,
-                  sep_begin=np.concatenate([t.sep_begin[ids] - start, [nin, nin]]).astype(np.int32),
-                  sep_end=np.concatenate([t.sep_end[ids] - start, [nin, n_s]]).astype(np.int32),
-                  child0=np.concatenate([remap(t.child0[ids]), [-1, m_ids - 1]]).astype(np.int32),
-                  child1=np.concatenate([remap(t.child1[ids]), [-1, m_ids]]).astype(np.int32),
+                  sep_begin=np.concatenate([tv.sep_begin[ids] - start, [nin, nin]]).astype(np.int32),
+                  sep_end=np.concatenate([tv.sep_end[ids] - start, [nin, n_s]]).astype(np.int32),
+                  child0=np.concatenate([remap(tv.child0[ids]), [-1, m_ids - 1]]).astype(np.int32),
+                  child1=np.concatenate([remap(tv.child1[ids]), [-1, m_ids]]).astype(np.int32),
                   parent=np.concatenate([par, [m_ids + 1, -1]]).astype(np.int32),
                   upd_ptr=up, upd_ind=np.concatenate(upd))
-    desc = (f"subtree of front {s} (level {t.level[s]}, {m_ids} fronts, n={nin}) + a dense "
-            f"root over its {len(U)} update indices")
-    if s == t.root_id():
-        desc = "the whole workload"
-        return pieces, None, desc
-    return pieces, float(fl.sum()), desc
+    nh = int(want[ids].sum())
+    desc = (f"subtree of front {s} (level {tv.level[s]}, m={m[s]}, {m_ids} fronts, {nh} HSS "
+            f"fronts, n={nin}) + a dense root over its {len(U)} update indices")
+    return pieces, ids, desc
 
 
 def run_reference_sample(cfg, pieces, threads):
@@ -266,8 +321,7 @@ def run_reference_sample(cfg, pieces, threads):
                                 pieces["sep_begin"], pieces["sep_end"], pieces["child0"],
                                 pieces["child1"], pieces["parent"], pieces["upd_ptr"],
                                 pieces["upd_ind"])
-    from paper_1502_07405_b200.problems import csr_matvec, x_true
-    b = csr_matvec(pieces["ptr"], pieces["ind"], pieces["val"], x_true(pieces["n"], 1))
+    b = ref_rhs(pieces["ptr"], pieces["ind"], pieces["val"], pieces["n"])
     mode = {"auto": 0, "mf": 1, "mf-hss": 2}[cfg.mode]
     t0 = time.perf_counter()
     F = ref.Factors(o, eps=cfg.eps, ls=cfg.ls, leaf=cfg.leaf, d0=cfg.d0, dd=cfg.dd, p=cfg.p,
@@ -275,8 +329,45 @@ def run_reference_sample(cfg, pieces, threads):
     F.solve(b)
     t = time.perf_counter() - t0
     # the reference's own per-front cost model of what it actually did on the
-    # sample (FrontStat.flops, multifrontal.hpp:432-445)
+    # sample (FrontStat.flops, multifrontal.hpp:432-445), the synthetic root
+    # included: it is timed too (and is an HSS front when nu(s) >= min_hss)
     return t, float(F.flops.astype(np.float64).sum()), int(F.hss_fronts)
+
+
+def ref_rhs(ptr, ind, val, n):
+    from paper_1502_07405_b200.problems import csr_matvec, x_true  # numpy only
+    return csr_matvec(ptr, ind, val, x_true(n, 1))
+
+
+def reference_scaled(cfg, tv, threads, steps, warmup, budget_s):
+    """Time the reference on a sample of the workload and scale it by the
+    ratio of the full workload's model cost to the sample's (reference-
+    reported) model cost. The warm-up runs (at least one) time the cheapest
+    HSS-rooted subtree; the timed sample is then the largest HSS-rooted
+    subtree whose predicted time (at the warm-up's model rate) fits
+    budget_s / steps, so the whole arm stays within about budget_s."""
+    full, src = front_model(tv, cfg)
+    cands = sample_candidates(tv, cfg)
+    p0, _, _ = subtree_sample(tv, cfg, cands[0][1])
+    rate = None
+    for _ in range(max(1, warmup)):
+        tw, fw, _ = run_reference_sample(cfg, p0, threads)
+        rate = fw / max(tw, 1e-6)
+    per_step = budget_s / max(1, steps)
+    pick = cands[0][1]
+    for cost, s_ in cands:
+        if cost / rate <= per_step:
+            pick = s_
+    pieces, ids, desc = subtree_sample(tv, cfg, pick)
+    runs = [run_reference_sample(cfg, pieces, threads) for _ in range(steps)]
+    t = float(np.mean([r[0] for r in runs]))
+    sfl = runs[0][1]
+    scale = float(full.sum()) / sfl
+    desc += (f"; {runs[0][2]} HSS fronts factored by the reference in the sample; measured "
+             f"{t:.3f} s per sample (mean of {steps}), scaled x{scale:.2f} by the reference's "
+             f"per-front cost model (full workload from the {src}); sample picked for a "
+             f"{budget_s:.0f} s arm budget from a warm-up rate of {rate / 1e9:.2f} model GF/s")
+    return t * scale, t, scale, desc
 
 
 def cpu_threads():
@@ -286,33 +377,45 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def reference_arm(args, cfg, op):
+def reference_arm(args, cfg):
     from oracle import ref
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    pieces, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
+    o = oracle_ordered(cfg)
+    tv = TreeView.of_oracle(o)
     thr = cpu_threads()
-    for _ in range(args.warmup):
-        run_reference_sample(cfg, pieces, thr)
-    runs = [run_reference_sample(cfg, pieces, thr) for _ in range(args.steps)]
-    t = float(np.mean([r[0] for r in runs]))
-    sfl = runs[0][1]
-    desc += f", {runs[0][2]} HSS fronts in the sample"
-    if tfl is None:
-        tfl = sfl
-    scaled = t * tfl / sfl
+    scaled, t, scale, desc = reference_scaled(cfg, tv, thr, args.steps, args.warmup,
+                                              args.ref_budget_s)
     line = {
         "metric": METRIC, "value": scaled, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": scaled * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_json(cfg, op, args),
+        "data": "synthetic",
+        "config": config_json(cfg, None, args, n=o.n, nnz=len(o.ind), fronts=o.nnodes),
         "cpu_baseline": {"value": scaled, "unit": "s", "cores": thr, "kind": "reference",
-                         "sample": desc + f"; measured {t:.3f} s/step, scaled x{tfl / sfl:.1f}"},
+                         "sample": desc},
         "e2e": {"value": scaled, "unit": "s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    line.update(full_reference_run(cfg))
     print(json.dumps(line))
+
+
+def full_reference_run(cfg):
+    """the committed full reference run of the workload, if any (validation
+    of the scaled sample)"""
+    from paper_1502_07405_b200.problems import CONFIGS
+    key = [k for k, v in CONFIGS.items() if v is cfg]
+    path = os.path.join(ROOT, "tests", "golden", f"ref_{key[0]}.npz") if key else ""
+    if not path or not os.path.exists(path):
+        return {}
+    g = np.load(path)
+    return {"reference_full_run": {
+        "factor_s": float(g["factor_s"]), "solve_s": float(g["solve_s"]),
+        "threads": int(g["threads"]), "relres": float(g["relres"]), "flops": int(g["flops"]),
+        "host": str(g["host"]) if "host" in g else None,
+        "source": f"tests/golden/{os.path.basename(path)} (tests/golden/make_golden.py)"}}
 
 
 def _metric():
@@ -327,8 +430,10 @@ def _metric():
 METRIC = _metric()
 
 
-def config_json(cfg, op, args):
-    return {"workload": cfg.name, "n": op.a.size(), "nnz": op.a.nnz(), "fronts": op.t.size(),
+def config_json(cfg, op, args, n=None, nnz=None, fronts=None):
+    if op is not None:
+        n, nnz, fronts = op.a.size(), op.a.nnz(), op.t.size()
+    return {"workload": cfg.name, "n": n, "nnz": nnz, "fronts": fronts,
             "nd_leaf": cfg.nd_leaf, "hss": {"ls": cfg.ls, "min_hss": cfg.min_hss,
                                             "eps": cfg.eps, "leaf": cfg.leaf, "mode": cfg.mode},
             "parallelism": f"subtree{args.gpus}" if args.gpus > 1 else "single",
@@ -388,8 +493,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
-    ap.add_argument("--sample-flops", type=float, default=5e11)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: seconds of timed reference work in total "
+                         "(the sample is sized to fit budget / steps)")
     ap.add_argument("--gmres", action="store_true",
                     help="also run GMRES(30) preconditioned by the timed factors (informational)")
     ap.add_argument("--dry-run", action="store_true",
@@ -644,16 +751,12 @@ def main():
         try:
             from oracle import ref
             if ref.available():
-                pieces, tfl, desc = subtree_sample(op, args.sample_flops, cfg)
                 thr = cpu_threads()
-                t, sfl, nh = run_reference_sample(cfg, pieces, thr)
-                if tfl is None:
-                    tfl = sfl
-                line["cpu_baseline"] = {"value": t * tfl / sfl, "unit": "s", "cores": thr,
-                                        "kind": "reference",
-                                        "sample": desc + f", {nh} HSS fronts in the sample; "
-                                                         f"measured {t:.3f} s, scaled x"
-                                                         f"{tfl / sfl:.1f} by the cost model"}
+                tv = TreeView.of_oracle(oracle_ordered(cfg))
+                scaled, t, scale, desc = reference_scaled(cfg, tv, thr, 1, 1, 30.0)
+                line["cpu_baseline"] = {"value": scaled, "unit": "s", "cores": thr,
+                                        "kind": "reference", "sample": desc}
+                line["cpu_baseline"].update(full_reference_run(cfg))
         except Exception as e:  # reported, never fatal for the GPU arm
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

@@ -229,6 +229,14 @@ void hssmf_factors_free(hssmf_factors* f);
 int hssmf_hss_dense(int device, const double* a, int lda, int n, int leaf, double eps, int d0,
                     int dd, int p, int max_rank, int on_device, hssmf_hss** out,
                     hssmf_status* st);
+/* hss_compress(A, tree, HssOptions) + ulv_factor for any postorder cluster
+ * tree over [0, n) (ClusterTree, cluster_tree.hpp:12-97: nodes root last,
+ * children split the parent's [begin, end)); seeds = row index
+ * (hss_compress.hpp:380-381) */
+int hssmf_hss_dense_tree(int device, const double* a, int lda, int n, int nnodes,
+                         const int* begin, const int* end, const int* child0, const int* child1,
+                         double eps, int d0, int dd, int p, int max_rank, int on_device,
+                         hssmf_hss** out, hssmf_status* st);
 int hssmf_hss_info(const hssmf_hss* h, int* u_rank, int* v_rank, int* rounds, int* d_final,
                    double* compress_ms, double* ulv_ms);
 /* UlvFactors::solve (hss_ulv.hpp:150-176) */

@@ -76,6 +76,8 @@ namespace {
       return fail(st, HSSMF_ERR_DIVERGENCE, e.what());
     } catch (const CudaError& e) {
       return fail(st, HSSMF_ERR_CUDA, e.what());
+    } catch (const std::invalid_argument& e) {  // malformed input (IoError)
+      return fail(st, HSSMF_ERR_SHAPE, e.what());
     } catch (const std::exception& e) {
       return fail(st, HSSMF_ERR_OTHER, e.what());
     }
@@ -545,6 +547,21 @@ int hssmf_hss_dense(int device, const double* a, int lda, int n, int leaf, doubl
   const int rc = guard(st, [&] {
     h->h = std::make_unique<DenseHss>(device);
     h->h->run(a, lda, n, leaf, eps, d0, dd, p, max_rank, on_device != 0);
+  });
+  if (rc == HSSMF_OK) *out = h.release();
+  return rc;
+}
+
+int hssmf_hss_dense_tree(int device, const double* a, int lda, int n, int nnodes,
+                         const int* begin, const int* end, const int* child0, const int* child1,
+                         double eps, int d0, int dd, int p, int max_rank, int on_device,
+                         hssmf_hss** out, hssmf_status* st) {
+  *out = nullptr;
+  auto h = std::make_unique<hssmf_hss>();
+  const int rc = guard(st, [&] {
+    h->h = std::make_unique<DenseHss>(device);
+    h->h->run_tree(a, lda, n, nnodes, begin, end, child0, child1, eps, d0, dd, p, max_rank,
+                   on_device != 0);
   });
   if (rc == HSSMF_OK) *out = h.release();
   return rc;

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <atomic>
 #include <cstdint>
 #include <stdexcept>
@@ -30,6 +32,15 @@ namespace hssmf_b200 {
     ++::hssmf_b200::launch_counter();        \
     HSSMF_CUDA(cudaGetLastError());          \
   } while (0)
+
+  // NVTX range for timeline tools (nsys / ncu --nvtx); header-only NVTX 3,
+  // a no-op pointer check when no tool is attached
+  struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+  };
 
   inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 

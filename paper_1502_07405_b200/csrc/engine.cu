@@ -1209,6 +1209,10 @@ namespace hssmf_b200 {
       if (Lh >= 0 && L < Lh) break;
       auto& P = D.levels[L];
       const int* ids = D.d_ids.as<int>() + P.dids_off;
+      char rname[48];
+      snprintf(rname, sizeof rname, "factor level %d (%d dense, %d hss)", L, P.ndf,
+               (int)P.hss.size());
+      NvtxRange nv(rname);
       // the level's zeroing is part of assembly: timed in the same bracket
       // as the scatter kernel, whose bytes count it (bytes_asm)
       D.launch(K_ASM, 0, P.bytes_asm, [&] {
@@ -1424,6 +1428,7 @@ namespace hssmf_b200 {
     lo = std::max(lo, 0);
     hi = std::min(hi, nlev - 1);
     const int nr = D.bupd_nr;
+    NvtxRange nv(forward ? "solve forward" : "solve backward");
     if (forward) {
       // forward sweep, deepest level first (mf_forward, multifrontal.hpp:507-567)
       for (int L = hi; L >= lo; L--) {

@@ -291,6 +291,7 @@ namespace hssmf_b200 {
       std::chrono::steady_clock::time_point t0;
       int prev_phase;
       Ph(HssImpl* hh, int i) : h(hh), id(i), f0(hh->flops) {
+        nvtxRangePushA(hss_phase_name(i));
         prev_phase = probe_phase();
         probe_phase() = i;
         if (!g_phase_timing) return;
@@ -299,6 +300,7 @@ namespace hssmf_b200 {
         HSSMF_CUDA(cudaEventRecord(a, h->s));
       }
       ~Ph() {
+        nvtxRangePop();
         probe_phase() = prev_phase;
         if (!a) return;
         h->ph_host[id] +=

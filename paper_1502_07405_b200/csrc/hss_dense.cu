@@ -5,6 +5,8 @@
 #include "common.cuh"
 #include "hss.hpp"
 
+#include <stdexcept>
+
 namespace hssmf_b200 {
 
   struct DenseHss::Impl {
@@ -32,6 +34,43 @@ namespace hssmf_b200 {
 
   void DenseHss::run(const double* a, int lda, int n, int leaf, double eps, int d0, int dd, int p,
                      int max_rank, bool on_device) {
+    const ClusterTree ct = ClusterTree::balanced(n, leaf);
+    std::vector<int> b, e, c0, c1;
+    for (const auto& c : ct.nodes) {
+      b.push_back(c.begin);
+      e.push_back(c.end);
+      c0.push_back(c.child0);
+      c1.push_back(c.child1);
+    }
+    run_tree(a, lda, n, (int)ct.nodes.size(), b.data(), e.data(), c0.data(), c1.data(), eps, d0,
+             dd, p, max_rank, on_device);
+  }
+
+  void DenseHss::run_tree(const double* a, int lda, int n, int nnodes, const int* begin,
+                          const int* end, const int* child0, const int* child1, double eps,
+                          int d0, int dd, int p, int max_rank, bool on_device) {
+    // the tree must be a postorder binary partition of [0, n) (ClusterTree,
+    // cluster_tree.hpp:12-97): checked here, the compression trusts it
+    if (nnodes < 1 || begin[nnodes - 1] != 0 || end[nnodes - 1] != n)
+      throw std::invalid_argument("hss_compress: cluster tree root must span [0, n)");
+    ClusterTree ct;
+    ct.nodes.resize(nnodes);
+    for (int i = 0; i < nnodes; i++) {
+      auto& c = ct.nodes[i];
+      c.begin = begin[i];
+      c.end = end[i];
+      c.child0 = child0[i];
+      c.child1 = child1[i];
+      if ((c.child0 < 0) != (c.child1 < 0) || c.child0 >= i || c.child1 >= i || c.end < c.begin)
+        throw std::invalid_argument("hss_compress: cluster tree not postorder binary");
+      if (c.child0 >= 0) {
+        const auto& l = ct.nodes[c.child0];
+        const auto& r = ct.nodes[c.child1];
+        if (l.begin != c.begin || l.end != r.begin || r.end != c.end)
+          throw std::invalid_argument("hss_compress: children must split the parent range");
+        ct.nodes[c.child0].parent = ct.nodes[c.child1].parent = i;
+      }
+    }
     auto& D = *d_;
     HSSMF_CUDA(cudaSetDevice(D.device));
     D.n = n;
@@ -54,7 +93,7 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaEventCreate(&e2));
     D.h = std::make_unique<HssMatrixDev>(D.s);
     HSSMF_CUDA(cudaEventRecord(e0, D.s));
-    D.h->compress(D.A, n, ClusterTree::balanced(n, leaf), seeds, o);
+    D.h->compress(D.A, n, ct, seeds, o);
     HSSMF_CUDA(cudaEventRecord(e1, D.s));
     D.h->ulv_full();
     HSSMF_CUDA(cudaEventRecord(e2, D.s));

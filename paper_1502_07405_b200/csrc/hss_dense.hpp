@@ -12,6 +12,10 @@ namespace hssmf_b200 {
     ~DenseHss();
     void run(const double* a, int lda, int n, int leaf, double eps, int d0, int dd, int p,
              int max_rank, bool on_device);
+    // any postorder cluster tree over [0, n) (root last)
+    void run_tree(const double* a, int lda, int n, int nnodes, const int* begin, const int* end,
+                  const int* child0, const int* child1, double eps, int d0, int dd, int p,
+                  int max_rank, bool on_device);
     void solve(double* b, int ldb, int nrhs, bool on_device);
     void ranks(std::vector<int>& u, std::vector<int>& v) const;
     int rounds() const;

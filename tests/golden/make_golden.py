@@ -47,8 +47,28 @@ def host_info():
     return info
 
 
+def run_dense(name, cfg, threads, out_dir):
+    """BASELINE config 2: standalone dense HSS (hss_compress.hpp:373-383 +
+    ulv_factor / UlvFactors::solve) on A_ij = 1/(1+|i-j|) + 4 delta_ij"""
+    from paper_1502_07405_b200.problems import dense_c2
+    ref.set_threads(threads)
+    a = dense_c2(cfg.k)
+    h = ref.DenseHss(a, leaf=cfg.leaf, eps=cfg.eps, d0=cfg.d0, dd=cfg.dd, p=cfg.p)
+    b = x_true(cfg.k, 1)
+    x = h.solve(b)[:, 0]
+    relres = np.linalg.norm(a @ x - b) / np.linalg.norm(b)
+    out = dict(name=name, n=cfg.k, threads=threads, u_rank=h.u_rank, v_rank=h.v_rank,
+               rounds=h.rounds, d_final=h.d_final, compress_s=h.t_compress, ulv_s=h.t_ulv,
+               relres=relres, x=x, host=str(host_info()))
+    np.savez_compressed(os.path.join(out_dir, f"ref_{name}.npz"), **out)
+    print(f"{name}: compress {h.t_compress:.2f}s ulv {h.t_ulv:.3f}s rounds {h.rounds} d_final "
+          f"{h.d_final} max rank {int(h.u_rank[:-1].max())} relres {relres:.3e}", flush=True)
+
+
 def run(name, threads, out_dir):
     cfg = CONFIGS[name]
+    if cfg.kind == "dense":
+        return run_dense(name, cfg, threads, out_dir)
     ref.set_threads(threads)
     t0 = time.time()
     o = ordered(cfg)

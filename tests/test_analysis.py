@@ -25,6 +25,19 @@ def test_pipeline_bit_exact(oracle, kind, k, nd_leaf):
         assert np.array_equal(getattr(op.t, f), getattr(o, f)), f
 
 
+def test_c5_analysis_bit_exact(oracle):
+    # the bench workload's integer structure (BASELINE config 5: P3D 128^3,
+    # ND leaf 32): permutation, CSR, tree and upd sets identical to the
+    # reference's
+    op = P.ordered_grid("p3d", 128, 32)
+    o = oracle.ordered_grid("p3d", 128, 32)
+    assert np.array_equal(op.perm, o.perm)
+    for mine, theirs in zip(op.a.arrays(), (o.ptr, o.ind, o.val)):
+        assert np.array_equal(mine, theirs)
+    for f in TREE_FIELDS:
+        assert np.array_equal(getattr(op.t, f), getattr(o, f)), f
+
+
 def test_grid_generator_values_bitwise(oracle):
     for kind in ["p2d", "p3d", "c2d", "c3d"]:
         g = P.generate_grid_problem(kind, 9, 1e-3)

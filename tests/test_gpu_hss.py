@@ -167,6 +167,23 @@ def test_dense_c2_reduced_size_vs_reference(oracle):
     assert res <= 10 * max(rres, 1e-15)
 
 
+def test_dense_c2_full_size_vs_golden():
+    # BASELINE config 2 at its stated size: N = 16384, leaf 128, eps 1e-8
+    # (hss_compress.hpp:373-383); reference: tests/golden/ref_c2.npz
+    g = np.load(os.path.join(GOLD, "ref_c2.npz"))
+    n = int(g["n"])
+    a = dense_c2(n)
+    h = P.hss_compress(a, 128, hopts(eps=1e-8))
+    assert h.rounds == int(g["rounds"]) and h.d_final == int(g["d_final"])
+    assert ranks_close(h.u_rank[:-1], g["u_rank"][:-1])
+    assert ranks_close(h.v_rank[:-1], g["v_rank"][:-1])
+    b = x_true(n, 1)
+    x = h.solve(b)
+    res = np.linalg.norm(a @ x - b) / np.linalg.norm(b)
+    assert res <= 10 * float(g["relres"])
+    assert np.linalg.norm(x - g["x"]) / np.linalg.norm(g["x"]) <= 1e-6
+
+
 # ---------------------------------------------------------------- multifrontal
 def run_mf(kind, k, nd_leaf, **so):
     op = P.ordered_grid(kind, k, nd_leaf)
