@@ -712,6 +712,13 @@ def main():
     dom = [e for e in roofs if e.get("bound") in ("tensor", "hbm")]
     roof = dict(dom[0]) if dom else {"kernel": None}
     flops_total = sum(k["flops"] for k in ks)
+    # the reference's own per-front cost model over the fronts this run
+    # factored (FrontStat.flops, multifrontal.hpp:389-396, 432-445: dense
+    # 2ns^3/3 + 2ns^2 nu + 2ns nu^2, HSS 4 m^2 d_final + 8 m r^2 with this run's
+    # ranks and d_final): the algorithmic work of the step beside the executed
+    # flops (which include the dense-front sampling and densified updates the
+    # reference does not perform)
+    model_flops = float(np.asarray(ep.flops, np.float64).sum()) if hasattr(ep, "flops") else None
 
     # the solve's HBM roofline: every stored factor scalar is read once per
     # solve (the forward sweep reads L / L21 and the ULV lower factors, the
@@ -737,6 +744,9 @@ def main():
         "relres": relres,
         "gmres_preconditioned": gm,
         "fp64_tflops_step": flops_total / (ms * 1e-3) / 1e12,
+        "flops_per_step": {"executed": flops_total, "reference_front_model": model_flops,
+                           "reference_model_tflops": (model_flops / (ms * 1e-3) / 1e12
+                                                      if model_flops else None)},
         "e2e": {"value": e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),

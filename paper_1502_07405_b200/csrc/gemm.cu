@@ -6,6 +6,7 @@
 // owning problem is found by binary search over the tile prefix.
 #include "gemm.cuh"
 
+#include <cstdlib>
 #include <cstring>
 
 
@@ -13,9 +14,16 @@ namespace hssmf_b200 {
 
   namespace {
     constexpr int BM = kGemmBM, BN = kGemmBN, BK = 16, STAGES = 3, THREADS = 128;
-    constexpr int SA = BM + 4;  // A tile stored [k][m], conflict-free fragment loads
-    constexpr int SB = BK + 4;  // B tile stored [n][k]
-    constexpr int SMEM = STAGES * (BK * SA + BN * SB) * 8;
+    // shared memory of a TM x TN tile: A stored [k][m] (ld TM + 4), B stored
+    // [n][k] (ld BK + 4): conflict-free fragment loads
+    template<int TM, int TN> constexpr int smem_of() {
+      return STAGES * (BK * (TM + 4) + TN * (BK + 4)) * 8;
+    }
+    constexpr int SMEM = smem_of<BM, BN>();
+    // small batches (fewer 64 x 64 tiles than two per SM) run 32 x 32 tiles:
+    // four times the CTAs for launches that cannot fill the GPU otherwise
+    constexpr int SM_BM = 32, SM_BN = 32;
+    constexpr int SMEM_SMALL = smem_of<SM_BM, SM_BN>();
 
     // descriptors passed by value as a __grid_constant__ kernel parameter:
     // a dynamic-phase launch then needs no separate descriptor upload
@@ -36,10 +44,14 @@ namespace hssmf_b200 {
       return lo;
     }
 
-    // one 64 x 64 output tile t of problem P
-    template<bool TA, bool TB>
+    // one TM x TN output tile t of problem P (4 warps in a 2 x 2 grid of
+    // (TM/2) x (TN/2) warp tiles)
+    template<bool TA, bool TB, int TM = BM, int TN = BN>
     __device__ __forceinline__ void gemm_tile(const GemmProblem& P, int t, double alpha,
                                               double beta) {
+      constexpr int BM = TM, BN = TN;
+      constexpr int SA = BM + 4, SB = BK + 4;
+      constexpr int MI = BM / 16, NJ = BN / 16;  // 8 x 8 DMMA tiles per warp
       extern __shared__ __align__(16) double gsm[];
       double (*As)[BK * SA] = reinterpret_cast<double (*)[BK * SA]>(gsm);
       double (*Bs)[BN * SB] = reinterpret_cast<double (*)[BN * SB]>(gsm + STAGES * BK * SA);
@@ -47,17 +59,18 @@ namespace hssmf_b200 {
       if (P.skip && __ldcg(P.skip)) return;
       const int tiles_m = (P.m + BM - 1) / BM;
       const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
-      if (P.lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
+      // lower-triangle problems: the 64 x 64 blocks on or below the diagonal
+      if (P.lower && (n0 >> 6) > (m0 >> 6)) return;
       const int K = P.k;
 
       const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
       const int wm = warp & 1, wn = warp >> 1;
 
-      double acc[4][4][2];
+      double acc[MI][NJ][2];
 #pragma unroll
-      for (int i = 0; i < 4; i++)
+      for (int i = 0; i < MI; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
       auto load_stage = [&](int st, int k0) {
         // A tile: BM x BK logical (rows m, cols k)
@@ -94,7 +107,7 @@ namespace hssmf_b200 {
         if (s < nk) load_stage(s, s * BK);
         cp_async_commit();
       }
-      const int am = wm * 32 + (lane >> 2), bn = wn * 32 + (lane >> 2), kq = lane & 3;
+      const int am = wm * (BM / 2) + (lane >> 2), bn = wn * (BN / 2) + (lane >> 2), kq = lane & 3;
       for (int kt = 0; kt < nk; kt++) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
@@ -107,29 +120,29 @@ namespace hssmf_b200 {
         const double* bs = Bs[kt % STAGES];
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-          double a[4], b[4];
+          double a[MI], b[NJ];
 #pragma unroll
-          for (int i = 0; i < 4; i++) a[i] = as[(kk + kq) * SA + am + i * 8];
+          for (int i = 0; i < MI; i++) a[i] = as[(kk + kq) * SA + am + i * 8];
 #pragma unroll
-          for (int j = 0; j < 4; j++) b[j] = bs[(bn + j * 8) * SB + kk + kq];
+          for (int j = 0; j < NJ; j++) b[j] = bs[(bn + j * 8) * SB + kk + kq];
 #pragma unroll
-          for (int i = 0; i < 4; i++)
+          for (int i = 0; i < MI; i++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) dmma8x8x4(acc[i][j], a[i], b[j]);
+            for (int j = 0; j < NJ; j++) dmma8x8x4(acc[i][j], a[i], b[j]);
         }
       }
       cp_async_wait<0>();
 
       // epilogue
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int r = m0 + wm * 32 + i * 8 + (lane >> 2);
+      for (int i = 0; i < MI; i++) {
+        const int r = m0 + wm * (BM / 2) + i * 8 + (lane >> 2);
         if (r >= P.m) continue;
 #pragma unroll
-        for (int j = 0; j < 4; j++)
+        for (int j = 0; j < NJ; j++)
 #pragma unroll
           for (int v = 0; v < 2; v++) {
-            const int c = n0 + wn * 32 + j * 8 + 2 * kq + v;
+            const int c = n0 + wn * (BN / 2) + j * 8 + 2 * kq + v;
             if (c >= P.n) continue;
             double* cp = P.C + r + (size_t)c * P.ldc;
             const double x = alpha * acc[i][j][v];
@@ -148,16 +161,17 @@ namespace hssmf_b200 {
     }
 
     // mixed batch: every problem carries its own transposes and alpha / beta
+    template<int TM, int TN>
     __global__ void __launch_bounds__(THREADS)
     gemm_param_kernel(const __grid_constant__ GemmParam b) {
       const int lo = find_problem(b.pre, b.nprob, blockIdx.x);
       const GemmProblem& P = b.p[lo];
       const int t = blockIdx.x - b.pre[lo];
       switch (P.trans) {
-        case 0: gemm_tile<false, false>(P, t, P.alpha, P.beta); break;
-        case 1: gemm_tile<true, false>(P, t, P.alpha, P.beta); break;
-        case 2: gemm_tile<false, true>(P, t, P.alpha, P.beta); break;
-        default: gemm_tile<true, true>(P, t, P.alpha, P.beta); break;
+        case 0: gemm_tile<false, false, TM, TN>(P, t, P.alpha, P.beta); break;
+        case 1: gemm_tile<true, false, TM, TN>(P, t, P.alpha, P.beta); break;
+        case 2: gemm_tile<false, true, TM, TN>(P, t, P.alpha, P.beta); break;
+        default: gemm_tile<true, true, TM, TN>(P, t, P.alpha, P.beta); break;
       }
     }
 
@@ -181,7 +195,8 @@ namespace hssmf_b200 {
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
       HSSMF_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      HSSMF_CUDA(cudaFuncSetAttribute(gemm_param_kernel<SM_BM, SM_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SMALL));
       });
     }
   }  // namespace
@@ -233,10 +248,12 @@ namespace hssmf_b200 {
     gemm_run_mixed(q, s);
   }
 
-  int gemm_splitk_factor(int m, int n, int k) {
-    // resident CTAs: 4 per SM (smem / registers of the 64 x 64 tile kernel)
-    const long long slots = 148LL * 4;
-    const long long tiles = (long long)ceil_div(m, BM) * ceil_div(n, BN);
+  int gemm_splitk_factor(int m, int n, int k, bool tma) {
+    // resident CTAs: 4 per SM for the 64 x 64 tile kernel, 1 per SM for the
+    // 128 x 128 TMA kernel
+    const long long slots = tma ? 148LL : 148LL * 4;
+    const long long tiles = tma ? (long long)ceil_div(m, 128) * ceil_div(n, 128)
+                                : (long long)ceil_div(m, BM) * ceil_div(n, BN);
     if (tiles >= 4 * slots || k < 2048) return 1;
     int best = 1;
     double best_eff = 0;
@@ -254,7 +271,9 @@ namespace hssmf_b200 {
   void gemm_run_splitk(const GemmProblem& p0, char ta, char tb, double alpha, double beta,
                        cudaStream_t s) {
     if (p0.m <= 0 || p0.n <= 0) return;
-    const int S = gemm_splitk_factor(p0.m, p0.n, p0.k);
+    GemmProblem pt = p0;
+    gemm_set_op(pt, ta, tb, alpha, beta);
+    const int S = gemm_splitk_factor(p0.m, p0.n, p0.k, gemm_tma_eligible(pt));
     if (S <= 1) {
       gemm_run_host({p0}, ta, tb, alpha, beta, s);
       return;
@@ -288,8 +307,21 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaFreeAsync(W, s));
   }
 
-  void gemm_run_mixed(const std::vector<GemmProblem>& p, cudaStream_t s) {
+  void gemm_run_mixed(const std::vector<GemmProblem>& p0, cudaStream_t s) {
+    // big aligned problems go to the TMA kernel, the rest stay here
+    std::vector<GemmProblem> big, p;
+    for (const auto& x : p0) (gemm_tma_eligible(x) ? big : p).push_back(x);
+    if (!big.empty()) gemm_tma_run(big, s);
+    if (p.empty()) return;
     set_gemm_attrs();
+    // tile size of the launch: 32 x 32 when the whole list has fewer 64 x 64
+    // tiles than two per SM (latency-bound batches of the adaptive rounds)
+    long long t64 = 0;
+    for (const auto& x : p)
+      if (x.m > 0 && x.n > 0) t64 += (long long)ceil_div(x.m, BM) * ceil_div(x.n, BN);
+    static const bool no_small = getenv("HSSMF_GEMM_NO_SMALL") != nullptr;
+    const bool small = !no_small && t64 < 2 * 148;
+    const int tm = small ? SM_BM : BM, tn = small ? SM_BN : BN;
     GemmParam b;
     b.nprob = 0;
     b.pre[0] = 0;
@@ -311,7 +343,8 @@ namespace hssmf_b200 {
         pr.tiles = tiles;
         pr.kmax = km;
         pr.nprob = b.nprob;
-        gemm_param_kernel<<<tiles, THREADS, SMEM, s>>>(b);
+        if (small) gemm_param_kernel<SM_BM, SM_BN><<<tiles, THREADS, SMEM_SMALL, s>>>(b);
+        else gemm_param_kernel<BM, BN><<<tiles, THREADS, SMEM, s>>>(b);
         HSSMF_LAUNCH_CHECK();
       }
       b.nprob = 0;
@@ -322,7 +355,7 @@ namespace hssmf_b200 {
       if (x.m <= 0 || x.n <= 0) continue;
       if (b.nprob == kParamProbs) flush();
       b.p[b.nprob] = x;
-      b.pre[b.nprob + 1] = b.pre[b.nprob] + ceil_div(x.m, BM) * ceil_div(x.n, BN);
+      b.pre[b.nprob + 1] = b.pre[b.nprob] + ceil_div(x.m, tm) * ceil_div(x.n, tn);
       b.nprob++;
     }
     flush();

@@ -68,10 +68,16 @@ namespace hssmf_b200 {
   void gemm_run_host(const std::vector<GemmProblem>& p, char ta, char tb, double alpha,
                      double beta, cudaStream_t s);
   void gemm_run_mixed(const std::vector<GemmProblem>& p, cudaStream_t s);
+  // TMA-fed 128 x 128 DMMA kernel (gemm_tma.cu) for big problems whose A and
+  // B are 16-byte aligned with even leading dimensions; gemm_run_mixed routes
+  // eligible problems there by itself
+  bool gemm_tma_eligible(const GemmProblem& g);
+  void gemm_tma_run(const std::vector<GemmProblem>& p, cudaStream_t s);
+
   // one large-K problem with few output tiles: split-K over extra CTAs to fill
   // the resident-CTA waves, partial products reduced in a fixed order
   // (deterministic); falls back to a plain launch when splitting does not pay
-  int gemm_splitk_factor(int m, int n, int k);
+  int gemm_splitk_factor(int m, int n, int k, bool tma = false);
   void gemm_run_splitk(const GemmProblem& p, char ta, char tb, double alpha, double beta,
                        cudaStream_t s);
 

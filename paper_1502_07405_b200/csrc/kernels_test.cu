@@ -1,5 +1,7 @@
 #include "kernels_test.hpp"
 
+#include <cstring>
+
 #include <cstdlib>
 #include <stdexcept>
 #include <vector>
@@ -162,13 +164,22 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemcpy(D.p, p.data(), sizeof(GemmProblem), cudaMemcpyHostToDevice));
     HSSMF_CUDA(cudaMemcpy((char*)D.p + sizeof(GemmProblem), pre.data(), pre.size() * 4, cudaMemcpyHostToDevice));
     GemmBatchDev b{D.as<GemmProblem>(), (const int*)((char*)D.p + sizeof(GemmProblem)), 1, pre.back()};
-    gemm_run(b, ta, tb, 1.0, 1.0, 0);
+    // HSSMF_BENCH_PATH=mixed: the dynamic-batch entry (TMA kernel for
+    // eligible problems), =splitk: the split-K entry of the sampling products
+    const char* path = getenv("HSSMF_BENCH_PATH");
+    const int mode = !path ? 0 : !strcmp(path, "mixed") ? 1 : !strcmp(path, "splitk") ? 2 : 0;
+    auto run = [&] {
+      if (mode == 1) gemm_run_host(p, ta, tb, 1.0, 1.0, 0);
+      else if (mode == 2) gemm_run_splitk(p[0], ta, tb, 1.0, 1.0, 0);
+      else gemm_run(b, ta, tb, 1.0, 1.0, 0);
+    };
+    run();
     HSSMF_CUDA(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     HSSMF_CUDA(cudaEventCreate(&e0));
     HSSMF_CUDA(cudaEventCreate(&e1));
     HSSMF_CUDA(cudaEventRecord(e0, 0));
-    for (int i = 0; i < iters; i++) gemm_run(b, ta, tb, 1.0, 1.0, 0);
+    for (int i = 0; i < iters; i++) run();
     HSSMF_CUDA(cudaEventRecord(e1, 0));
     HSSMF_CUDA(cudaEventSynchronize(e1));
     float ms = 0;

@@ -13,7 +13,11 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (64, 64, 16), (130, 67, 45),
                                    (257, 129, 300),
                                    # split-K (few output tiles, long K): the HSS sampling shape
-                                   (700, 96, 5003), (200, 128, 2048)])
+                                   (700, 96, 5003), (200, 128, 2048),
+                                   # TMA kernel (even leading dimensions): edges
+                                   # by zero fill, split-K, several k-tiles
+                                   (96, 96, 32), (258, 130, 302), (1000, 998, 46),
+                                   (640, 128, 4096), (384, 256, 1024)])
 def test_gemm_matches_fp64(ta, tb, m, n, k):
     rng = np.random.default_rng(m * 1000 + n * 10 + k)
     a = rng.standard_normal((m, k) if ta == "N" else (k, m))
