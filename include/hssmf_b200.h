@@ -239,6 +239,18 @@ int hssmf_hss_dense_tree(int device, const double* a, int lda, int n, int nnodes
                          hssmf_hss** out, hssmf_status* st);
 int hssmf_hss_info(const hssmf_hss* h, int* u_rank, int* v_rank, int* rounds, int* d_final,
                    double* compress_ms, double* ulv_ms);
+/* HssMatrix::matvec (hss_matrix.hpp:234-249, mv_up/mv_down :349-413):
+ * y = op(A_hss) x on the subtree of cluster node `root` (-1: whole matrix),
+ * op 'N', 'T' or 'C' (= 'T' for real data); x is nrows x nc with nrows the
+ * node's size (else HSSMF_ERR_SHAPE, the reference's IoError) */
+int hssmf_hss_matvec(hssmf_hss* h, char op, int root, const double* x, int ldx, int nrows,
+                     int nc, double* y, int ldy, int on_device, hssmf_status* st);
+/* HssMatrix::extract (hss_matrix.hpp:261-280, ex_up/ex_down :425-506):
+ * out (ni x nj, ld ni) = A_hss(rows, cols) for index lists in any order (the
+ * reference requires sorted lists); out-of-range indices ->
+ * HSSMF_ERR_SHAPE. leaf_visits (optional) = leaves the pruned traversal read */
+int hssmf_hss_extract(hssmf_hss* h, const int* rows, int ni, const int* cols, int nj,
+                      double* out, int on_device, long long* leaf_visits, hssmf_status* st);
 /* UlvFactors::solve (hss_ulv.hpp:150-176) */
 int hssmf_hss_solve(hssmf_hss* h, double* b, int ldb, int nrhs, int on_device,
                     hssmf_status* st);

@@ -372,3 +372,35 @@ def cluster_front(ns, nu, leaf):
     arr = [np.zeros(nn, np.int32) for _ in range(5)]
     L.ref_cluster_front(ns, nu, leaf, *[a.ctypes.data for a in arr])
     return arr
+
+
+def stats_strings(s, include_per_front=True):
+    """the reference's stats_to_json / stats_csv_header / stats_csv_row
+    (src/stats.cpp:37-123) for a RunStats-like object (fields of
+    paper_1502_07405_b200.stats.RunStats; its rank_guard is passed as the
+    options' max_rank, which resolves to itself)"""
+    L = lib()
+    ints = np.array([s.n, s.nnz, s.ls, s.leaf, s.d0, s.dd, s.p, s.min_hss, s.rank_guard,
+                     s.threads, s.restart, s.maxit, s.nd_leaf, s.factor_flops, s.solve_flops,
+                     s.factor_nnz, s.factor_nnz_bytes, s.peak_bytes, s.max_rank, s.fronts,
+                     s.hss_fronts, s.hss_fallbacks, s.tree_depth, s.iterations,
+                     1 if s.converged else 0], np.int64)
+    reals = np.array([s.eps, s.rtol, s.atol, s.t_analysis, s.t_factor, s.t_solve, s.t_total,
+                      s.relres, s.absres], np.float64)
+    pf = np.array([[f["id"], f["level"], f["dim"], f["sep"], f["rank"], f["flops"]]
+                   for f in s.per_front], np.int64).reshape(-1, 6)
+    types = (C.c_char_p * max(1, len(s.per_front)))(*[f["type"].encode() for f in s.per_front])
+    fn = L.ref_stats
+    fn.restype = C.c_longlong
+    fn.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_void_p, C.c_void_p, C.c_char_p,
+                   C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_char_p,
+                   C.c_longlong]
+    args = [s.source.encode(), 1 if s.strategy == "graph" else 0, s.mode.encode(),
+            ints.ctypes.data, reals.ctypes.data, s.method.encode(), s.error.encode(),
+            len(s.per_front), pf.ctypes.data if len(pf) else None, types,
+            1 if include_per_front else 0]
+    need = fn(*args, None, 0)
+    buf = C.create_string_buffer(int(need))
+    fn(*args, buf, need)
+    parts = buf.raw[:need].split(b"\0")
+    return parts[0].decode(), parts[1].decode(), parts[2].decode()

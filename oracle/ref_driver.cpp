@@ -47,6 +47,7 @@
 #include "hssmf/solver_options.hpp"
 #include "hssmf/sparse_matrix.hpp"
 #include "hssmf/task_parallel.hpp"
+#include "hssmf/stats.hpp"
 
 using namespace hssmf;
 
@@ -501,6 +502,79 @@ int ref_cluster_front(int ns, int nu, int leaf, int* begin, int* end, int* c0, i
       parent[i] = t.node(i).parent;
     }
   return t.size();
+}
+
+// stats_to_json / stats_csv_header / stats_csv_row (src/stats.cpp:37-123) of
+// a RunStats given field by field: ints = {n, nnz, ls, leaf, d0, dd, p,
+// min_hss, max_rank, threads, restart, maxit, nd_leaf, factor_flops,
+// solve_flops, factor_nnz, factor_nnz_bytes, peak_bytes, max_rank_obs, fronts,
+// hss_fronts, hss_fallbacks, tree_depth, iterations, converged}; reals = {eps,
+// rtol, atol, t_analysis, t_factor, t_solve, t_total, relres, absres};
+// per-front rows pf = {id, level, dim, sep, rank, flops} x npf. Returns the
+// bytes needed (json + csv header + csv row, NUL-separated).
+long long ref_stats(const char* source, int strategy_graph, const char* mode, const long long* in,
+                    const double* re, const char* method, const char* error, int npf,
+                    const long long* pf, const char* const* pf_type, int include_pf, char* out,
+                    long long cap) {
+  RunStats s;
+  s.source = source;
+  s.opts.strategy = strategy_graph ? OrderingStrategy::Graph : OrderingStrategy::Geometric;
+  s.opts.mode = parse_solver_mode(mode);
+  s.n = (int)in[0];
+  s.nnz = in[1];
+  s.opts.ls = (int)in[2];
+  s.opts.leaf = (int)in[3];
+  s.opts.d0 = (int)in[4];
+  s.opts.dd = (int)in[5];
+  s.opts.p = (int)in[6];
+  s.opts.min_hss = (int)in[7];
+  s.opts.max_rank = (int)in[8];
+  s.opts.threads = (int)in[9];
+  s.opts.restart = (int)in[10];
+  s.opts.maxit = (int)in[11];
+  s.opts.nd_leaf = (int)in[12];
+  s.factor_flops = in[13];
+  s.solve_flops = in[14];
+  s.factor_nnz = in[15];
+  s.factor_nnz_bytes = in[16];
+  s.peak_bytes = in[17];
+  s.max_rank = (int)in[18];
+  s.fronts = (int)in[19];
+  s.hss_fronts = (int)in[20];
+  s.hss_fallbacks = (int)in[21];
+  s.tree_depth = (int)in[22];
+  s.iterations = (int)in[23];
+  s.converged = in[24] != 0;
+  s.opts.eps = re[0];
+  s.opts.rtol = re[1];
+  s.opts.atol = re[2];
+  s.t_analysis = re[3];
+  s.t_factor = re[4];
+  s.t_solve = re[5];
+  s.t_total = re[6];
+  s.relres = re[7];
+  s.absres = re[8];
+  s.method = method;
+  s.error = error;
+  for (int q = 0; q < npf; q++) {
+    FrontStat f;
+    f.id = (int)pf[6 * q];
+    f.level = (int)pf[6 * q + 1];
+    f.dim = (int)pf[6 * q + 2];
+    f.sep = (int)pf[6 * q + 3];
+    f.rank = (int)pf[6 * q + 4];
+    f.flops = pf[6 * q + 5];
+    f.type = pf_type[q];
+    s.per_front.push_back(f);
+  }
+  std::string all = stats_to_json(s, include_pf != 0);
+  all.push_back('\0');
+  all += stats_csv_header();
+  all.push_back('\0');
+  all += stats_csv_row(s);
+  all.push_back('\0');
+  if ((long long)all.size() <= cap) std::memcpy(out, all.data(), all.size());
+  return (long long)all.size();
 }
 
 }  // extern "C"

@@ -104,6 +104,10 @@ _SIGS = {
     "hssmf_hss_dense_tree": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp,
                                        C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.POINTER(vp), C.POINTER(Status)]),
+    "hssmf_hss_matvec": (C.c_int, [vp, C.c_char, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp,
+                                   C.c_int, C.c_int, C.POINTER(Status)]),
+    "hssmf_hss_extract": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int,
+                                    C.POINTER(C.c_longlong), C.POINTER(Status)]),
     "hssmf_hss_info": (C.c_int, [vp, vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "hssmf_hss_solve": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Status)]),

@@ -642,6 +642,31 @@ class HssFactors:
     def solve_device(self, ptr, ldb, nrhs):
         _call("hssmf_hss_solve", self._h, C.c_void_p(ptr), int(ldb), int(nrhs), 1)
 
+    def matvec(self, op, x, root=-1):
+        """HssMatrix::matvec_new (hss_matrix.hpp:234-249): op(A_hss) x on the
+        subtree of cluster node `root` (-1: the whole matrix); op 'N', 'T' or
+        'C'. Raises IoError when x's rows do not match the node."""
+        X = np.array(x, dtype=np.float64, order="F", copy=True)
+        X2 = X.reshape(-1, 1) if X.ndim == 1 else X
+        Y = np.zeros_like(X2, order="F")
+        _call("hssmf_hss_matvec", self._h, op.encode()[:1], int(root),
+              X2.ctypes.data_as(C.c_void_p), max(1, X2.shape[0]), X2.shape[0], X2.shape[1],
+              Y.ctypes.data_as(C.c_void_p), max(1, X2.shape[0]), 0)
+        return Y.reshape(X.shape)
+
+    def extract(self, rows, cols):
+        """HssMatrix::extract (hss_matrix.hpp:261-280): A_hss(rows, cols) for
+        index lists in any order; returns (block, leaves visited)"""
+        ri = np.ascontiguousarray(rows, np.int32)
+        ci = np.ascontiguousarray(cols, np.int32)
+        out = np.zeros((len(ri), len(ci)), order="F")
+        v = C.c_longlong()
+        _call("hssmf_hss_extract", self._h, ri.ctypes.data_as(C.c_void_p), len(ri),
+              ci.ctypes.data_as(C.c_void_p), len(ci), out.ctypes.data_as(C.c_void_p), 0,
+              C.byref(v))
+        self.leaf_visits = v.value
+        return out
+
     def __del__(self):
         try:
             if self._h:

@@ -567,6 +567,25 @@ int hssmf_hss_dense_tree(int device, const double* a, int lda, int n, int nnodes
   return rc;
 }
 
+int hssmf_hss_matvec(hssmf_hss* h, char op, int root, const double* x, int ldx, int nrows,
+                     int nc, double* y, int ldy, int on_device, hssmf_status* st) {
+  return guard(st, [&] {
+    if (op != 'N' && op != 'T' && op != 'C') throw std::invalid_argument("hss matvec: op must be N, T or C");
+    if (nrows != h->h->node_size(root))
+      throw std::invalid_argument("hss matvec: x rows do not match the cluster node");
+    if (ldx < nrows || ldy < nrows) throw std::invalid_argument("hss matvec: leading dimension");
+    h->h->matvec(op == 'N' ? 'N' : 'T', root, x, ldx, nc, y, ldy, on_device != 0);
+  });
+}
+
+int hssmf_hss_extract(hssmf_hss* h, const int* rows, int ni, const int* cols, int nj,
+                      double* out, int on_device, long long* leaf_visits, hssmf_status* st) {
+  return guard(st, [&] {
+    const long long v = h->h->extract(rows, ni, cols, nj, out, on_device != 0);
+    if (leaf_visits) *leaf_visits = v;
+  });
+}
+
 int hssmf_hss_info(const hssmf_hss* h, int* u_rank, int* v_rank, int* rounds, int* d_final,
                    double* compress_ms, double* ulv_ms) {
   std::vector<int> u, v;

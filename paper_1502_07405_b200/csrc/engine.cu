@@ -710,8 +710,29 @@ namespace hssmf_b200 {
     ho.max_rank = std::min(opt.resolved_max_rank(t.n), m);
     auto H = std::make_unique<HssMatrixDev>(st);
     bool fallback = false;
+    // the compression reads the front through TMA-fed GEMMs, which need an
+    // even leading dimension: an odd-sized front is compressed from a copy
+    // with ld m + 1 (one extra 16 B per element of traffic; the assembled F
+    // stays for the rank-guard fallback). Freed on every exit.
+    struct Pad {
+      double* p = nullptr;
+      cudaStream_t st;
+      ~Pad() {
+        if (p) cudaFreeAsync(p, st);
+      }
+    } pad{nullptr, st};
+    const double* Fc = F;
+    long long ldF = m;
+    static const bool no_pad = getenv("HSSMF_NO_TMA") != nullptr;
+    if ((m & 1) && !no_pad) {
+      ldF = m + 1;
+      HSSMF_CUDA(cudaMallocAsync((void**)&pad.p, (size_t)ldF * m * sizeof(double), st));
+      HSSMF_CUDA(cudaMemcpy2DAsync(pad.p, (size_t)ldF * sizeof(double), F, (size_t)m * sizeof(double),
+                                   (size_t)m * sizeof(double), m, cudaMemcpyDeviceToDevice, st));
+      Fc = pad.p;
+    }
     try {
-      H->compress(F, m, tree, seeds, ho);
+      H->compress(Fc, ldF, tree, seeds, ho);
       if (nu) H->ulv_partial(hf0[i].C, nu);
       else H->ulv_full();
     } catch (const HssRankError&) {

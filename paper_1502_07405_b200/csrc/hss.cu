@@ -18,6 +18,7 @@
 #include "hss_kernels.cuh"
 #include "gram_id.cuh"
 #include <exception>
+#include <stdexcept>
 #include "rng.cuh"
 #include "staging.cuh"
 #include "arena.cuh"
@@ -1750,9 +1751,271 @@ namespace hssmf_b200 {
       subtree(Rt.c0, set0);
       backward_set(set0, x1);
     }
+
+    // ---- HSS matvec and extraction on the device (HssMatrix::matvec /
+    // mv_up / mv_down, hss_matrix.hpp:234-249, 349-413; HssMatrix::extract /
+    // ex_up / ex_down, :261-280, 425-506). Both read the leaf D blocks, which
+    // live in the compressed matrix A (kept by the standalone dense HSS).
+    // dense nested-basis block Pi [I; E] (mt x r) of one node, row (U) or
+    // column (V) side (BasisId::dense, hss_matrix.hpp:61-67)
+    DBuf<double> basis_dense(const HssNode& N, bool vside) {
+      const bool v = vside && !sym;
+      DBuf<double> u;
+      const int mt = N.mt, r = N.r, k = mt - r;
+      u.alloc((size_t)mt * r + 1, s);
+      u.zero();
+      if (!r) return u;
+      std::vector<CopyDesc> c;
+      const int* perm = (v ? N.d_vp : N.d_up).p;
+      CopyDesc e1 = cd(one.p, 0, 0, nullptr, 0, nullptr, 0, u.p, mt, perm, 0, nullptr, 0, r, r);
+      e1.diag = 1;
+      c.push_back(e1);
+      if (k) c.push_back(cd((v ? N.Ev : N.Eu).p, 1, k, nullptr, 0, nullptr, 0, u.p, mt, perm + r, 0,
+                            nullptr, 0, k, r));
+      index_copy_run(c, s);
+      return u;
+    }
+
+    void need_dense(const char* what) const {
+      if (!A) throw std::invalid_argument(std::string(what) +
+                                          ": the leaf blocks were released with the front");
+    }
+
+    // y = op(A_hss) x on the subtree of node rt (op: 'N' or 'T'; 'C' is 'T'
+    // for real data); x, y: size(rt) x nc device blocks
+    void matvec(char op, int rt, const double* x, long long ldx, int nc, double* y,
+                long long ldy) {
+      need_dense("hss matvec");
+      const bool tr = op != 'N';
+      std::vector<int> pre;
+      subtree(rt, pre);  // preorder: parents before children
+      const int off = nodes[rt].begin;
+      std::vector<DBuf<double>> xh(nodes.size()), yh(nodes.size()), bu(nodes.size()),
+          bv(nodes.size());
+      for (int n : pre)
+        if (n != rt && nodes[n].r) {
+          bu[n] = basis_dense(nodes[n], tr);   // the down sweep's basis
+          bv[n] = basis_dense(nodes[n], !tr);  // the up sweep's basis
+        }
+      // up sweep (mv_up): xh = B^T [x(leaf) | xh_c0; xh_c1]
+      for (auto it = pre.rbegin(); it != pre.rend(); ++it) {
+        const int n = *it;
+        const auto& N = nodes[n];
+        if (n == rt || !N.r) continue;
+        xh[n].alloc((size_t)N.r * nc + 1, s);
+        if (N.leaf) {
+          gemm_run_host({{bv[n].p, x + (N.begin - off), xh[n].p, N.r, nc, N.mt, N.mt, (int)ldx, N.r}},
+                        'T', 'N', 1.0, 0.0, s);
+        } else {
+          const auto& a = nodes[N.c0];
+          const auto& b = nodes[N.c1];
+          std::vector<GemmProblem> g;
+          if (a.r) g.push_back({bv[n].p, xh[N.c0].p, xh[n].p, N.r, nc, a.r, N.mt, a.r, N.r});
+          if (b.r) {
+            GemmProblem q{bv[n].p + a.r, xh[N.c1].p, xh[n].p, N.r, nc, b.r, N.mt, b.r, N.r};
+            g.push_back(q);
+          }
+          // two accumulations into xh[n]: first overwrite, then add
+          if (g.empty()) xh[n].zero();
+          for (size_t q = 0; q < g.size(); q++) gemm_run_host({g[q]}, 'T', 'N', 1.0, q ? 1.0 : 0.0, s);
+        }
+      }
+      // down sweep (mv_down): couplings, then the parent's part through U
+      for (int n : pre) {
+        const auto& N = nodes[n];
+        if (!yh[n].p && n != rt && N.r) {
+          yh[n].alloc((size_t)N.r * nc + 1, s);
+          yh[n].zero();
+        }
+        if (N.leaf) continue;
+        const auto& a = nodes[N.c0];
+        const auto& b = nodes[N.c1];
+        for (int c : {N.c0, N.c1})
+          if (!yh[c].p && nodes[c].r) {
+            yh[c].alloc((size_t)nodes[c].r * nc + 1, s);
+            yh[c].zero();
+          }
+        std::vector<GemmProblem> g;
+        char tb = 'N';
+        if (a.r && b.r) {
+          if (!tr) {
+            g.push_back({N.B12.p, xh[N.c1].p, yh[N.c0].p, a.r, nc, b.r, a.r, b.r, a.r});
+            g.push_back({N.B21.p, xh[N.c0].p, yh[N.c1].p, b.r, nc, a.r, b.r, a.r, b.r});
+            gemm_run_host(g, 'N', tb, 1.0, 1.0, s);
+          } else {
+            g.push_back({N.B21.p, xh[N.c1].p, yh[N.c0].p, a.r, nc, b.r, b.r, b.r, a.r});
+            g.push_back({N.B12.p, xh[N.c0].p, yh[N.c1].p, b.r, nc, a.r, a.r, a.r, b.r});
+            gemm_run_host(g, 'T', tb, 1.0, 1.0, s);
+          }
+        }
+        if (n != rt && N.r) {
+          std::vector<GemmProblem> h;
+          if (a.r) h.push_back({bu[n].p, yh[n].p, yh[N.c0].p, a.r, nc, N.r, N.mt, N.r, a.r});
+          if (b.r) h.push_back({bu[n].p + a.r, yh[n].p, yh[N.c1].p, b.r, nc, N.r, N.mt, N.r, b.r});
+          gemm_run_host(h, 'N', 'N', 1.0, 1.0, s);
+        }
+      }
+      // leaves: y = op(D) x (+ B yh)
+      for (int n : pre) {
+        const auto& N = nodes[n];
+        if (!N.leaf) continue;
+        double* yl = y + (N.begin - off);
+        gemm_run_host({{N.D, x + (N.begin - off), yl, N.mt, nc, N.mt, (int)N.ldD, (int)ldx, (int)ldy}},
+                      tr ? 'T' : 'N', 'N', 1.0, 0.0, s);
+        if (n != rt && N.r)
+          gemm_run_host({{bu[n].p, yh[n].p, yl, N.mt, nc, N.r, N.mt, N.r, (int)ldy}}, 'N', 'N', 1.0,
+                        1.0, s);
+      }
+      stream_sync(s);
+    }
+
+    // out(q, p) = A_hss(I[q], J[p]) (out device, ld ni), any index order; only
+    // the leaves and nodes the sets touch are visited (ex_up / ex_down's
+    // pruning). Returns the number of leaves visited.
+    long long extract(const std::vector<int>& I, const std::vector<int>& J, double* out) {
+      need_dense("hss extract");
+      const int ni = (int)I.size(), nj = (int)J.size();
+      for (int v : I) if (v < 0 || v >= m) throw std::invalid_argument("hss extract: row index out of range");
+      for (int v : J) if (v < 0 || v >= m) throw std::invalid_argument("hss extract: column index out of range");
+      if (!ni || !nj) return 0;
+      // positions sorted by index: a node's share of a set is one contiguous
+      // run of the sorted order, child0's run before child1's
+      auto sorted = [](const std::vector<int>& v) {
+        std::vector<int> p(v.size());
+        std::iota(p.begin(), p.end(), 0);
+        std::stable_sort(p.begin(), p.end(), [&](int x, int y) { return v[x] < v[y]; });
+        return p;
+      };
+      const std::vector<int> pI = sorted(I), pJ = sorted(J);
+      auto range = [](const std::vector<int>& v, const std::vector<int>& p, int b, int e) {
+        const auto lo = std::lower_bound(p.begin(), p.end(), b, [&](int q, int x) { return v[q] < x; });
+        const auto hi = std::lower_bound(p.begin(), p.end(), e, [&](int q, int x) { return v[q] < x; });
+        return std::make_pair((int)(lo - p.begin()), (int)(hi - p.begin()));
+      };
+      IdxPool pool;
+      // device copies of the sorted positions and of the local indices
+      std::vector<int> liI(ni), liJ(nj);
+      for (int q = 0; q < ni; q++) liI[q] = I[pI[q]];
+      for (int q = 0; q < nj; q++) liJ[q] = J[pJ[q]];
+      const size_t oPI = pool.add(pI), oPJ = pool.add(pJ), oLI = pool.add(liI), oLJ = pool.add(liJ);
+      pool.upload(s);
+      long long visits = 0;
+      std::vector<DBuf<double>> urow(nodes.size()), vrow(nodes.size());
+      std::vector<char> have_u(nodes.size(), 0), have_v(nodes.size(), 0);
+      // rows of Ubig_n (side u) / Vbig_n at the set's indices inside node n:
+      // |set ∩ n| x r_n, stacked in sorted order (ex_up)
+      std::function<void(int, bool)> rows_of = [&](int n, bool vside) {
+        auto& have = vside ? have_v : have_u;
+        if (have[n]) return;
+        have[n] = 1;
+        const auto& N = nodes[n];
+        const auto& v = vside ? J : I;
+        const auto& p = vside ? pJ : pI;
+        const auto rg = range(v, p, N.begin, N.end);
+        const int cnt = rg.second - rg.first;
+        auto& out_n = (vside ? vrow : urow)[n];
+        out_n.alloc((size_t)cnt * N.r + 1, s);
+        if (!cnt || !N.r) return;
+        DBuf<double> B = basis_dense(N, vside);
+        if (N.leaf) {
+          visits++;
+          // rows (index - begin) of the dense leaf basis
+          const int* li = pool.at(vside ? oLJ : oLI) + rg.first;
+          // (a gather with an index list reads src[list[i]]: the basis pointer
+          // is shifted so that global row indices address it)
+          index_copy_run({cd(B.p - N.begin, 1, N.mt, li, 0, nullptr, 0, out_n.p, cnt, nullptr, 0,
+                             nullptr, 0, cnt, N.r)}, s);
+          return;
+        }
+        const auto& a = nodes[N.c0];
+        const auto& b = nodes[N.c1];
+        const auto ra = range(v, p, a.begin, a.end), rb = range(v, p, b.begin, b.end);
+        std::vector<GemmProblem> g;
+        if (ra.second > ra.first && a.r) {
+          rows_of(N.c0, vside);
+          g.push_back({(vside ? vrow : urow)[N.c0].p, B.p, out_n.p, ra.second - ra.first, N.r, a.r,
+                       ra.second - ra.first, N.mt, cnt});
+        }
+        if (rb.second > rb.first && b.r) {
+          rows_of(N.c1, vside);
+          g.push_back({(vside ? vrow : urow)[N.c1].p, B.p + a.r, out_n.p + (ra.second - ra.first),
+                       rb.second - rb.first, N.r, b.r, rb.second - rb.first, N.mt, cnt});
+        }
+        out_n.zero();  // a child without rank contributes 0 rows
+        gemm_run_host(g, 'N', 'N', 1.0, 0.0, s);
+      };
+      // ex_down: diagonal leaf blocks and the couplings of every node whose
+      // two children split a row and a column of the request
+      std::vector<CopyDesc> cp;
+      std::vector<DBuf<double>> tmp;
+      std::vector<int> stack{root};
+      while (!stack.empty()) {
+        const int n = stack.back();
+        stack.pop_back();
+        const auto& N = nodes[n];
+        const auto ri = range(I, pI, N.begin, N.end), rj = range(J, pJ, N.begin, N.end);
+        if (ri.second == ri.first || rj.second == rj.first) continue;  // pruned
+        if (N.leaf) {
+          visits++;
+          // D = A(leaf, leaf): gathered from A at global indices
+          cp.push_back(cd(A, 1, lda, pool.at(oLI) + ri.first, 0, pool.at(oLJ) + rj.first, 0, out, ni,
+                          pool.at(oPI) + ri.first, 0, pool.at(oPJ) + rj.first, 0,
+                          ri.second - ri.first, rj.second - rj.first));
+          continue;
+        }
+        const auto& a = nodes[N.c0];
+        const auto& b = nodes[N.c1];
+        for (int side = 0; side < 2; side++) {
+          const HssNode& X = side ? b : a;  // rows
+          const HssNode& Y = side ? a : b;  // columns
+          const int cx = side ? N.c1 : N.c0, cy = side ? N.c0 : N.c1;
+          const auto rx = range(I, pI, X.begin, X.end), ry = range(J, pJ, Y.begin, Y.end);
+          const int nx = rx.second - rx.first, ny = ry.second - ry.first;
+          if (!nx || !ny) continue;
+          DBuf<double> blk;
+          blk.alloc((size_t)nx * ny + 1, s);
+          if (!X.r || !Y.r) {
+            blk.zero();
+          } else {
+            rows_of(cx, false);
+            rows_of(cy, true);
+            // (Urows_x B) Vrows_y^T, B = B12 (side 0) or B21 (side 1)
+            DBuf<double> t;
+            t.alloc((size_t)nx * Y.r + 1, s);
+            gemm_run_host({{urow[cx].p, (side ? N.B21 : N.B12).p, t.p, nx, Y.r, X.r, nx, X.r, nx}},
+                          'N', 'N', 1.0, 0.0, s);
+            gemm_run_host({{t.p, vrow[cy].p, blk.p, nx, ny, Y.r, nx, ny, nx}}, 'N', 'T', 1.0, 0.0, s);
+          }
+          cp.push_back(cd(blk.p, 1, nx, nullptr, 0, nullptr, 0, out, ni, pool.at(oPI) + rx.first, 0,
+                          pool.at(oPJ) + ry.first, 0, nx, ny));
+          tmp.push_back(std::move(blk));
+        }
+        stack.push_back(N.c1);
+        stack.push_back(N.c0);
+      }
+      index_copy_run(cp, s);
+      stream_sync(s);
+      return visits;
+    }
   };
 
   HssMatrixDev::HssMatrixDev(cudaStream_t s) : d_(new HssImpl(s)) {}
+
+  void HssMatrixDev::matvec(char op, int root, const double* x, long long ldx, int nc, double* y,
+                            long long ldy) {
+    StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena, &d_->keep_arena);
+    d_->matvec(op, root < 0 ? d_->root : root, x, ldx, nc, y, ldy);
+  }
+  int HssMatrixDev::node_size(int node) const {
+    return d_->nodes[node < 0 ? d_->root : node].size();
+  }
+  long long HssMatrixDev::extract(const std::vector<int>& I, const std::vector<int>& J,
+                                  double* out) {
+    StagingScope sc(staging_for(d_->s));
+    ArenaScope as(&d_->arena, &d_->keep_arena);
+    return d_->extract(I, J, out);
+  }
   HssMatrixDev::~HssMatrixDev() = default;
 
   void HssMatrixDev::compress(const double* A, long long lda, const ClusterTree& tree,

@@ -99,6 +99,15 @@ namespace hssmf_b200 {
     void partial_forward(const double* b1, double* bupd);
     void partial_backward(double* x1, const double* x2);
 
+    // y = op(A_hss) x on the subtree of cluster node `root` (-1: the whole
+    // matrix), device blocks of size(root) x nc (HssMatrix::matvec,
+    // hss_matrix.hpp:234-249); needs the leaf blocks (before drop_dense)
+    void matvec(char op, int root, const double* x, long long ldx, int nc, double* y,
+                long long ldy);
+    int node_size(int node) const;  // rows of a cluster node (-1: the root)
+    // out (ni x nj, ld ni, device) = A_hss(I, J) for any index lists
+    // (HssMatrix::extract, hss_matrix.hpp:261-280); returns the leaves visited
+    long long extract(const std::vector<int>& I, const std::vector<int>& J, double* out);
     int rows() const;
     int rounds() const;
     int d_final() const;

@@ -124,6 +124,47 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaStreamSynchronize(D.s));
   }
 
+  int DenseHss::node_size(int root) const { return d_->h->node_size(root); }
+
+  void DenseHss::matvec(char op, int root, const double* x, int ldx, int nc, double* y, int ldy,
+                        bool on_device) {
+    auto& D = *d_;
+    HSSMF_CUDA(cudaSetDevice(D.device));
+    const int nr = D.h->node_size(root);
+    if (nc <= 0 || nr <= 0) return;
+    if (on_device) {
+      D.h->matvec(op, root, x, ldx, nc, y, ldy);
+      return;
+    }
+    double *dx = nullptr, *dy = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&dx, (size_t)nr * nc * sizeof(double), D.s));
+    HSSMF_CUDA(cudaMallocAsync((void**)&dy, (size_t)nr * nc * sizeof(double), D.s));
+    HSSMF_CUDA(cudaMemcpy2DAsync(dx, nr * sizeof(double), x, (size_t)ldx * sizeof(double),
+                                 nr * sizeof(double), nc, cudaMemcpyHostToDevice, D.s));
+    D.h->matvec(op, root, dx, nr, nc, dy, nr);
+    HSSMF_CUDA(cudaMemcpy2DAsync(y, (size_t)ldy * sizeof(double), dy, nr * sizeof(double),
+                                 nr * sizeof(double), nc, cudaMemcpyDeviceToHost, D.s));
+    HSSMF_CUDA(cudaFreeAsync(dx, D.s));
+    HSSMF_CUDA(cudaFreeAsync(dy, D.s));
+    HSSMF_CUDA(cudaStreamSynchronize(D.s));
+  }
+
+  long long DenseHss::extract(const int* I, int ni, const int* J, int nj, double* out,
+                              bool on_device) {
+    auto& D = *d_;
+    HSSMF_CUDA(cudaSetDevice(D.device));
+    std::vector<int> vi(I, I + ni), vj(J, J + nj);
+    if (on_device) return D.h->extract(vi, vj, out);
+    double* dout = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&dout, (size_t)ni * nj * sizeof(double) + 8, D.s));
+    const long long v = D.h->extract(vi, vj, dout);
+    HSSMF_CUDA(cudaMemcpyAsync(out, dout, (size_t)ni * nj * sizeof(double), cudaMemcpyDeviceToHost,
+                               D.s));
+    HSSMF_CUDA(cudaFreeAsync(dout, D.s));
+    HSSMF_CUDA(cudaStreamSynchronize(D.s));
+    return v;
+  }
+
   void DenseHss::ranks(std::vector<int>& u, std::vector<int>& v) const { d_->h->ranks(u, v); }
   int DenseHss::rounds() const { return d_->h->rounds(); }
   int DenseHss::d_final() const { return d_->h->d_final(); }

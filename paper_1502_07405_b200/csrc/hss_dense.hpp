@@ -17,6 +17,13 @@ namespace hssmf_b200 {
                   const int* child0, const int* child1, double eps, int d0, int dd, int p,
                   int max_rank, bool on_device);
     void solve(double* b, int ldb, int nrhs, bool on_device);
+    // y = op(A_hss) x on the subtree of cluster node `root` (-1: all);
+    // x is node_size(root) x nc
+    void matvec(char op, int root, const double* x, int ldx, int nc, double* y, int ldy,
+                bool on_device);
+    int node_size(int root) const;
+    // out (ni x nj, ld ni) = A_hss(I, J); returns the leaves visited
+    long long extract(const int* I, int ni, const int* J, int nj, double* out, bool on_device);
     void ranks(std::vector<int>& u, std::vector<int>& v) const;
     int rounds() const;
     int d_final() const;

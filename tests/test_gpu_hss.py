@@ -167,6 +167,64 @@ def test_dense_c2_reduced_size_vs_reference(oracle):
     assert res <= 10 * max(rres, 1e-15)
 
 
+def test_matvec_matches_dense_products():
+    # test_hss.cpp:256-278: N and C products, a subtree product sees only its
+    # diagonal block, shape mismatch -> IoError
+    n = 128
+    a = structured(n, 32, 5, 30.0, 41)
+    h = P.hss_compress(a, 32, hopts(eps=1e-12))
+    rng = np.random.default_rng(42)
+    x = rng.uniform(-1, 1, (n, 5))
+    rel = lambda g, w: np.linalg.norm(g - w) / np.linalg.norm(w)  # noqa: E731
+    assert rel(h.matvec("N", x), a @ x) <= 1e-12
+    assert rel(h.matvec("C", x), a.T @ x) <= 1e-12
+    assert rel(h.matvec("T", x), a.T @ x) <= 1e-12
+    # balanced(128, 32): postorder 0..6, root 6, root.child1 = 5 = [64, 128)
+    x1 = rng.uniform(-1, 1, (64, 2))
+    assert rel(h.matvec("N", x1, root=5), a[64:, 64:] @ x1) <= 1e-12
+    with pytest.raises(P.IoError):
+        h.matvec("N", rng.uniform(-1, 1, (n - 1, 1)))
+
+
+def test_matvec_is_linear():
+    # test_hss.cpp:280-295
+    n = 128
+    a = structured(n, 32, 4, 20.0, 51)
+    h = P.hss_compress(a, 32, hopts(eps=1e-10))
+    rng = np.random.default_rng(52)
+    x = rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, n)
+    lhs = h.matvec("N", 0.7 * x - 1.3 * y)
+    rhs = 0.7 * h.matvec("N", x) - 1.3 * h.matvec("N", y)
+    assert np.linalg.norm(lhs - rhs) / np.linalg.norm(rhs) <= 1e-13
+
+
+def test_extract_equals_reconstruction_and_prunes():
+    # test_hss.cpp:297-327: extract(all, all) is the reconstruction (here the
+    # HSS operator applied to the identity), index subsets in any order agree
+    # with it, a within-leaf entry touches one leaf and equals D exactly, an
+    # out-of-range index -> IoError
+    n = 64
+    a = structured(n, 16, 3, 15.0, 61)
+    h = P.hss_compress(a, 16, hopts(eps=1e-12))
+    allv = np.arange(n)
+    full = h.extract(allv, allv)
+    recon = h.matvec("N", np.eye(n))
+    nrm = np.linalg.norm(a)
+    assert np.abs(full - recon).max() <= 1e-13 * nrm
+    assert np.abs(full - a).max() <= 1e-10 * nrm
+    is_, js = [1, 7, 20, 33, 34, 57], [0, 15, 16, 40, 63]
+    sub = h.extract(is_, js)
+    assert np.abs(sub - full[np.ix_(is_, js)]).max() <= 1e-13 * nrm
+    # unsorted and repeated lists (the reference requires sorted ones)
+    iu, ju = [57, 1, 34, 7, 34], [63, 0, 40, 16, 15, 0]
+    assert np.abs(h.extract(iu, ju) - full[np.ix_(iu, ju)]).max() <= 1e-13 * nrm
+    d0 = h.extract([10], [11])
+    assert h.leaf_visits == 1 and d0[0, 0] == a[10, 11]
+    with pytest.raises(P.IoError):
+        h.extract([n], [0])
+
+
 def test_dense_c2_full_size_vs_golden():
     # BASELINE config 2 at its stated size: N = 16384, leaf 128, eps 1e-8
     # (hss_compress.hpp:373-383); reference: tests/golden/ref_c2.npz
