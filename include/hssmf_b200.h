@@ -307,6 +307,39 @@ long long hssmf_launch_count(void);
 
 const char* hssmf_version(void);
 
+/* ---- multi-GPU subtree partition ----
+ * One process per GPU. The elimination tree's 2^L subtrees at level
+ * L = log2(nranks) are factored independently (rank r owns the r-th); a front
+ * above level L belongs to the owner of its child0 subtree. Update blocks
+ * (factor), bupd (forward solve) and x(upd) (backward solve) cross ranks
+ * along tree edges only, through the caller's point-to-point transport
+ * (include/hssmf_b200/mgpu_nccl.hpp: ncclSend / ncclRecv over NVLink). Every
+ * rank calls the same entry points with the same matrix and tree. */
+typedef struct hssmf_transport {
+  void* ctx;
+  /* blocking: dev_buf (count doubles of device memory) may be reused on return */
+  int (*send)(void* ctx, const double* dev_buf, long long count, int peer);
+  /* blocking: the data has landed in dev_buf on return */
+  int (*recv)(void* ctx, double* dev_buf, long long count, int peer);
+} hssmf_transport;
+/* owner rank per front (nnodes) and the number of cross-rank tree edges */
+int hssmf_mgpu_partition(const hssmf_tree* t, int nranks, int* owner, int* nedges,
+                         hssmf_status* st);
+/* this rank's share of mf_factor (multifrontal.hpp:473-503) */
+int hssmf_mgpu_factor(int device, const hssmf_csr* a, const hssmf_tree* t,
+                      const hssmf_options* o, int rank, int nranks, const hssmf_transport* tr,
+                      hssmf_factors** out, hssmf_status* st);
+/* this rank's share of mf_solve (multifrontal.hpp:612-622) on a device x
+ * (n x nrhs, ld ldx) holding b on entry; on return x is correct on the
+ * separators of the fronts this rank owns */
+int hssmf_mgpu_solve(hssmf_factors* f, const hssmf_transport* tr, double* x, int ldx, int nrhs,
+                     hssmf_status* st);
+/* all nranks ranks in this process on one device (in-process mailbox): the
+ * partitioned factor + solve of the device block x (n x nrhs, ld n), b on
+ * entry, the assembled solution on return */
+int hssmf_mgpu_local(int device, const hssmf_csr* a, const hssmf_tree* t, const hssmf_options* o,
+                     int nranks, double* x, int nrhs, hssmf_status* st);
+
 #ifdef __cplusplus
 }
 #endif

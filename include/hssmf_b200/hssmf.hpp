@@ -142,61 +142,71 @@ namespace hssmf_b200 {
     std::int64_t nnz_ = 0;
   };
 
+  namespace detail {
+    // C-ABI copies of a reference-typed matrix and tree (RAII)
+    struct Inputs {
+      hssmf_csr* c = nullptr;
+      hssmf_tree* tr = nullptr;
+      Inputs() = default;
+      Inputs(const Inputs&) = delete;
+      Inputs& operator=(const Inputs&) = delete;
+      ~Inputs() {
+        if (tr) hssmf_tree_free(tr);
+        if (c) hssmf_csr_free(c);
+      }
+    };
+    template<class Sparse, class Tree>
+    void make_inputs(const Sparse& a, const Tree& t, Inputs& in) {
+      hssmf_status st{};
+      if (a.size() != t.n) throw IoError("mf factor: matrix and tree sizes differ");
+      check(hssmf_csr_create(a.size(), a.ptr().data(), a.ind().data(), a.val().data(), &in.c, &st), st);
+      const int nn = static_cast<int>(t.nodes.size());
+      std::vector<int> sb(nn), se(nn), c0(nn), c1(nn), pa(nn), up(nn + 1, 0), ui;
+      for (int i = 0; i < nn; i++) {
+        const auto& f = t.nodes[i];
+        sb[i] = f.sep_begin;
+        se[i] = f.sep_end;
+        c0[i] = f.child0;
+        c1[i] = f.child1;
+        pa[i] = f.parent;
+        ui.insert(ui.end(), f.upd.begin(), f.upd.end());
+        up[i + 1] = static_cast<int>(ui.size());
+      }
+      check(hssmf_tree_create(t.n, nn, sb.data(), se.data(), c0.data(), c1.data(), pa.data(),
+                              up.data(), ui.data(), &in.tr, &st), st);
+      // separator clusters from the reference's reorder_tree_separators
+      // (FrontNode::sep_clusters) travel with the tree
+      for (int i = 0; i < nn; i++) {
+        const auto& sc = t.nodes[i].sep_clusters;
+        if (sc.empty()) continue;
+        const int cn = sc.size();
+        std::vector<int> cb(cn), ce(cn), cc0(cn), cc1(cn);
+        for (int k = 0; k < cn; k++) {
+          cb[k] = sc.node(k).begin;
+          ce[k] = sc.node(k).end;
+          cc0[k] = sc.node(k).child0;
+          cc1[k] = sc.node(k).child1;
+        }
+        check(hssmf_tree_set_sep_clusters(in.tr, i, cn, cb.data(), ce.data(), cc0.data(),
+                                          cc1.data(), &st), st);
+      }
+    }
+    template<class Opts> hssmf_options options(const Opts& opts) {
+      return hssmf_options{opts.ls, opts.eps, opts.leaf, opts.d0, opts.dd, opts.p, opts.min_hss,
+                           opts.max_rank, static_cast<int>(opts.mode)};
+    }
+  }  // namespace detail
+
   // mf_factor(a, t, opts) (reference multifrontal.hpp:473-503). `a` must carry
   // the tree's ordering (SparseMatrix::permuted), `t` the symbolic upd sets.
   template<class Sparse, class Tree, class Opts>
   MfFactors mf_factor(const Sparse& a, const Tree& t, const Opts& opts, int device = 0) {
+    detail::Inputs in;
+    detail::make_inputs(a, t, in);
+    hssmf_options o = detail::options(opts);
     hssmf_status st{};
-    if (a.size() != t.n) throw IoError("mf factor: matrix and tree sizes differ");
-    hssmf_csr* c = nullptr;
-    detail::check(hssmf_csr_create(a.size(), a.ptr().data(), a.ind().data(), a.val().data(), &c, &st), st);
-    const int nn = static_cast<int>(t.nodes.size());
-    std::vector<int> sb(nn), se(nn), c0(nn), c1(nn), pa(nn), up(nn + 1, 0), ui;
-    for (int i = 0; i < nn; i++) {
-      const auto& f = t.nodes[i];
-      sb[i] = f.sep_begin;
-      se[i] = f.sep_end;
-      c0[i] = f.child0;
-      c1[i] = f.child1;
-      pa[i] = f.parent;
-      ui.insert(ui.end(), f.upd.begin(), f.upd.end());
-      up[i + 1] = static_cast<int>(ui.size());
-    }
-    hssmf_tree* tr = nullptr;
-    int rc = hssmf_tree_create(t.n, nn, sb.data(), se.data(), c0.data(), c1.data(), pa.data(),
-                               up.data(), ui.data(), &tr, &st);
-    if (rc != HSSMF_OK) {
-      hssmf_csr_free(c);
-      detail::raise(rc, st);
-    }
-    // separator clusters from the reference's reorder_tree_separators
-    // (FrontNode::sep_clusters) travel with the tree
-    for (int i = 0; i < nn && rc == HSSMF_OK; i++) {
-      const auto& sc = t.nodes[i].sep_clusters;
-      if (sc.empty()) continue;
-      const int cn = sc.size();
-      std::vector<int> cb(cn), ce(cn), cc0(cn), cc1(cn);
-      for (int k = 0; k < cn; k++) {
-        cb[k] = sc.node(k).begin;
-        ce[k] = sc.node(k).end;
-        cc0[k] = sc.node(k).child0;
-        cc1[k] = sc.node(k).child1;
-      }
-      rc = hssmf_tree_set_sep_clusters(tr, i, cn, cb.data(), ce.data(), cc0.data(), cc1.data(),
-                                       &st);
-    }
-    if (rc != HSSMF_OK) {
-      hssmf_tree_free(tr);
-      hssmf_csr_free(c);
-      detail::raise(rc, st);
-    }
-    hssmf_options o{opts.ls, opts.eps, opts.leaf, opts.d0, opts.dd, opts.p, opts.min_hss,
-                    opts.max_rank, static_cast<int>(opts.mode)};
     hssmf_factors* h = nullptr;
-    rc = hssmf_factor(device, c, tr, &o, &h, &st);
-    hssmf_tree_free(tr);
-    hssmf_csr_free(c);
-    detail::check(rc, st);
+    detail::check(hssmf_factor(device, in.c, in.tr, &o, &h, &st), st);
     MfFactors m;
     m.adopt(h, a.size());
     return m;

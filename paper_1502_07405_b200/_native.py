@@ -108,6 +108,11 @@ _SIGS = {
                                    C.c_int, C.c_int, C.POINTER(Status)]),
     "hssmf_hss_extract": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int,
                                     C.POINTER(C.c_longlong), C.POINTER(Status)]),
+    "hssmf_mgpu_partition": (C.c_int, [vp, C.c_int, vp, C.POINTER(C.c_int), C.POINTER(Status)]),
+    "hssmf_mgpu_factor": (C.c_int, [C.c_int, vp, vp, vp, C.c_int, C.c_int, vp, C.POINTER(vp),
+                                    C.POINTER(Status)]),
+    "hssmf_mgpu_solve": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.POINTER(Status)]),
+    "hssmf_mgpu_local": (C.c_int, [C.c_int, vp, vp, vp, C.c_int, vp, C.c_int, C.POINTER(Status)]),
     "hssmf_hss_info": (C.c_int, [vp, vp, vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "hssmf_hss_solve": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Status)]),

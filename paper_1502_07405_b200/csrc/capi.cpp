@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "engine.hpp"
+#include "mgpu.hpp"
 #include "hss.hpp"
 #include "hss_dense.hpp"
 #include "host/analysis.hpp"
@@ -41,7 +42,13 @@ namespace hssmf_b200 {
 
 struct hssmf_csr { Csr a; };
 struct hssmf_tree { Etree t; };
-struct hssmf_factors { std::unique_ptr<Engine> e; };
+struct hssmf_factors {
+  std::unique_ptr<Engine> e;
+  // multi-GPU rank handle (hssmf_mgpu_factor): the partition and the tree
+  std::shared_ptr<MgpuPlan> plan;
+  std::shared_ptr<Etree> tree;
+  int rank = 0;
+};
 struct hssmf_hss { std::unique_ptr<DenseHss> h; };
 
 namespace {
@@ -662,3 +669,105 @@ int hssmf_dev_lu(int device, double* a, int m, int n, int* piv, hssmf_status* st
 }
 
 }  // extern "C"
+
+/* ---- multi-GPU subtree partition (mgpu.cu) ---- */
+namespace {
+  struct CallbackTransport : MgpuTransport {
+    const hssmf_transport* cb;
+    explicit CallbackTransport(const hssmf_transport* c) : cb(c) {}
+    void send(const double* buf, long long count, int dst, int) override {
+      if (cb->send(cb->ctx, buf, count, dst) != 0)
+        throw SolverFailure(HSSMF_ERR_NCCL, -1, -1, "mgpu transport: send to rank " + std::to_string(dst) + " failed");
+    }
+    void recv(double* buf, long long count, int src, int) override {
+      if (cb->recv(cb->ctx, buf, count, src) != 0)
+        throw SolverFailure(HSSMF_ERR_NCCL, -1, -1, "mgpu transport: recv from rank " + std::to_string(src) + " failed");
+    }
+  };
+  std::vector<char> owned_mask(const MgpuPlan& P, int rank) {
+    std::vector<char> m(P.owner.size());
+    for (size_t i = 0; i < m.size(); i++) m[i] = P.owner[i] == rank;
+    return m;
+  }
+}  // namespace
+
+int hssmf_mgpu_partition(const hssmf_tree* t, int nranks, int* owner, int* nedges,
+                         hssmf_status* st) {
+  return guard(st, [&] {
+    const MgpuPlan P = mgpu_partition(t->t, nranks);
+    if (owner) std::copy(P.owner.begin(), P.owner.end(), owner);
+    if (nedges) *nedges = (int)P.edges.size();
+  });
+}
+
+int hssmf_mgpu_factor(int device, const hssmf_csr* a, const hssmf_tree* t,
+                      const hssmf_options* o, int rank, int nranks, const hssmf_transport* tr,
+                      hssmf_factors** out, hssmf_status* st) {
+  *out = nullptr;
+  auto f = std::make_unique<hssmf_factors>();
+  const int rc = guard(st, [&] {
+    if (!tr || !tr->send || !tr->recv) throw std::invalid_argument("mgpu factor: no transport");
+    if (rank < 0 || rank >= nranks) throw std::invalid_argument("mgpu factor: bad rank");
+    f->plan = std::make_shared<MgpuPlan>(mgpu_partition(t->t, nranks));
+    f->tree = std::make_shared<Etree>(t->t);
+    f->rank = rank;
+    const auto mask = owned_mask(*f->plan, rank);
+    f->e = std::make_unique<Engine>(device);
+    HSSMF_CUDA(cudaSetDevice(device));
+    f->e->analyze(a->a, t->t, to_opts(o), mask.data());
+    std::map<int, Engine*> eng{{rank, f->e.get()}};
+    CallbackTransport ct(tr);
+    mgpu_factor(*f->plan, eng, ct);
+  });
+  if (rc == HSSMF_OK) *out = f.release();
+  return rc;
+}
+
+int hssmf_mgpu_solve(hssmf_factors* f, const hssmf_transport* tr, double* x, int ldx, int nrhs,
+                     hssmf_status* st) {
+  return guard(st, [&] {
+    if (!f->plan) throw std::invalid_argument("mgpu solve: factors were not made by hssmf_mgpu_factor");
+    std::map<int, Engine*> eng{{f->rank, f->e.get()}};
+    std::map<int, double*> xs{{f->rank, x}};
+    CallbackTransport ct(tr);
+    mgpu_solve(*f->plan, *f->tree, eng, xs, ldx, nrhs, ct);
+  });
+}
+
+int hssmf_mgpu_local(int device, const hssmf_csr* a, const hssmf_tree* t, const hssmf_options* o,
+                     int nranks, double* x, int nrhs, hssmf_status* st) {
+  return guard(st, [&] {
+    HSSMF_CUDA(cudaSetDevice(device));
+    const MgpuPlan P = mgpu_partition(t->t, nranks);
+    const Options opts = to_opts(o);
+    std::vector<std::unique_ptr<Engine>> es;
+    std::map<int, Engine*> eng;
+    for (int r = 0; r < nranks; r++) {
+      const auto mask = owned_mask(P, r);
+      es.push_back(std::make_unique<Engine>(device));
+      es.back()->analyze(a->a, t->t, opts, mask.data());
+      eng[r] = es.back().get();
+    }
+    LocalTransport lt;
+    mgpu_factor(P, eng, lt);
+    const int n = t->t.n;
+    // every rank solves its own copy of b; the solution is assembled from the
+    // separators each rank owns
+    std::vector<double*> xr(nranks, nullptr);
+    std::map<int, double*> xs;
+    for (int r = 0; r < nranks; r++) {
+      HSSMF_CUDA(cudaMalloc(&xr[r], (size_t)n * nrhs * sizeof(double) + 8));
+      HSSMF_CUDA(cudaMemcpy(xr[r], x, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToDevice));
+      xs[r] = xr[r];
+    }
+    mgpu_solve(P, t->t, eng, xs, n, nrhs, lt);
+    for (size_t i = 0; i < t->t.nodes.size(); i++) {
+      const auto& fn = t->t.nodes[i];
+      if (!fn.ns()) continue;
+      HSSMF_CUDA(cudaMemcpy2D(x + fn.sep_begin, (size_t)n * sizeof(double),
+                              xr[P.owner[i]] + fn.sep_begin, (size_t)n * sizeof(double),
+                              (size_t)fn.ns() * sizeof(double), nrhs, cudaMemcpyDeviceToDevice));
+    }
+    for (auto p : xr) cudaFree(p);
+  });
+}

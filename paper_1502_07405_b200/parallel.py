@@ -414,3 +414,37 @@ class DistributedMf:
         self.solve_device(xs)
         x = self.combine(xs).cpu().numpy().T
         return x.reshape(bb.shape)
+
+
+# ---- the native (C++) driver of the same protocol (csrc/mgpu.cu) ----------
+def native_partition(t, nranks):
+    """owner per front and the cross-rank edge count from the C++ partition
+    (hssmf_mgpu_partition); equal to subtree_partition's"""
+    import ctypes as C
+    from . import _native as N
+    from .api import _call
+    owner = np.zeros(len(t.child0), np.int32)
+    ne = C.c_int()
+    _call("hssmf_mgpu_partition", t._h, int(nranks), owner.ctypes.data_as(C.c_void_p),
+          C.byref(ne))
+    del N
+    return owner, ne.value
+
+
+def native_local_solve(a, t, opts, nranks, b, device=0):
+    """all nranks ranks of the C++ driver in this process on one GPU
+    (hssmf_mgpu_local: in-process mailbox): partitioned factor + solve of b
+    (n or n x nrhs), returns x"""
+    import ctypes as C
+
+    import torch
+
+    from .api import _call
+    bb = np.asarray(b, np.float64)
+    b2 = bb.reshape(-1, 1) if bb.ndim == 1 else bb
+    x = torch.from_numpy(np.ascontiguousarray(b2.T)).to(torch.device("cuda", device))
+    torch.cuda.synchronize(device)
+    o = opts.native()
+    _call("hssmf_mgpu_local", int(device), a._h, t._h, C.byref(o), int(nranks),
+          C.c_void_p(x.data_ptr()), int(b2.shape[1]))
+    return x.cpu().numpy().T.reshape(bb.shape)

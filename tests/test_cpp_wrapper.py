@@ -66,3 +66,18 @@ def test_dropin_reference_names_and_signatures(oracle):
     assert np.all(np.abs(np.array(d["dense_u"][:-1]) - ru) <= np.maximum(2, 0.1 * ru))
     assert d["dense_rounds"] == r.rounds and d["dense_d_final"] == r.d_final
     assert d["dense_relres"] < 1e-7 and d["uneven_relres"] < 1e-7
+
+
+MGPU = os.path.join(ROOT, "oracle", "_ref", "mgpu_check")
+
+
+@pytest.mark.gpu
+def test_nccl_dropin_runs():
+    # include/hssmf_b200/mgpu_nccl.hpp: the C++ multi-GPU path over NCCL with
+    # every visible GPU (one on a gpurun box) equals the single-GPU drop-in
+    if not os.path.exists(MGPU):
+        pytest.skip("mgpu_check not built (make -C oracle mgpu)")
+    out = subprocess.run([MGPU], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["nranks"] >= 1 and d["max_diff"] == 0.0

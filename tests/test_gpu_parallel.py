@@ -39,3 +39,24 @@ def test_partitioned_equals_single(kind, k, nd_leaf, so, nranks):
     # refactor + solve again (the phases restart from the deepest level)
     d.factor()
     assert np.array_equal(d.solve(b), x1)
+
+
+@pytest.mark.parametrize("kind,k,nd_leaf,so,nranks", [
+    ("p2d", 64, 16, dict(mode="mf"), 4),
+    ("p3d", 24, 32, dict(min_hss=300, eps=1e-6, leaf=64, ls=64), 2),
+    ("p3d", 24, 32, dict(min_hss=300, eps=1e-6, leaf=64, ls=64), 4),
+])
+def test_native_driver_equals_single(kind, k, nd_leaf, so, nranks):
+    # the C++ driver of the phased protocol (csrc/mgpu.cu, the path the C++
+    # drop-in uses over NCCL) with all ranks in this process: bitwise equal
+    # to one engine, two right-hand sides
+    from paper_1502_07405_b200.parallel import native_local_solve
+    op = P.ordered_grid(kind, k, nd_leaf)
+    ptr, ind, val = op.a.arrays()
+    b = csr_matvec(ptr, ind, val, x_true(op.a.size(), 1))
+    b2 = np.stack([b, 2.0 * b - 1.0], axis=1)
+    opts = P.SolverOptions(nd_leaf=nd_leaf, **so)
+    m = P.mf_factor(op.a, op.t, opts)
+    x1 = P.mf_solve_new(m, b2)
+    x2 = native_local_solve(op.a, op.t, opts, nranks, b2)
+    assert np.array_equal(x1, x2)

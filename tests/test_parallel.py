@@ -165,3 +165,14 @@ def test_bench_spawns_ranks_dry_run():
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 4 and line["protocol_ok"] is True
     assert line["config"]["parallelism"] == "subtree4" and line["partition"]["edges"] == 3
+
+
+@pytest.mark.parametrize("kind,k,leaf,nranks", [("p3d", 32, 32, 2), ("p3d", 48, 32, 8),
+                                                  ("p2d", 64, 16, 4)])
+def test_native_partition_matches_python(kind, k, leaf, nranks):
+    # the C++ driver (csrc/mgpu.cu) partitions exactly like parallel.py
+    from paper_1502_07405_b200.parallel import native_partition
+    op = P.ordered_grid(kind, k, leaf)
+    part = subtree_partition(op.t, nranks)
+    owner, ne = native_partition(op.t, nranks)
+    assert np.array_equal(owner, part.owner) and ne == len(part.edges)
