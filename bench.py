@@ -339,7 +339,7 @@ def ref_rhs(ptr, ind, val, n):
     return csr_matvec(ptr, ind, val, x_true(n, 1))
 
 
-def reference_scaled(cfg, tv, threads, steps, warmup, budget_s):
+def reference_scaled(cfg, tv, threads, steps, warmup, budget_s, full_model=None):
     """Time the reference on a sample of the workload and scale it by the
     ratio of the full workload's model cost to the sample's (reference-
     reported) model cost. The warm-up runs (at least one) time the cheapest
@@ -347,6 +347,8 @@ def reference_scaled(cfg, tv, threads, steps, warmup, budget_s):
     subtree whose predicted time (at the warm-up's model rate) fits
     budget_s / steps, so the whole arm stays within about budget_s."""
     full, src = front_model(tv, cfg)
+    if full_model is not None:  # per-front costs supplied by the caller
+        full, src = np.asarray(full_model, np.float64), "caller's per-front model"
     cands = sample_candidates(tv, cfg)
     p0, _, _ = subtree_sample(tv, cfg, cands[0][1])
     rate = None

@@ -72,6 +72,10 @@ CONFIGS = {
     "c4": Config("c4_cd3d96_hss", "cd3d", 96, 32, 64, 2000, 1e-5, 128),
     "c5": Config("c5_p3d128_hss", "p3d", 128, 32, 64, 4000, 1e-4, 256),
     "c5_mf": Config("c5_p3d128_mf", "p3d", 128, 32, 0, 4000, 1e-4, 256, mode="mf"),
+    # config 5's options on smaller grids (reference runs that fit in time and
+    # memory; the validation of the reference arm's sample scaling)
+    "c5_96": Config("p3d96_c5opts", "p3d", 96, 32, 64, 4000, 1e-4, 256),
+    "c5_112": Config("p3d112_c5opts", "p3d", 112, 32, 64, 4000, 1e-4, 256),
 }
 
 
