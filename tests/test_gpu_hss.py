@@ -351,6 +351,30 @@ def test_baseline_config_vs_golden(name):
     assert res <= 10 * float(g["relres"])
 
 
+@pytest.mark.parametrize("route", ["default", "householder"])
+def test_config5_vs_full_reference_run(route, monkeypatch):
+    # BASELINE config 5 itself (P3D 128^3, eps 1e-4, leaf 256, HSS >= 4000)
+    # against the reference's full run on the GPU-box host
+    # (tests/golden/ref_c5.npz, tools/ref_c5_box.sh): identical front types,
+    # every HSS front's rank within +-10%, relres <= 10x the reference's (1.996)
+    if route == "householder":
+        monkeypatch.setenv("HSSMF_ID_ALGO", "householder")
+    from paper_1502_07405_b200.problems import CONFIGS
+    cfg = CONFIGS["c5"]
+    g = np.load(os.path.join(GOLD, "ref_c5.npz"))
+    op = P.ordered_grid(cfg.kind, cfg.k, cfg.nd_leaf)
+    ptr, ind, val = op.a.arrays()
+    b = csr_matvec(ptr, ind, val, x_true(op.a.size(), 1))
+    m = P.mf_factor(op.a, op.t, cfg.solver_options())
+    x = P.mf_solve_new(m, b)
+    res = np.linalg.norm(op.a.matvec(x) - b) / np.linalg.norm(b)
+    assert np.array_equal(m.type, g["type"])
+    hs = g["hss_ids"]
+    bad = np.nonzero(~close_mask(m.rank[hs], g["rank"][hs]))[0]
+    assert bad.size == 0, [(int(hs[q]), int(m.rank[hs[q]]), int(g["rank"][hs[q]])) for q in bad]
+    assert res <= 10 * float(g["relres"])
+
+
 @pytest.mark.parametrize("k", [64, 80, 96])
 def test_p3d_with_config5_options_vs_reference(k):
     # BASELINE config 5 options (HSS >= 4000, eps 1e-4, leaf 256) on smaller
