@@ -894,9 +894,6 @@ namespace hssmf_b200 {
           for (int p = 0; p < kHssPhases; p++) fprintf(stderr, " %.0f", ps[p].host_ms);
           // phase_stats drains the event list: re-add so profiling still sees it
           res[q].hss->restore_phase_stats(ps);
-          int tc = 0, tcc = 0;
-          res[q].hss->tail_stats(tc, tcc);
-          fprintf(stderr, " | tail %d/%d", tcc, tc);
         }
         fprintf(stderr, "\n");
       }

@@ -72,6 +72,7 @@ namespace hssmf_b200 {
   // B are 16-byte aligned with even leading dimensions; gemm_run_mixed routes
   // eligible problems there by itself
   bool gemm_tma_eligible(const GemmProblem& g);
+  bool gemm_tma_aligned(const GemmProblem& g);  // alignment / size only (no K rule)
   void gemm_tma_run(const std::vector<GemmProblem>& p, cudaStream_t s);
 
   // one large-K problem with few output tiles: split-K over extra CTAs to fill

@@ -266,13 +266,24 @@ namespace hssmf_b200 {
     }
   }  // namespace
 
+  bool gemm_tma_aligned(const GemmProblem& g) {
+    static const bool off = getenv("HSSMF_NO_TMA") != nullptr;
+    if (off || g.m < 96 || g.n < 96) return false;
+    if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15)) return false;
+    return !(g.lda & 1) && !(g.ldb & 1);
+  }
+
   bool gemm_tma_eligible(const GemmProblem& g) {
     static const bool off = getenv("HSSMF_NO_TMA") != nullptr;
     if (off) return false;
     const bool ta = g.trans & 1, tb = g.trans & 2;
-    // big enough for 128 x 128 tiles to pay (smaller products stay on the
-    // 64 x 64 cp.async kernel)
-    if (g.m < 96 || g.n < 96 || g.k < 32) return false;
+    // long products only: one 128 x 128 CTA per SM does not overlap a tile's
+    // pipeline fill and epilogue with another tile, so short-K shapes run
+    // faster on the 64 x 64 kernel (4 CTAs per SM). Measured on B200
+    // (profiles/r02_gemm_shapes.json): 8192^3 33.5-34.6 TF/s vs 30.9;
+    // 3000^2 x 960 25.5 vs 29.6; 4096^2 x 128 11.8 vs 18.9.
+    static const int kmin = getenv("HSSMF_TMA_KMIN") ? atoi(getenv("HSSMF_TMA_KMIN")) : 2048;
+    if (g.m < 96 || g.n < 96 || g.k < kmin) return false;
     if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15)) return false;
     if ((g.lda & 1) || (g.ldb & 1)) return false;
     (void)ta;

@@ -21,7 +21,6 @@
 #include <stdexcept>
 #include "rng.cuh"
 #include "staging.cuh"
-#include "tail_check.cuh"
 #include "arena.cuh"
 
 namespace hssmf_b200 {
@@ -263,7 +262,6 @@ namespace hssmf_b200 {
     int d = 0, rounds = 0;
     double flops = 0;
     bool gram = false;  // ID route: Gram / pivoted Cholesky (eps >= 5e-5) or Householder
-    int tail_checked = 0, tail_certified = 0;  // tail_check outcomes (debug output)
     // numerically symmetric front (|F - F^T| <= 1e-10 max|F|, far below any
     // compression tolerance of the Gram route): S_c = F^T R equals S_r = F R
     // up to that perturbation, so the column-side IDs are taken from the
@@ -913,74 +911,6 @@ namespace hssmf_b200 {
       N.spec_d = 0;
     }
 
-    // The Gram route's stop test near the cap of a large node is decided at
-    // the rounding level of its Schur-complement diagonal (tail_check.cu). A
-    // task that stopped uncertified at its cap with its own residual within a
-    // factor of the threshold gets the residual recomputed directly from the
-    // samples; if that one passes the reference's test (rrqr.hpp:67-72) the ID
-    // is certified at the cap. A run task is checked once (a symmetric front's
-    // column twin takes the row side's outcome).
-    void tail_check(const std::vector<int>& act, const std::vector<int>& run_t,
-                    const std::vector<GramTask>& gt, const std::vector<const double*>& Luse,
-                    std::vector<DBuf<int>>& perm, std::vector<int>& rk, std::vector<int>& ce,
-                    double abs_tol) {
-      static const bool off = getenv("HSSMF_NO_TAIL_CHECK") != nullptr;
-      static const int min_rows = getenv("HSSMF_TAIL_MIN_ROWS") ? atoi(getenv("HSSMF_TAIL_MIN_ROWS")) : 1024;
-      if (off) return;
-      std::vector<int> cand;
-      for (int t : run_t) {
-        const GramTask& T = gt[t];
-        if (ce[t] || rk[t] != T.kmax || T.kmax >= T.kmax_dim || T.n < min_rows || !T.dg) continue;
-        cand.push_back(t);
-      }
-      if (cand.empty()) return;
-      Ph ph_(this, 3);
-      // the Gram route's own squared residual at the cap and r11, one readback
-      DBuf<double> v;
-      v.alloc(2 * cand.size() + 1, s);
-      for (size_t q = 0; q < cand.size(); q++) {
-        const GramTask& T = gt[cand[q]];
-        gram_dg_max(T.dg, T.flag, T.n, v.p + 2 * q, s);
-        HSSMF_CUDA(cudaMemcpyAsync(v.p + 2 * q + 1, T.r11, sizeof(double), cudaMemcpyDeviceToDevice, s));
-      }
-      std::vector<double> hv(2 * cand.size());
-      d2h(hv.data(), v.p, hv.size() * sizeof(double), s);
-      stream_sync(s);
-      std::vector<int> chk;
-      std::vector<double> thr;
-      for (size_t q = 0; q < cand.size(); q++) {
-        const double th = std::max(o.eps * hv[2 * q + 1], abs_tol);
-        // a residual well above the threshold is not a rounding question
-        if (std::sqrt(std::max(hv[2 * q], 0.0)) <= 8.0 * th) {
-          chk.push_back(cand[q]);
-          thr.push_back(th);
-        }
-      }
-      if (chk.empty()) return;
-      DBuf<double> pv;
-      pv.alloc(chk.size() + 1, s);
-      for (size_t q = 0; q < chk.size(); q++) {
-        const int t = chk[q];
-        const auto& N = nodes[act[t / 2]];
-        const Grow& S = (t % 2) ? N.slc : N.slr;
-        gram_tail_residual2(S.b.p, S.rows, gt[t].n, d, Luse[t], gt[t].n, perm[t].p, rk[t],
-                            pv.p + q, s);
-      }
-      std::vector<double> hp(chk.size());
-      d2h(hp.data(), pv.p, hp.size() * sizeof(double), s);
-      stream_sync(s);
-      for (size_t q = 0; q < chk.size(); q++) {
-        const double p = std::sqrt(std::max(hp[q], 0.0));
-        if (p <= thr[q]) {
-          const int t = chk[q];
-          ce[t] = 1;
-          if (sym) ce[t + 1] = 1;
-          tail_certified++;
-        }
-        tail_checked++;
-      }
-    }
-
     void gram_ids(const std::vector<int>& act, int cap_id, double abs_tol,
                   std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
                   std::vector<DBuf<int>>& perm, DBuf<int>& outs, std::vector<CpqrTask>& tasks,
@@ -1095,7 +1025,6 @@ namespace hssmf_b200 {
           rk[2 * q] = rk[2 * q + 1] = N.spec_rank;
           ce[2 * q] = ce[2 * q + 1] = N.spec_cert;
         }
-      tail_check(act, run_t, gt, Luse, perm, rk, ce, abs_tol);
       prb.unpack(hp);
       ho.assign(2 * nt, 0);
       std::vector<CopyDesc> rc;
@@ -2077,10 +2006,6 @@ namespace hssmf_b200 {
     StagingScope sc(staging_for(d_->s));
     ArenaScope as(&d_->arena, &d_->keep_arena);
     d_->matvec(op, root < 0 ? d_->root : root, x, ldx, nc, y, ldy);
-  }
-  void HssMatrixDev::tail_stats(int& checked, int& certified) const {
-    checked = d_->tail_checked;
-    certified = d_->tail_certified;
   }
   int HssMatrixDev::node_size(int node) const {
     return d_->nodes[node < 0 ? d_->root : node].size();

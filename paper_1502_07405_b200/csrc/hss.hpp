@@ -109,8 +109,6 @@ namespace hssmf_b200 {
     // (HssMatrix::extract, hss_matrix.hpp:261-280); returns the leaves visited
     long long extract(const std::vector<int>& I, const std::vector<int>& J, double* out);
     int rows() const;
-    // Gram-route stop tests recomputed from the samples / certified by them
-    void tail_stats(int& checked, int& certified) const;
     int rounds() const;
     int d_final() const;
     int hss_rank() const;
