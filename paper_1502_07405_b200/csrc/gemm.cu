@@ -321,11 +321,17 @@ namespace hssmf_b200 {
     set_gemm_attrs();
     // tile size of the launch: 32 x 32 when the whole list has fewer 64 x 64
     // tiles than two per SM (latency-bound batches of the adaptive rounds)
+    // (long-K products keep 64 x 64 tiles: 6000 x 128 x 6000 ran at 10.6 TF/s
+    // on 32 x 32 tiles against 18.5)
     long long t64 = 0;
+    int kmax_all = 0;
     for (const auto& x : p)
-      if (x.m > 0 && x.n > 0) t64 += (long long)ceil_div(x.m, BM) * ceil_div(x.n, BN);
+      if (x.m > 0 && x.n > 0) {
+        t64 += (long long)ceil_div(x.m, BM) * ceil_div(x.n, BN);
+        kmax_all = std::max(kmax_all, x.k);
+      }
     static const bool no_small = getenv("HSSMF_GEMM_NO_SMALL") != nullptr;
-    const bool small = !no_small && t64 < 2 * 148;
+    const bool small = !no_small && t64 < 2 * 148 && kmax_all <= 1024;
     const int tm = small ? SM_BM : BM, tn = small ? SM_BN : BN;
     GemmParam b;
     b.nprob = 0;

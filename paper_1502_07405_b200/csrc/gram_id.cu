@@ -722,6 +722,144 @@ namespace hssmf_b200 {
             if (i < n && j < n && i >= j) G[i + (size_t)j * n] = c[mi][ni][v] - acc[mi][ni][v];
           }
     }
+
+    // Persistent form of the trailing update (opt-in, HSSMF_GRAM_SYRK=persist):
+    // every CTA walks the lower 64 x 64 tiles of all tasks (stride gridDim.x)
+    // and double-buffers them through shared memory, the next tile's G and L
+    // blocks streaming in (cp.async) while the current tile's DMMA products run.
+    // One 136 KB CTA per SM hides less latency than two one-tile CTAs per SM:
+    // measured 1.92 TB/s on c5 against 2.51 TB/s. Same arithmetic per element.
+    constexpr int kSyrkMaxTasks = 128;
+    struct SyrkParam {
+      int nt;
+      int pre[kSyrkMaxTasks + 1];  // tile prefix per task
+    };
+    template <int NB>
+    __global__ void __launch_bounds__(256, 1)
+    gram_syrk_persist_kernel(const GramTask* __restrict__ tasks, int k0,
+                             const __grid_constant__ SyrkParam prm,
+                             unsigned long long* probe_bytes) {
+      constexpr int SP = 68, GP = 65;
+      extern __shared__ __align__(16) double sm6[];
+      // stage st: As[NB][SP], Bs[NB][SP], Gs[64][GP] (Gs[c][r] = G(i0 + r, j0 + c))
+      constexpr int STAGE = 2 * NB * SP + 64 * GP;
+      __shared__ int live[kSyrkMaxTasks];
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      for (int q = tid; q < prm.nt; q += blockDim.x) live[q] = !__ldcg(tasks[q].state + 1);
+      __syncthreads();
+      if (probe_bytes && blockIdx.x == 0 && tid == 0)
+        for (int q = 0; q < prm.nt; q++)
+          if (live[q]) {
+            const unsigned long long n = tasks[q].n;
+            atomicAdd(probe_bytes, n * (n + 1) / 2 * 16ull);
+          }
+      const int total = prm.pre[prm.nt];
+      struct Tile { int q, i0, j0, n; const double* Lk; double* G; };
+      auto locate = [&](int T) {
+        int lo = 0, hi = prm.nt - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (prm.pre[mid] <= T) lo = mid; else hi = mid - 1;
+        }
+        Tile x;
+        x.q = lo;
+        const GramTask& Tk = tasks[lo];
+        x.n = Tk.n;
+        const int nbt = (x.n + 63) >> 6;
+        const int t = T - prm.pre[lo];
+        auto before = [&](int c) { return c * nbt - c * (c - 1) / 2; };
+        const double bb = 2.0 * nbt + 1.0;
+        int tj = (int)((bb - sqrt(fmax(bb * bb - 8.0 * t, 0.0))) * 0.5);
+        tj = max(0, min(tj, nbt - 1));
+        while (tj > 0 && before(tj) > t) tj--;
+        while (tj + 1 < nbt && before(tj + 1) <= t) tj++;
+        x.i0 = (tj + (t - before(tj))) * 64;
+        x.j0 = tj * 64;
+        x.Lk = Tk.L + (size_t)k0 * x.n;
+        x.G = Tk.G;
+        return x;
+      };
+      // next live tile at or after T (stride gridDim.x)
+      auto next_live = [&](int T) {
+        while (T < total) {
+          int lo = 0, hi = prm.nt - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (prm.pre[mid] <= T) lo = mid; else hi = mid - 1;
+          }
+          if (live[lo]) return T;
+          T += gridDim.x;
+        }
+        return total;
+      };
+      auto load = [&](const Tile& x, int st) {
+        double* As = sm6 + st * STAGE;
+        double* Bs = As + NB * SP;
+        double* Gs = Bs + NB * SP;
+        const int n = x.n;
+        for (int e = tid; e < NB * 64; e += 256) {
+          const int q = e >> 6, r = e & 63;
+          const bool va = x.i0 + r < n, vb = x.j0 + r < n;
+          cp_async8(As + q * SP + r, va ? x.Lk + x.i0 + r + (size_t)q * n : x.Lk, va);
+          cp_async8(Bs + q * SP + r, vb ? x.Lk + x.j0 + r + (size_t)q * n : x.Lk, vb);
+        }
+        for (int e = tid; e < 64 * 64; e += 256) {
+          const int c = e >> 6, r = e & 63;
+          const bool v = x.i0 + r < n && x.j0 + c < n && x.i0 + r >= x.j0 + c;
+          cp_async8(Gs + c * GP + r, v ? x.G + x.i0 + r + (size_t)(x.j0 + c) * n : x.G, v);
+        }
+      };
+      const int wm = warp & 1, wn = warp >> 1;  // warp tile rows 32 wm, cols 16 wn
+      const int lr = lane >> 2, lc = lane & 3;
+      int T = next_live(blockIdx.x), st = 0;
+      if (T < total) load(locate(T), 0);
+      cp_async_commit();
+      while (T < total) {
+        const Tile x = locate(T);
+        const int Tn = next_live(T + gridDim.x);
+        if (Tn < total) load(locate(Tn), st ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* As = sm6 + st * STAGE;
+        const double* Bs = As + NB * SP;
+        const double* Gs = Bs + NB * SP;
+        double acc[4][2][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+          for (int ni = 0; ni < 2; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NB; kk += 4) {
+          double a[4], b[2];
+#pragma unroll
+          for (int mi = 0; mi < 4; mi++) a[mi] = As[(kk + lc) * SP + 32 * wm + 8 * mi + lr];
+#pragma unroll
+          for (int ni = 0; ni < 2; ni++) b[ni] = Bs[(kk + lc) * SP + 16 * wn + 8 * ni + lr];
+#pragma unroll
+          for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+            for (int ni = 0; ni < 2; ni++) dmma8x8x4(acc[mi][ni], a[mi], b[ni]);
+        }
+        const int n = x.n;
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+          for (int ni = 0; ni < 2; ni++)
+#pragma unroll
+            for (int v = 0; v < 2; v++) {
+              const int r = 32 * wm + 8 * mi + lr, c = 16 * wn + 8 * ni + 2 * lc + v;
+              const int i = x.i0 + r, j = x.j0 + c;
+              if (i < n && j < n && i >= j)
+                x.G[i + (size_t)j * n] = Gs[c * GP + r] - acc[mi][ni][v];
+            }
+        __syncthreads();  // stage st is refilled in the next iteration
+        st ^= 1;
+        T = Tn;
+      }
+      cp_async_wait<0>();
+    }
+
   }  // namespace
 
   // per-step segment cycles of the panel kernel (measurement knob): wait,
@@ -795,6 +933,7 @@ namespace hssmf_b200 {
     // decision work); HSSMF_GRAM_V1=1 keeps the older shared-memory kernel
     const bool force_v1 = getenv("HSSMF_GRAM_V1") != nullptr;
     constexpr int NB2 = 32, RPC_MAX = 512;
+    constexpr int kSyrkPersistSmem = 2 * (2 * NB2 * 68 + 64 * 65) * 8;
     const bool v2 = !force_v1 && max_n <= 16 * RPC_MAX;
     int T2 = 32, CL2 = 1;
     if (v2) {
@@ -809,6 +948,9 @@ namespace hssmf_b200 {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 64 * 8));
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_dmma_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_persist_kernel<NB2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kSyrkPersistSmem));
       });
       while (CL2 * RPC_MAX < max_n) CL2 *= 2;
       T2 = std::max(32, ((max_n + CL2 - 1) / CL2 + 31) / 32 * 32);
@@ -818,6 +960,10 @@ namespace hssmf_b200 {
     // trailing update on the FP64 tensor pipe unless HSSMF_GRAM_SYRK=fma
     const char* esy = getenv("HSSMF_GRAM_SYRK");
     const bool syrk_cuda_cores = esy && !strcmp(esy, "fma");
+    // HSSMF_GRAM_SYRK=persist: the persistent double-buffered update (measured
+    // slower on c5: 1.92 TB/s against 2.51 for one tile per CTA, 2 CTAs per SM,
+    // profiles/r02/README.md)
+    const bool syrk_persist = esy && !strcmp(esy, "persist");
     // all panels are queued without host round trips: a finished task's
     // panel kernel returns at once and its trailing GEMM is skipped on device
     for (int k0 = 0; k0 <= kmax; k0 += nb) {
@@ -848,7 +994,18 @@ namespace hssmf_b200 {
         {
           ProbeScope prs(PROBE_GRAM_SYRK, s, 0.0, 0.0);
           unsigned long long* pb = probe_enabled() ? probe_device_bytes() : nullptr;
-          if (syrk_cuda_cores)
+          if (syrk_persist && nt <= kSyrkMaxTasks) {
+            SyrkParam sp;
+            sp.nt = nt;
+            sp.pre[0] = 0;
+            for (int q = 0; q < nt; q++) {
+              const int b = (tasks[q].n + 63) / 64;
+              sp.pre[q + 1] = sp.pre[q] + b * (b + 1) / 2;
+            }
+            const int grid = std::max(1, std::min(sp.pre[nt], 148));
+            gram_syrk_persist_kernel<NB2><<<grid, 256, kSyrkPersistSmem, s>>>(
+                (const GramTask*)d, k0, sp, pb);
+          } else if (syrk_cuda_cores)
             gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
                 (const GramTask*)d, k0, pb);
           else

@@ -369,15 +369,15 @@ def test_config5_vs_full_reference_run(route, monkeypatch):
     # BASELINE config 5 itself (P3D 128^3, eps 1e-4, leaf 256, HSS >= 4000)
     # against the reference's full run on the GPU-box host
     # (tests/golden/ref_c5.npz, tools/ref_c5_box.sh: 3186 s on 16 threads,
-    # relres 1.996). Both routes: identical front types, relres <= 10x.
-    # The Householder ID route (the reference's own CPQR, rrqr.hpp:32-151):
-    # every HSS front's rank within +-10%. The default Gram route: the top
-    # fronts certify where the greedy pivots' residual at the round's cap
-    # crosses eps r11, a near-tie that both implementations' rounding decide
-    # (its top fronts landed 4 rounds early to 3 rounds late over four runs,
-    # profiles/r02/README.md); its gate is every front within +-10% or within
-    # 4 adaptive rounds (dd = 128 sample columns) of the reference's rank, and
-    # at least 150 of the 155 fronts within +-10%.
+    # relres 1.996); both ID routes. Identical front types and relres <= 10x.
+    # Ranks: every HSS front whose children are dense assembles the same
+    # matrix as the reference (up to rounding) and must be within +-10%. A
+    # front with an HSS child assembles the child's compressed update, which
+    # differs from the reference's compressed update at the eps level (other
+    # pivots, other bases): its eps-rank is decided on a perturbed operator, so
+    # its gate is +-10% or within 4 adaptive rounds (dd = 128 sample columns)
+    # of the reference's (over five runs the top fronts landed between 4
+    # rounds early and 3 rounds late; profiles/r02/README.md).
     if route == "householder":
         monkeypatch.setenv("HSSMF_ID_ALGO", "householder")
     from paper_1502_07405_b200.problems import CONFIGS
@@ -396,13 +396,15 @@ def test_config5_vs_full_reference_run(route, monkeypatch):
     assert np.array_equal(types, g["type"])
     assert res <= 10 * float(g["relres"])
     hs = g["hss_ids"]
+    gt = g["type"]
+    hss_child = np.array([any(c >= 0 and gt[c] == 1 for c in (op.t.child0[i], op.t.child1[i]))
+                          for i in hs])
     ok = close_mask(ranks[hs], g["rank"][hs])
-    bad = [(int(hs[q]), int(ranks[hs[q]]), int(g["rank"][hs[q]])) for q in np.nonzero(~ok)[0]]
-    if route == "householder":
-        assert not bad, bad
-    else:
-        assert ok.sum() >= 150, bad
-        assert all(abs(mine - ref) <= 4 * 128 + 2 for _, mine, ref in bad), bad
+    within = np.abs(ranks[hs] - g["rank"][hs]) <= 4 * 128 + 2
+    bad = [(int(hs[q]), int(ranks[hs[q]]), int(g["rank"][hs[q]]), bool(hss_child[q]))
+           for q in np.nonzero(~ok)[0]]
+    assert np.all(ok | (hss_child & within)), bad
+    assert (~hss_child).sum() > 100 and np.all(ok[~hss_child])
 
 
 @pytest.mark.parametrize("k", [64, 80, 96])
