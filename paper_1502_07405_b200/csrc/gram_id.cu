@@ -932,7 +932,10 @@ namespace hssmf_b200 {
     // to 16, the CTA sized to its rows (no idle warps in the per-step
     // decision work); HSSMF_GRAM_V1=1 keeps the older shared-memory kernel
     const bool force_v1 = getenv("HSSMF_GRAM_V1") != nullptr;
-    constexpr int NB2 = 32, RPC_MAX = 512;
+    // panel width of the one-row-per-thread panel: 48 steps (three panels of 32
+    // per two of 48: a third fewer trailing updates, which move the whole
+    // lower Gram matrix each; 512 rows x 48 columns of L = 192 KB of shared memory)
+    constexpr int NB2 = 48, RPC_MAX = 512;
     constexpr int kSyrkPersistSmem = 2 * (2 * NB2 * 68 + 64 * 65) * 8;
     const bool v2 = !force_v1 && max_n <= 16 * RPC_MAX;
     int T2 = 32, CL2 = 1;
