@@ -419,7 +419,12 @@ namespace hssmf_b200 {
         __syncthreads();
         if (warp >= CL) return;
         best_of(wred[b], NW, v, p, ix);
+        // the winner's panel row: nv <= NB values, lane c carries columns
+        // c and c + 32 (NB <= 64)
+        static_assert(NB <= 64, "panel rows are pushed by two lanes' worth of columns");
         const double rv = (lane < nv && ix >= 0) ? Lp[lane * RPC + (ix - rank * RPC)] : 0.0;
+        const double rv2 =
+            (lane + 32 < nv && ix >= 0) ? Lp[(lane + 32) * RPC + (ix - rank * RPC)] : 0.0;
         for (int peer = warp; peer < CL; peer += NW) {
           const uint32_t rbar = mapa(smem_u32(&mbar[b]), peer);
           if (lane == 0)
@@ -430,6 +435,9 @@ namespace hssmf_b200 {
           if (lane < nv)
             st_async_b64(mapa(smem_u32(&strow[b][rank][lane]), peer),
                          (unsigned long long)__double_as_longlong(rv), rbar);
+          if (lane + 32 < nv)
+            st_async_b64(mapa(smem_u32(&strow[b][rank][lane + 32]), peer),
+                         (unsigned long long)__double_as_longlong(rv2), rbar);
         }
       };
       int stopped = 0, cert = 0, jend = k0;
