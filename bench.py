@@ -442,6 +442,22 @@ def config_json(cfg, op, args, n=None, nnz=None, fronts=None):
             "l2": "inputs > L2 (factor storage tens of GB), no flush needed"}
 
 
+def reference_counted(cfg, ms):
+    """the reference's own counters::flops of its full run of this workload
+    (counters.hpp:15-42, tests/golden/ref_<config>.npz) over this step's time:
+    the reference-counted algorithmic rate of the GPU step"""
+    from paper_1502_07405_b200.problems import CONFIGS
+    key = [k for k, v in CONFIGS.items() if v is cfg]
+    path = os.path.join(ROOT, "tests", "golden", f"ref_{key[0]}.npz") if key else ""
+    if not path or not os.path.exists(path):
+        return {}
+    f = float(np.load(path)["flops"])
+    return {"reference_counters_flops": f,
+            "reference_counters_tflops": f / (ms * 1e-3) / 1e12,
+            "reference_counters_note": "counters::flops of the reference's full run (factor "
+                                       "only) / this step's factor+solve time"}
+
+
 def spawn_ranks(n, dry):
     """re-exec this command under torch.distributed.run with n local ranks;
     returns the launcher's exit code"""
@@ -746,9 +762,10 @@ def main():
         "relres": relres,
         "gmres_preconditioned": gm,
         "fp64_tflops_step": flops_total / (ms * 1e-3) / 1e12,
-        "flops_per_step": {"executed": flops_total, "reference_front_model": model_flops,
-                           "reference_model_tflops": (model_flops / (ms * 1e-3) / 1e12
-                                                      if model_flops else None)},
+        "flops_per_step": dict({"executed": flops_total, "reference_front_model": model_flops,
+                                "reference_model_tflops": (model_flops / (ms * 1e-3) / 1e12
+                                                           if model_flops else None)},
+                               **reference_counted(cfg, ms)),
         "e2e": {"value": e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),

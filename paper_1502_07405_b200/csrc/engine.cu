@@ -261,6 +261,10 @@ namespace hssmf_b200 {
       }
     }
     double* assemble_hss_front(int i, cudaStream_t st);
+    // every HSS front of a level at once: one zeroing per front, then one
+    // sparse-scatter launch and one extend-add launch per child slot for the
+    // whole list (assemble_dense semantics and order, multifrontal.hpp:141-170)
+    std::vector<double*> assemble_hss_fronts(const std::vector<int>& lst, cudaStream_t st);
     void assemble_on(int i, const FrontDev& view, cudaStream_t st);
     void upload_front_on(int i, cudaStream_t st) {
       HSSMF_CUDA(cudaMemcpyAsync(d_fronts.as<FrontDev>() + i, &hf[i], sizeof(FrontDev),
@@ -691,6 +695,57 @@ namespace hssmf_b200 {
     return F;
   }
 
+  std::vector<double*> Engine::Impl::assemble_hss_fronts(const std::vector<int>& lst,
+                                                         cudaStream_t st) {
+    std::vector<double*> F(lst.size(), nullptr);
+    if (lst.empty()) return F;
+    // ids, then the two slots' child-column prefixes, in one upload
+    std::vector<long long> pre0{0}, pre1{0};
+    for (size_t q = 0; q < lst.size(); q++) {
+      const int i = lst[q];
+      const auto& fn = t.nodes[i];
+      const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
+      HSSMF_CUDA(cudaMallocAsync((void**)&F[q], (size_t)m * m * sizeof(double) + 8 + (size_t)ns * 4, st));
+      HSSMF_CUDA(cudaMemsetAsync(F[q], 0, (size_t)m * m * sizeof(double), st));
+      FrontDev view = hf0[i];
+      view.P = F[q];
+      view.U = F[q] + (size_t)ns * m;
+      view.C = F[q] + ns + (size_t)ns * m;
+      view.ldu = m;
+      view.ldc = m;
+      view.perm = reinterpret_cast<int*>(F[q] + (size_t)m * m + 1);  // identity written by assembly
+      hf[i] = view;
+      upload_front_on(i, st);
+      pre0.push_back(pre0.back() + (fn.child0 >= 0 ? t.nodes[fn.child0].nu() : 0));
+      pre1.push_back(pre1.back() + (fn.child1 >= 0 ? t.nodes[fn.child1].nu() : 0));
+    }
+    const int nf = (int)lst.size();
+    const size_t bytes = (2 * pre0.size()) * sizeof(long long) + nf * sizeof(int);
+    std::vector<char> h(bytes);
+    std::memcpy(h.data(), pre0.data(), pre0.size() * sizeof(long long));
+    std::memcpy(h.data() + pre0.size() * sizeof(long long), pre1.data(),
+                pre1.size() * sizeof(long long));
+    std::memcpy(h.data() + 2 * pre0.size() * sizeof(long long), lst.data(), nf * sizeof(int));
+    char* d = nullptr;
+    HSSMF_CUDA(cudaMallocAsync((void**)&d, bytes, st));
+    HSSMF_CUDA(cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st));
+    const long long* d0 = reinterpret_cast<const long long*>(d);
+    const long long* d1 = d0 + pre0.size();
+    const int* did = reinterpret_cast<const int*>(d + 2 * pre0.size() * sizeof(long long));
+    const FrontDev* Fd = d_fronts.as<FrontDev>();
+    DenseKernels::assemble_sparse(Fd, did, nf, d_ptr.as<int>(), d_ind.as<int>(), d_val.as<double>(), st);
+    DenseKernels::extend_add(Fd, did, nf, 0, d0, pre0.back(), st);
+    DenseKernels::extend_add(Fd, did, nf, 1, d1, pre1.back(), st);
+    HSSMF_CUDA(cudaFreeAsync(d, st));
+    stream_sync(st);  // h and the views are host data of this frame
+    for (int i : lst) {
+      hf[i] = hf0[i];
+      upload_front_on(i, st);
+    }
+    stream_sync(st);
+    return F;
+  }
+
   // compression + ULV + densified update of an assembled HSS front on its own
   // stream (factor_front_hss, multifrontal.hpp:348-377). Runs on a worker
   // thread; the rank-guard fallback (multifrontal.hpp:414-421) factors the
@@ -786,7 +841,7 @@ namespace hssmf_b200 {
   void Engine::Impl::factor_hss_level(const std::vector<int>& lst) {
     if (lst.empty()) return;
     std::vector<double*> F(lst.size());
-    for (size_t q = 0; q < lst.size(); q++) F[q] = assemble_hss_front(lst[q], s);
+    F = assemble_hss_fronts(lst, s);
     // fronts of >= 9000 rows saturate the device on their own (the Gram-route
     // trailing updates are full-device, HBM-bound kernels, and concurrent
     // ones starve the 16-CTA cluster panels): at most 6 of them at a time
