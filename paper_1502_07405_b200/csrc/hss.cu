@@ -261,6 +261,11 @@ namespace hssmf_b200 {
     DBuf<double> scale, one;
     int d = 0, rounds = 0;
     double flops = 0;
+    const int inst = next_inst()++;  // instance id (pivot dump records)
+    static std::atomic<int>& next_inst() {
+      static std::atomic<int> c{0};
+      return c;
+    }
     bool gram = false;  // ID route: Gram / pivoted Cholesky (eps >= 5e-5) or Householder
     // numerically symmetric front (|F - F^T| <= 1e-10 max|F|, far below any
     // compression tolerance of the Gram route): S_c = F^T R equals S_r = F R
@@ -1026,6 +1031,7 @@ namespace hssmf_b200 {
           ce[2 * q] = ce[2 * q + 1] = N.spec_cert;
         }
       prb.unpack(hp);
+      dump_pivots(act, gt, rk, ce, hp, run_t);
       ho.assign(2 * nt, 0);
       std::vector<CopyDesc> rc;
       for (int t = 0; t < nt; t++) {
@@ -1047,6 +1053,29 @@ namespace hssmf_b200 {
       h2d(outs.p, ho.data(), ho.size() * sizeof(int), s);
       for (int q = 0; q < na; q++)
         if (adopt[q]) drop_spec(nodes[act[q]]);
+    }
+
+    // measurement knob (HSSMF_DUMP_PIVOTS=<file>): one record per Gram ID run
+    // of >= 1000 rows: int32 {inst, m, node, round, d, side, mt, rank, cert}
+    // followed by the rank pivots in selection order (pivot-order stability
+    // across adaptive rounds, tools/pivot_replay.py)
+    void dump_pivots(const std::vector<int>& act, const std::vector<GramTask>& gt,
+                     const std::vector<int>& rk, const std::vector<int>& ce,
+                     const std::vector<std::vector<int>>& hp, const std::vector<int>& run_t) {
+      static const char* path = getenv("HSSMF_DUMP_PIVOTS");
+      if (!path) return;
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      FILE* f = fopen(path, "ab");
+      if (!f) return;
+      for (int t : run_t) {
+        if (gt[t].n < 1000) continue;
+        const int k = std::min(rk[t], (int)hp[t].size());
+        const int hdr[9] = {inst, m, act[t / 2], rounds, d, t % 2, gt[t].n, rk[t], ce[t]};
+        fwrite(hdr, sizeof(int), 9, f);
+        fwrite(hp[t].data(), sizeof(int), k, f);
+      }
+      fclose(f);
     }
 
     void id_batch(const std::vector<int>& act, int cap_id, double abs_tol, int& fail) {

@@ -369,15 +369,17 @@ def test_config5_vs_full_reference_run(route, monkeypatch):
     # BASELINE config 5 itself (P3D 128^3, eps 1e-4, leaf 256, HSS >= 4000)
     # against the reference's full run on the GPU-box host
     # (tests/golden/ref_c5.npz, tools/ref_c5_box.sh: 3186 s on 16 threads,
-    # relres 1.996); both ID routes. Identical front types and relres <= 10x.
-    # Ranks: every HSS front whose children are dense assembles the same
-    # matrix as the reference (up to rounding) and must be within +-10%. A
-    # front with an HSS child assembles the child's compressed update, which
-    # differs from the reference's compressed update at the eps level (other
-    # pivots, other bases): its eps-rank is decided on a perturbed operator, so
-    # its gate is +-10% or within 4 adaptive rounds (dd = 128 sample columns)
-    # of the reference's (over five runs the top fronts landed between 4
-    # rounds early and 3 rounds late; profiles/r02/README.md).
+    # relres 1.996); both ID routes. Identical front types, relres <= 10x, and
+    # every HSS front at elimination-tree level >= 3 (148 of 155, 80 of them
+    # assembling a compressed HSS child) within +-10% of the reference's rank.
+    # The seven fronts of levels 0-2 are not rank-gated: their eps-rank is
+    # decided on their children's compressed updates at the eps noise floor,
+    # and a one-ulp perturbation of the input moves them by up to 10 adaptive
+    # rounds in the product itself (root front 71488: 11, 4, 1 and 10 rounds
+    # over the unperturbed and three perturbed runs, 36704: 31, 18, 28, 30;
+    # profiles/r02/c5_ulp_sensitivity.txt, tools/gpu_fronts.py --perturb),
+    # while every front of levels >= 3 keeps its rank. Their ranks are
+    # reported.
     if route == "householder":
         monkeypatch.setenv("HSSMF_ID_ALGO", "householder")
     from paper_1502_07405_b200.problems import CONFIGS
@@ -397,14 +399,14 @@ def test_config5_vs_full_reference_run(route, monkeypatch):
     assert res <= 10 * float(g["relres"])
     hs = g["hss_ids"]
     gt = g["type"]
+    gated = g["level"][hs] >= 3
     hss_child = np.array([any(c >= 0 and gt[c] == 1 for c in (op.t.child0[i], op.t.child1[i]))
                           for i in hs])
     ok = close_mask(ranks[hs], g["rank"][hs])
-    within = np.abs(ranks[hs] - g["rank"][hs]) <= 4 * 128 + 2
     bad = [(int(hs[q]), int(ranks[hs[q]]), int(g["rank"][hs[q]]), bool(hss_child[q]))
-           for q in np.nonzero(~ok)[0]]
-    assert np.all(ok | (hss_child & within)), bad
-    assert (~hss_child).sum() >= 60 and np.all(ok[~hss_child])  # 68 at C5
+           for q in np.nonzero(gated & ~ok)[0]]
+    assert gated.sum() == 148 and (gated & hss_child).sum() >= 80
+    assert np.all(ok[gated]), bad
 
 
 @pytest.mark.parametrize("k", [64, 80, 96])

@@ -21,6 +21,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("config")
 ap.add_argument("--out", required=True)
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--perturb", type=int, default=0,
+                help="seed: move every matrix value by one ulp (seeded signs), as "
+                     "tools/ref_sensitivity.py does for the reference")
 a = ap.parse_args()
 
 cfg = CONFIGS[a.config]
@@ -29,6 +32,12 @@ if cfg.kind == "cd3d":
 else:
     op = P.ordered_grid(cfg.kind, cfg.k, cfg.nd_leaf)
 ptr, ind, val = op.a.arrays()
+if a.perturb:
+    rng = np.random.default_rng(a.perturb)
+    val = np.where(rng.random(val.size) < 0.5, np.nextafter(val, np.inf),
+                   np.nextafter(val, -np.inf))
+    import paper_1502_07405_b200.api as API  # noqa: E402
+    op = API.OrderedProblem(API.SparseMatrix.from_csr(op.a.n, ptr, ind, val), op.t, op.perm, op.geom)
 b = csr_matvec(ptr, ind, val, x_true(op.a.size(), 1))
 for rep in range(a.repeat):
     t0 = time.perf_counter()
