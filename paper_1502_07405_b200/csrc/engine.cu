@@ -279,7 +279,7 @@ namespace hssmf_b200 {
     std::vector<double*> region_c;  // pool-allocated update blocks of region fronts
     std::vector<int> region_singular;  // first zero-pivot column per region front
     int region_level = -1;             // deepest level holding an HSS front
-    HssResult compress_hss_front(int i, double* F, cudaStream_t st);
+    HssResult compress_hss_front(int i, double* F, cudaStream_t st, int peers = 0);
     void factor_hss_level(const std::vector<int>& lst);
     size_t devmem_bytes() const;  // engine-owned cudaMalloc storage
   };
@@ -750,7 +750,8 @@ namespace hssmf_b200 {
   // stream (factor_front_hss, multifrontal.hpp:348-377). Runs on a worker
   // thread; the rank-guard fallback (multifrontal.hpp:414-421) factors the
   // assembled front densely in place.
-  Engine::Impl::HssResult Engine::Impl::compress_hss_front(int i, double* F, cudaStream_t st) {
+  Engine::Impl::HssResult Engine::Impl::compress_hss_front(int i, double* F, cudaStream_t st,
+                                                             int peers) {
     HssResult res;
     const auto& fn = t.nodes[i];
     const int ns = fn.ns(), nu = fn.nu(), m = ns + nu;
@@ -763,6 +764,7 @@ namespace hssmf_b200 {
     ho.dd = opt.dd;
     ho.p = opt.p;
     ho.max_rank = std::min(opt.resolved_max_rank(t.n), m);
+    ho.peers = peers;
     auto H = std::make_unique<HssMatrixDev>(st);
     bool fallback = false;
     // the compression reads the front through TMA-fed GEMMs, which need an
@@ -891,7 +893,7 @@ namespace hssmf_b200 {
         tstart[q] = a - t0;
         const SyncClock c0 = sync_clock();
         try {
-          res[q] = compress_hss_front(lst[q], F[q], hstreams[w]);
+          res[q] = compress_hss_front(lst[q], F[q], hstreams[w], (int)lst.size());
         } catch (const CudaError& e) {
           // the front's own buffers are released on unwinding; its assembled
           // dense front F is read-only in the HSS path, so it is retried alone
@@ -921,7 +923,7 @@ namespace hssmf_b200 {
       if (dbg) fprintf(stderr, "[hssmf]   front %d: out of memory concurrently, retried alone\n", lst[q]);
       const double a = now();
       try {
-        res[q] = compress_hss_front(lst[q], F[q], hstreams[0]);
+        res[q] = compress_hss_front(lst[q], F[q], hstreams[0], 1);
       } catch (const std::exception& e) {
         res[q].error = e.what();
       }

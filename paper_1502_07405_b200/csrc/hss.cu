@@ -500,7 +500,7 @@ namespace hssmf_b200 {
             HSSMF_CUDA(cudaEventRecord(side.done, side.s));
           };
         }
-        for (int lv = maxdepth; lv >= 0; lv--) pass_level(lv, cap_id, abs_tol, fail);
+        pass_wavefronts(cap_id, abs_tol, fail);
         if (nodes[root].state == DONE) {
           pending_spec = nullptr;
           break;
@@ -641,14 +641,63 @@ namespace hssmf_b200 {
       f();
     }
 
-    void pass_level(int lv, int cap_id, double abs_tol, int& fail) {
-      std::vector<int> act;
-      for (int n : levels[lv]) {
-        auto& N = nodes[n];
-        if (N.state == DONE) continue;
-        if (!N.leaf && (nodes[N.c0].state != DONE || nodes[N.c1].state != DONE)) continue;
-        act.push_back(n);
+    // One bottom-up pass (compress_pass, hss_compress.hpp:211-297). The
+    // reference visits a node once per round, after its children; a node runs
+    // its ID iff both children are done by then. The nodes whose children were
+    // done before the round are independent of each other whatever their HSS
+    // level, so they form ONE batch (one pivot chain as long as the longest
+    // instead of one per level); parents enabled by this round's
+    // certifications follow in further batches. HSSMF_LEVEL_PASS=1 keeps one
+    // batch per HSS level.
+    void pass_wavefronts(int cap_id, double abs_tol, int& fail) {
+      static const bool by_level = getenv("HSSMF_LEVEL_PASS") != nullptr;
+      if (by_level) {
+        for (int lv = maxdepth; lv >= 0; lv--) {
+          std::vector<int> act;
+          for (int n : levels[lv]) {
+            auto& N = nodes[n];
+            if (N.state == DONE) continue;
+            if (!N.leaf && (nodes[N.c0].state != DONE || nodes[N.c1].state != DONE)) continue;
+            act.push_back(n);
+          }
+          pass_nodes(act, cap_id, abs_tol, fail);
+        }
+        return;
       }
+      std::vector<char> tried(nodes.size(), 0);
+      for (;;) {
+        std::vector<int> act;
+        for (int lv = maxdepth; lv >= 0; lv--)
+          for (int n : levels[lv]) {
+            auto& N = nodes[n];
+            if (N.state == DONE || tried[n]) continue;
+            if (!N.leaf && (nodes[N.c0].state != DONE || nodes[N.c1].state != DONE)) continue;
+            act.push_back(n);
+          }
+        if (act.empty()) return;
+        for (int n : act) tried[n] = 1;
+        // tasks of one batch share the launch geometry (cluster size, tile
+        // grid), sized by the largest: far smaller nodes go into a batch of
+        // their own
+        std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return rows_of(a) > rows_of(b); });
+        size_t b0 = 0;
+        while (b0 < act.size()) {
+          size_t b1 = b0 + 1;
+          while (b1 < act.size() && 4 * rows_of(act[b1]) >= rows_of(act[b0])) b1++;
+          std::vector<int> part(act.begin() + b0, act.begin() + b1);
+          std::sort(part.begin(), part.end());
+          pass_nodes(part, cap_id, abs_tol, fail);
+          b0 = b1;
+        }
+      }
+    }
+    // rows of a node's local samples (known before its first pass)
+    int rows_of(int n) const {
+      const auto& N = nodes[n];
+      return N.leaf ? N.size() : nodes[N.c0].r + nodes[N.c1].r;
+    }
+
+    void pass_nodes(std::vector<int> act, int cap_id, double abs_tol, int& fail) {
       if (act.empty()) return;
       auto* ph1 = new Ph(this, 1);
       // extract the dense pieces once (compress_pass, hss_compress.hpp:226-237)
@@ -813,9 +862,11 @@ namespace hssmf_b200 {
     // and 9.98 s (>= 6000) against 9.00 s without -- the speculative rounds
     // compete with the other fronts' work and their host-side setup delays the
     // pair, so the adopted rounds do not pay for it yet
-    static bool spec_id_enabled() {
+    bool spec_id_enabled() const {
       static const bool on = getenv("HSSMF_SPEC_ID") != nullptr;
-      return on;
+      // HSSMF_SPEC_PEERS=n: also for fronts of tree levels with at most n fronts
+      static const int peers = getenv("HSSMF_SPEC_PEERS") ? atoi(getenv("HSSMF_SPEC_PEERS")) : 0;
+      return on || (o.peers > 0 && o.peers <= peers);
     }
     // large IDs only: below this the device is busy with other fronts' work
     // and the speculation competes with it instead of filling idle SMs
@@ -1031,7 +1082,7 @@ namespace hssmf_b200 {
           ce[2 * q] = ce[2 * q + 1] = N.spec_cert;
         }
       prb.unpack(hp);
-      dump_pivots(act, gt, rk, ce, hp, run_t);
+      dump_pivots(act, gt, rk, ce, hp, run_t, Luse, perm);
       ho.assign(2 * nt, 0);
       std::vector<CopyDesc> rc;
       for (int t = 0; t < nt; t++) {
@@ -1041,6 +1092,16 @@ namespace hssmf_b200 {
         if (sym && t % 2) {  // the row side's twin: its coefficients are reused
           tasks[t] = tasks[t - 1];
           continue;
+        }
+        // a failing node keeps nothing of its IDs (compress_pass returns before
+        // touching the node, hss_compress.hpp:255-259; id_finalize skips it)
+        {
+          const int q = t / 2;
+          if (!ce[2 * q] || rk[2 * q] > cap_id || !ce[2 * q + 1] || rk[2 * q + 1] > cap_id) {
+            tasks[t] = {nullptr, k, mt, std::max(k, 1), std::max(cap_id, 0), perm[t].p, nullptr,
+                        outs.p + 2 * t};
+            continue;
+          }
         }
         Y[t].alloc((size_t)std::max(k, 1) * mt + 1, s);
         X[t].alloc((size_t)k * std::max(mt - k, 0) + 1, s);
@@ -1057,13 +1118,30 @@ namespace hssmf_b200 {
 
     // measurement knob (HSSMF_DUMP_PIVOTS=<file>): one record per Gram ID run
     // of >= 1000 rows: int32 {inst, m, node, round, d, side, mt, rank, cert}
-    // followed by the rank pivots in selection order (pivot-order stability
-    // across adaptive rounds, tools/pivot_replay.py)
+    // followed by the rank pivots in selection order and their norms
+    // L(p_j, j) as float64 (pivot-order stability and residual decay across
+    // adaptive rounds, tools/pivot_replay.py, tools/pivot_rounds.py)
     void dump_pivots(const std::vector<int>& act, const std::vector<GramTask>& gt,
                      const std::vector<int>& rk, const std::vector<int>& ce,
-                     const std::vector<std::vector<int>>& hp, const std::vector<int>& run_t) {
+                     const std::vector<std::vector<int>>& hp, const std::vector<int>& run_t,
+                     const std::vector<const double*>& Luse, std::vector<DBuf<int>>& perm) {
       static const char* path = getenv("HSSMF_DUMP_PIVOTS");
       if (!path) return;
+      // the pivot norms L(p_j, j) of every dumped task (side field | 0x100)
+      std::vector<std::vector<double>> nr(gt.size());
+      {
+        std::vector<DBuf<double>> dv(gt.size());
+        for (int t : run_t) {
+          if (gt[t].n < 1000) continue;
+          const int k = std::min(rk[t], (int)hp[t].size());
+          nr[t].resize(k);
+          if (!k) continue;
+          dv[t].alloc(k, s);
+          diag_gather_run(Luse[t], gt[t].n, perm[t].p, k, dv[t].p, s);
+          d2h(nr[t].data(), dv[t].p, k * sizeof(double), s);
+        }
+        stream_sync(s);
+      }
       static std::mutex mu;
       std::lock_guard<std::mutex> lk(mu);
       FILE* f = fopen(path, "ab");
@@ -1071,9 +1149,10 @@ namespace hssmf_b200 {
       for (int t : run_t) {
         if (gt[t].n < 1000) continue;
         const int k = std::min(rk[t], (int)hp[t].size());
-        const int hdr[9] = {inst, m, act[t / 2], rounds, d, t % 2, gt[t].n, rk[t], ce[t]};
+        const int hdr[9] = {inst, m, act[t / 2], rounds, d, (t % 2) | 0x100, gt[t].n, rk[t], ce[t]};
         fwrite(hdr, sizeof(int), 9, f);
         fwrite(hp[t].data(), sizeof(int), k, f);
+        fwrite(nr[t].data(), sizeof(double), k, f);
       }
       fclose(f);
     }

@@ -31,6 +31,10 @@ namespace hssmf_b200 {
   struct HssOpts {
     double eps = 1e-8;
     int d0 = 128, dd = 128, p = 10, max_rank = 5000;
+    // fronts compressed concurrently with this one (0: unknown): with few of
+    // them the device idles through the pivot chains, so the next round's IDs
+    // are computed speculatively beside the current ones
+    int peers = 0;
   };
 
   struct HssRankError : std::runtime_error {

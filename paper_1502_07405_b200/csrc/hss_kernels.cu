@@ -53,6 +53,12 @@ namespace hssmf_b200 {
         dst[g.off + i] = g.src[i];
     }
 
+    __global__ void diag_gather_kernel(const double* __restrict__ L, int n, const int* __restrict__ perm,
+                                       int k, double* __restrict__ out) {
+      const int j = blockIdx.x * blockDim.x + threadIdx.x;
+      if (j < k) out[j] = L[perm[j] + (size_t)j * n];
+    }
+
     __global__ void maxabs_kernel(const double* __restrict__ a, long long lda, int m, int n,
                                   unsigned long long* out) {
       double mx = 0;
@@ -536,6 +542,12 @@ namespace hssmf_b200 {
       maxn = std::max(maxn, g.n);
     }
     flush();
+  }
+
+  void diag_gather_run(const double* L, int n, const int* perm, int k, double* out, cudaStream_t s) {
+    if (k <= 0) return;
+    diag_gather_kernel<<<ceil_div(k, 256), 256, 0, s>>>(L, n, perm, k, out);
+    HSSMF_LAUNCH_CHECK();
   }
 
   void maxabs_run(const double* a, long long lda, int m, int n, double* out, cudaStream_t s) {

@@ -50,6 +50,8 @@ namespace hssmf_b200 {
   // *out = max(*out, max |a(i, j)|) over an m x n block (ld lda); out is a
   // device double holding a non-negative value (bitwise int64 ordering)
   void maxabs_run(const double* a, long long lda, int m, int n, double* out, cudaStream_t s);
+  // out[j] = L(perm[j], j), j < k: the pivot norms of a pivoted Cholesky (measurement dumps)
+  void diag_gather_run(const double* L, int n, const int* perm, int k, double* out, cudaStream_t s);
 
   // ---- ULV solve (hss_ulv.hpp:226-276), one CTA per node of one HSS level
   struct UlvSolveNode {

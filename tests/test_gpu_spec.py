@@ -31,7 +31,8 @@ print(json.dumps({"x": hashlib.sha256(x.tobytes()).hexdigest(), "rank": m.rank.t
 def run(env_extra):
     env = {k: v for k, v in os.environ.items()
            if k not in ("HSSMF_SPEC_FOLD", "HSSMF_NO_SPEC_SAMPLING", "HSSMF_NO_SYM",
-                        "HSSMF_SPEC_ID", "HSSMF_SPEC_ID_ROWS")}
+                        "HSSMF_SPEC_ID", "HSSMF_SPEC_ID_ROWS", "HSSMF_SPEC_PEERS",
+                        "HSSMF_LEVEL_PASS")}
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], capture_output=True, text=True,
                          env=env, timeout=600)
@@ -67,3 +68,14 @@ def test_speculative_ids_are_bitwise_neutral():
     assert base["hss"] > 0
     assert base["rank"] == spec["rank"]
     assert base["x"] == spec["x"]
+
+
+def test_wavefront_batches_match_level_batches():
+    # the IDs of all nodes whose children are done run as one batch whatever
+    # their HSS level (one pivot chain instead of one per level); the same
+    # nodes run the same IDs in the same rounds as with one batch per level
+    level = run({"HSSMF_LEVEL_PASS": "1"})
+    wave = run({})
+    assert level["hss"] > 0
+    assert level["rank"] == wave["rank"]
+    assert level["x"] == wave["x"]

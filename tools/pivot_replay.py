@@ -23,8 +23,13 @@ def read(path):
         k = min(rank, mt)
         piv = a[i + 9:i + 9 + k].copy()
         i += 9 + k
+        nrm = None
+        if side & 0x100:  # pivot norms follow (float64)
+            nrm = a[i:i + 2 * k].copy().view(np.float64)
+            i += 2 * k
+            side &= 0xff
         recs.append(dict(inst=inst, m=m, node=node, round=rnd, d=d, side=side, mt=mt,
-                         rank=rank, cert=cert, piv=piv))
+                         rank=rank, cert=cert, piv=piv, nrm=nrm))
     return recs
 
 
