@@ -1,4 +1,5 @@
 #include "cpqr.cuh"
+#include "staging.cuh"
 
 #include <cooperative_groups.h>
 
@@ -522,10 +523,115 @@ namespace hssmf_b200 {
       for (int r = 0; r < TB; r++)
         if (r < S.bs) col[r] = x[r];
     }
+
+    // inverse of an upper-triangular diagonal block (bs <= 64): thread j solves
+    // R x = e_j by back substitution from the shared copy of the block;
+    // out is 64 x 64 (ld 64), zero below the diagonal and beyond bs
+    struct InvStep {
+      const double* R;
+      int ldr, bs;
+      double* out;
+    };
+    __global__ void __launch_bounds__(TB) tri_inv_kernel(const InvStep* __restrict__ st) {
+      const InvStep S = st[blockIdx.x];
+      __shared__ double Rb[TB][TB + 1];
+      for (int e = threadIdx.x; e < S.bs * S.bs; e += TB) {
+        const int r = e % S.bs, c = e / S.bs;
+        Rb[r][c] = S.R[r + (size_t)c * S.ldr];
+      }
+      __syncthreads();
+      const int j = threadIdx.x;
+      double* o = S.out + (size_t)j * TB;
+      if (j >= S.bs) {
+        for (int i = 0; i < TB; i++) o[i] = 0.0;
+        return;
+      }
+      double x[TB];
+#pragma unroll
+      for (int i = 0; i < TB; i++) x[i] = 0.0;
+#pragma unroll
+      for (int i = TB - 1; i >= 0; i--) {
+        if (i <= j) {
+          double sacc = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+          for (int l = i + 1; l < TB; l++)
+            if (l <= j) sacc -= Rb[i][l] * x[l];
+          x[i] = sacc / Rb[i][i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TB; i++) o[i] = x[i];
+    }
   }  // namespace
 
   void id_solve_blocked(const std::vector<CpqrTask>& tasks, const std::vector<int>& ranks,
-                        cudaStream_t s, double* flops) {
+                        cudaStream_t s, double* flops, bool inv_blocks) {
+    if (inv_blocks) {
+      // X = R2; all diagonal blocks inverted in one launch; per block from the
+      // bottom: W = inv(R_bb) X_b (GEMM), X[0:i0] -= R[0:i0, b] W (GEMM), X_b = W
+      std::vector<InvStep> inv;
+      std::vector<size_t> first(tasks.size(), 0);
+      int maxb = 0;
+      size_t wtot = 0;
+      std::vector<size_t> woff(tasks.size(), 0);
+      for (size_t t = 0; t < tasks.size(); t++) {
+        const int k = ranks[t], nc = tasks[t].n - k;
+        if (k <= 0 || nc <= 0) continue;
+        HSSMF_CUDA(cudaMemcpy2DAsync(tasks[t].X, (size_t)k * sizeof(double),
+                                     tasks[t].Y + (size_t)k * tasks[t].ldy,
+                                     (size_t)tasks[t].ldy * sizeof(double), (size_t)k * sizeof(double),
+                                     nc, cudaMemcpyDeviceToDevice, s));
+        const int nb = (k + TB - 1) / TB;
+        maxb = std::max(maxb, nb);
+        first[t] = inv.size();
+        for (int j = 0; j < nb; j++) {
+          const int i1 = k - j * TB, i0 = std::max(0, i1 - TB);
+          inv.push_back({tasks[t].Y + i0 + (size_t)i0 * tasks[t].ldy, tasks[t].ldy, i1 - i0, nullptr});
+        }
+        woff[t] = wtot;
+        wtot += (size_t)TB * nc;
+      }
+      if (inv.empty()) return;
+      char* buf = nullptr;
+      const size_t inv_bytes = inv.size() * (size_t)TB * TB * sizeof(double);
+      const size_t st_bytes = inv.size() * sizeof(InvStep);
+      HSSMF_CUDA(cudaMallocAsync((void**)&buf, inv_bytes + wtot * sizeof(double) + st_bytes, s));
+      double* invs = reinterpret_cast<double*>(buf);
+      double* W = invs + inv.size() * (size_t)TB * TB;
+      InvStep* dst = reinterpret_cast<InvStep*>(buf + inv_bytes + wtot * sizeof(double));
+      for (size_t q = 0; q < inv.size(); q++) inv[q].out = invs + q * (size_t)TB * TB;
+      h2d(dst, inv.data(), st_bytes, s);  // (copied out of the vector before returning)
+      tri_inv_kernel<<<(unsigned)inv.size(), TB, 0, s>>>(dst);
+      HSSMF_LAUNCH_CHECK();
+      for (int j = 0; j < maxb; j++) {
+        std::vector<GemmProblem> solve, up;
+        struct Back { double* x; int ldx, bs, nc; const double* w; };
+        std::vector<Back> back;
+        for (size_t t = 0; t < tasks.size(); t++) {
+          const auto& T = tasks[t];
+          const int k = ranks[t], nc = T.n - k;
+          if (k <= 0 || nc <= 0) continue;
+          const int i1 = k - j * TB;
+          if (i1 <= 0) continue;
+          const int i0 = std::max(0, i1 - TB), bs = i1 - i0;
+          double* Wt = W + woff[t];
+          solve.push_back({inv[first[t] + j].out, T.X + i0, Wt, bs, nc, bs, TB, k, TB});
+          if (i0 > 0) {
+            up.push_back({T.Y + (size_t)i0 * T.ldy, Wt, T.X, i0, nc, bs, T.ldy, TB, k});
+            if (flops) *flops += 2.0 * i0 * nc * bs;
+          }
+          back.push_back({T.X + i0, k, bs, nc, Wt});
+          if (flops) *flops += (double)bs * bs * nc;
+        }
+        gemm_run_host(solve, 'N', 'N', 1.0, 0.0, s);
+        gemm_run_host(up, 'N', 'N', -1.0, 1.0, s);
+        for (const auto& b : back)
+          HSSMF_CUDA(cudaMemcpy2DAsync(b.x, (size_t)b.ldx * sizeof(double), b.w, (size_t)TB * sizeof(double),
+                                       (size_t)b.bs * sizeof(double), b.nc, cudaMemcpyDeviceToDevice, s));
+      }
+      HSSMF_CUDA(cudaFreeAsync(buf, s));
+      return;
+    }
     // X = R2 (copies), then blocks from the bottom
     int maxb = 0;
     for (size_t t = 0; t < tasks.size(); t++) {

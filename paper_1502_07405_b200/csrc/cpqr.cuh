@@ -30,8 +30,11 @@ namespace hssmf_b200 {
   // X = R2; for each 64-row block from the bottom, a triangular solve of the
   // block (CTA per 128 columns) and a DMMA GEMM update of the rows above
   // (reference trsm, kernels.hpp:205-244, with the same recursion base)
+  // inv_blocks: the 64 x 64 diagonal blocks are inverted first (one launch for
+  // all blocks of all tasks) and each block solve becomes a DMMA GEMM with the
+  // inverse (Gram route; the Householder route keeps the substitution kernel)
   void id_solve_blocked(const std::vector<CpqrTask>& tasks, const std::vector<int>& ranks,
-                        cudaStream_t s, double* flops = nullptr);
+                        cudaStream_t s, double* flops = nullptr, bool inv_blocks = false);
 
   // convenience: both phases with an internal rank readback
   void cpqr_id_run(const CpqrTask* tasks, int ntask, int max_m, int max_n, double eps,

@@ -309,18 +309,31 @@ namespace hssmf_b200 {
     // CPQR column swap is resolved locally (the row at position j is the one
     // whose position equals j; it takes the pivot's old position, which
     // travels with the candidate).
+    // warp-wide best candidate (largest v, lowest position on ties), returned
+    // to every lane. Non-negative doubles order like their bit patterns, so the
+    // argmax is three redux.sync operations (high word, low word among the
+    // high-word winners, lowest position among the value winners) and one
+    // broadcast instead of a five-level butterfly of four shuffles each. A lane
+    // without a candidate passes v = -1 (p = INT_MAX, ix = -1): it keys as
+    // zero and loses every tie on its position.
     __device__ __forceinline__ void warp_best(double& v, int& p, int& ix) {
-      for (int o = 16; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
-        if (better(v2, p2, v, p)) { v = v2; p = p2; ix = i2; }
-      }
+      const unsigned full = 0xffffffffu;
+      const unsigned long long bits = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+      const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+      const unsigned mh = __reduce_max_sync(full, hi);
+      const unsigned ml = __reduce_max_sync(full, hi == mh ? lo : 0u);
+      const bool top = hi == mh && lo == ml;
+      const unsigned mp = __reduce_min_sync(full, top ? (unsigned)p : 0xffffffffu);
+      const unsigned win = __ballot_sync(full, top && (unsigned)p == mp);
+      const int src = __ffs(win) - 1;  // (some lane always matches: mp is a top lane's position)
+      ix = __shfl_sync(full, ix, src);
+      p = (int)mp;
+      v = ix >= 0 ? __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)) : -1.0;
     }
 
     // best of the first cnt (<= 32) candidates in shared memory, returned to
-    // every lane: a short sequential scan for a few entries, otherwise a
-    // log2(cnt)-level butterfly over the low lanes and a broadcast
+    // every lane: a short sequential scan for a few entries, otherwise the
+    // warp argmax over the low lanes
     __device__ __forceinline__ void best_of(const Cand* c, int cnt, double& v, int& p, int& ix) {
       if (cnt <= 4) {
         v = c[0].v;
@@ -343,16 +356,7 @@ namespace hssmf_b200 {
         p = INT_MAX;
         ix = -1;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        if (o >= cnt) continue;  // uniform: lanes >= cnt hold no candidate
-        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
-        if (better(v2, p2, v, p)) { v = v2; p = p2; ix = i2; }
-      }
-      v = __shfl_sync(0xffffffffu, v, 0);
-      p = __shfl_sync(0xffffffffu, p, 0);
-      ix = __shfl_sync(0xffffffffu, ix, 0);
+      warp_best(v, p, ix);
     }
 
     template <int R, int NB>
@@ -731,6 +735,88 @@ namespace hssmf_b200 {
           }
     }
 
+    // Variant of the tensor-pipe update with more tiles in flight per SM
+    // (HSSMF_GRAM_SYRK=rmw): the G tile is read and written after the products
+    // (no 16 preloaded entries per thread), so a CTA needs at most 64
+    // registers per thread and four CTAs share an SM; while one waits for its
+    // L blocks or runs its products, the others' G traffic keeps HBM busy.
+    template <int NB, int OCC>
+    __global__ void __launch_bounds__(256, OCC)
+    gram_syrk_rmw_kernel(const GramTask* __restrict__ tasks, int k0,
+                         unsigned long long* probe_bytes) {
+      constexpr int SP = 68;
+      const GramTask Tk = tasks[blockIdx.y];
+      const int n = Tk.n;
+      const int nbt = (n + 63) >> 6;
+      const int t = blockIdx.x;
+      if (t >= nbt * (nbt + 1) / 2) return;
+      if (__ldcg(Tk.state + 1)) return;
+      if (probe_bytes && t == 0 && threadIdx.x == 0)
+        atomicAdd(probe_bytes, (unsigned long long)n * (n + 1) / 2 * 16ull);
+      auto before = [&](int c) { return c * nbt - c * (c - 1) / 2; };
+      const double bb = 2.0 * nbt + 1.0;
+      int tj = (int)((bb - sqrt(fmax(bb * bb - 8.0 * t, 0.0))) * 0.5);
+      tj = max(0, min(tj, nbt - 1));
+      while (tj > 0 && before(tj) > t) tj--;
+      while (tj + 1 < nbt && before(tj + 1) <= t) tj++;
+      const int ti = tj + (t - before(tj));
+      const int i0 = ti * 64, j0 = tj * 64;
+      extern __shared__ __align__(16) double sm7[];
+      double* As = sm7;
+      double* Bs = sm7 + NB * SP;
+      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+      const double* Lk = Tk.L + (size_t)k0 * n;
+      for (int e = tid; e < NB * 64; e += 256) {
+        const int q = e >> 6, r = e & 63;
+        const bool va = i0 + r < n, vb = j0 + r < n;
+        cp_async8(As + q * SP + r, va ? Lk + i0 + r + (size_t)q * n : Lk, va);
+        cp_async8(Bs + q * SP + r, vb ? Lk + j0 + r + (size_t)q * n : Lk, vb);
+      }
+      cp_async_commit();
+      const int wm = warp & 1, wn = warp >> 1;
+      const int lr = lane >> 2, lc = lane & 3;
+      double* G = Tk.G;
+      cp_async_wait<0>();
+      __syncthreads();
+      double acc[4][2][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NB; kk += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++) a[mi] = As[(kk + lc) * SP + 32 * wm + 8 * mi + lr];
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) b[ni] = Bs[(kk + lc) * SP + 16 * wn + 8 * ni + lr];
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+          for (int ni = 0; ni < 2; ni++) dmma8x8x4(acc[mi][ni], a[mi], b[ni]);
+      }
+      // two columns per lane are adjacent in no dimension (column stride n):
+      // one 8-byte access per entry, the loads of a half tile issued together
+#pragma unroll
+      for (int ni = 0; ni < 2; ni++) {
+        double g[4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            const int i = i0 + 32 * wm + 8 * mi + lr, j = j0 + 16 * wn + 8 * ni + 2 * lc + v;
+            g[mi][v] = (i < n && j < n && i >= j) ? G[i + (size_t)j * n] : 0.0;
+          }
+#pragma unroll
+        for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            const int i = i0 + 32 * wm + 8 * mi + lr, j = j0 + 16 * wn + 8 * ni + 2 * lc + v;
+            if (i < n && j < n && i >= j) G[i + (size_t)j * n] = g[mi][v] - acc[mi][ni][v];
+          }
+      }
+    }
+
     // Persistent form of the trailing update (opt-in, HSSMF_GRAM_SYRK=persist):
     // every CTA walks the lower 64 x 64 tiles of all tasks (stride gridDim.x)
     // and double-buffers them through shared memory, the next tile's G and L
@@ -962,6 +1048,10 @@ namespace hssmf_b200 {
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_persist_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kSyrkPersistSmem));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_rmw_kernel<NB2, 3>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
+        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_rmw_kernel<NB2, 4>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
       });
       while (CL2 * RPC_MAX < max_n) CL2 *= 2;
       T2 = std::max(32, ((max_n + CL2 - 1) / CL2 + 31) / 32 * 32);
@@ -975,6 +1065,8 @@ namespace hssmf_b200 {
     // slower on c5: 1.92 TB/s against 2.51 for one tile per CTA, 2 CTAs per SM,
     // profiles/r02/README.md)
     const bool syrk_persist = esy && !strcmp(esy, "persist");
+    const bool syrk_rmw4 = esy && !strcmp(esy, "rmw4");
+    const bool syrk_rmw = esy && (!strcmp(esy, "rmw") || syrk_rmw4);
     // all panels are queued without host round trips: a finished task's
     // panel kernel returns at once and its trailing GEMM is skipped on device
     for (int k0 = 0; k0 <= kmax; k0 += nb) {
@@ -1016,7 +1108,13 @@ namespace hssmf_b200 {
             const int grid = std::max(1, std::min(sp.pre[nt], 148));
             gram_syrk_persist_kernel<NB2><<<grid, 256, kSyrkPersistSmem, s>>>(
                 (const GramTask*)d, k0, sp, pb);
-          } else if (syrk_cuda_cores)
+          } else if (syrk_rmw4)
+            gram_syrk_rmw_kernel<NB2, 4><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
+                (const GramTask*)d, k0, pb);
+          else if (syrk_rmw)
+            gram_syrk_rmw_kernel<NB2, 3><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
+                (const GramTask*)d, k0, pb);
+          else if (syrk_cuda_cores)
             gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
                 (const GramTask*)d, k0, pb);
           else

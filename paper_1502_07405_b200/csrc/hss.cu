@@ -1211,6 +1211,10 @@ namespace hssmf_b200 {
       id_finalize(act, cap_id, fail, Y, X, perm, tasks, ho, hp);
     }
 
+    static bool no_inv_blocks() {
+      static const bool v = getenv("HSSMF_ID_SOLVE") && !strcmp(getenv("HSSMF_ID_SOLVE"), "subst");
+      return v;
+    }
     void id_finalize(const std::vector<int>& act, int cap_id, int& fail,
                      std::vector<DBuf<double>>& Y, std::vector<DBuf<double>>& X,
                      std::vector<DBuf<int>>& perm, std::vector<CpqrTask>& tasks,
@@ -1247,7 +1251,7 @@ namespace hssmf_b200 {
         }
       }
       if (okq.empty()) return;
-      if (!big_tasks.empty()) id_solve_blocked(big_tasks, big_ranks, s, &flops);
+      if (!big_tasks.empty()) id_solve_blocked(big_tasks, big_ranks, s, &flops, gram && !no_inv_blocks());
       if (!solve_tasks.empty()) {
         DBuf<CpqrTask> ds;
         ds.alloc(solve_tasks.size(), s);
