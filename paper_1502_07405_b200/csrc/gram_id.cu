@@ -378,6 +378,10 @@ namespace hssmf_b200 {
       __shared__ __align__(8) unsigned long long mbar[2];
       __shared__ Cand wred[2][16];
 
+      // (a warm-started task resumes at step kw from the state the fixed-order
+      // panels left; only cold tasks initialise in their first panel)
+      init = init && Tk.kw == 0;
+      k0 += Tk.kw;
       if (__ldcg(Tk.state + 1) && !init) return;  // finished in an earlier panel (uniform)
       double dg[R];
       int pos[R], flg[R];
@@ -494,6 +498,10 @@ namespace hssmf_b200 {
           stopped = 1;
           cert = ct;
           jend = j;
+          if (Tk.pvlast && rank == 0 && tid == 0) {
+            __stcg(Tk.pvlast + 0, pv);
+            __stcg(Tk.pvlast + 1, r11);
+          }
           break;
         }
         const int pj = bi, pp = bp;
@@ -587,6 +595,7 @@ namespace hssmf_b200 {
     __global__ void __launch_bounds__(256, 2)
     gram_syrk_kernel(const GramTask* __restrict__ tasks, int k0, unsigned long long* probe_bytes) {
       const GramTask Tk = tasks[blockIdx.y];
+      k0 += Tk.kw;
       const int n = Tk.n;
       const int nbt = (n + 63) >> 6;
       const int t = blockIdx.x;
@@ -660,9 +669,16 @@ namespace hssmf_b200 {
     template <int NB>
     __global__ void __launch_bounds__(256, 2)
     gram_syrk_dmma_kernel(const GramTask* __restrict__ tasks, int k0,
-                          unsigned long long* probe_bytes) {
+                          unsigned long long* probe_bytes, int warm) {
       constexpr int SP = 68;
       const GramTask Tk = tasks[blockIdx.y];
+      // warm phase: absolute panel k0 of the tasks still inside their warm
+      // part; search phase: panels counted from each task's kw
+      if (warm) {
+        if (k0 >= Tk.kw) return;
+      } else {
+        k0 += Tk.kw;
+      }
       const int n = Tk.n;
       const int nbt = (n + 63) >> 6;
       const int t = blockIdx.x;
@@ -735,88 +751,6 @@ namespace hssmf_b200 {
           }
     }
 
-    // Variant of the tensor-pipe update with more tiles in flight per SM
-    // (HSSMF_GRAM_SYRK=rmw): the G tile is read and written after the products
-    // (no 16 preloaded entries per thread), so a CTA needs at most 64
-    // registers per thread and four CTAs share an SM; while one waits for its
-    // L blocks or runs its products, the others' G traffic keeps HBM busy.
-    template <int NB, int OCC>
-    __global__ void __launch_bounds__(256, OCC)
-    gram_syrk_rmw_kernel(const GramTask* __restrict__ tasks, int k0,
-                         unsigned long long* probe_bytes) {
-      constexpr int SP = 68;
-      const GramTask Tk = tasks[blockIdx.y];
-      const int n = Tk.n;
-      const int nbt = (n + 63) >> 6;
-      const int t = blockIdx.x;
-      if (t >= nbt * (nbt + 1) / 2) return;
-      if (__ldcg(Tk.state + 1)) return;
-      if (probe_bytes && t == 0 && threadIdx.x == 0)
-        atomicAdd(probe_bytes, (unsigned long long)n * (n + 1) / 2 * 16ull);
-      auto before = [&](int c) { return c * nbt - c * (c - 1) / 2; };
-      const double bb = 2.0 * nbt + 1.0;
-      int tj = (int)((bb - sqrt(fmax(bb * bb - 8.0 * t, 0.0))) * 0.5);
-      tj = max(0, min(tj, nbt - 1));
-      while (tj > 0 && before(tj) > t) tj--;
-      while (tj + 1 < nbt && before(tj + 1) <= t) tj++;
-      const int ti = tj + (t - before(tj));
-      const int i0 = ti * 64, j0 = tj * 64;
-      extern __shared__ __align__(16) double sm7[];
-      double* As = sm7;
-      double* Bs = sm7 + NB * SP;
-      const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-      const double* Lk = Tk.L + (size_t)k0 * n;
-      for (int e = tid; e < NB * 64; e += 256) {
-        const int q = e >> 6, r = e & 63;
-        const bool va = i0 + r < n, vb = j0 + r < n;
-        cp_async8(As + q * SP + r, va ? Lk + i0 + r + (size_t)q * n : Lk, va);
-        cp_async8(Bs + q * SP + r, vb ? Lk + j0 + r + (size_t)q * n : Lk, vb);
-      }
-      cp_async_commit();
-      const int wm = warp & 1, wn = warp >> 1;
-      const int lr = lane >> 2, lc = lane & 3;
-      double* G = Tk.G;
-      cp_async_wait<0>();
-      __syncthreads();
-      double acc[4][2][2];
-#pragma unroll
-      for (int mi = 0; mi < 4; mi++)
-#pragma unroll
-        for (int ni = 0; ni < 2; ni++) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < NB; kk += 4) {
-        double a[4], b[2];
-#pragma unroll
-        for (int mi = 0; mi < 4; mi++) a[mi] = As[(kk + lc) * SP + 32 * wm + 8 * mi + lr];
-#pragma unroll
-        for (int ni = 0; ni < 2; ni++) b[ni] = Bs[(kk + lc) * SP + 16 * wn + 8 * ni + lr];
-#pragma unroll
-        for (int mi = 0; mi < 4; mi++)
-#pragma unroll
-          for (int ni = 0; ni < 2; ni++) dmma8x8x4(acc[mi][ni], a[mi], b[ni]);
-      }
-      // two columns per lane are adjacent in no dimension (column stride n):
-      // one 8-byte access per entry, the loads of a half tile issued together
-#pragma unroll
-      for (int ni = 0; ni < 2; ni++) {
-        double g[4][2];
-#pragma unroll
-        for (int mi = 0; mi < 4; mi++)
-#pragma unroll
-          for (int v = 0; v < 2; v++) {
-            const int i = i0 + 32 * wm + 8 * mi + lr, j = j0 + 16 * wn + 8 * ni + 2 * lc + v;
-            g[mi][v] = (i < n && j < n && i >= j) ? G[i + (size_t)j * n] : 0.0;
-          }
-#pragma unroll
-        for (int mi = 0; mi < 4; mi++)
-#pragma unroll
-          for (int v = 0; v < 2; v++) {
-            const int i = i0 + 32 * wm + 8 * mi + lr, j = j0 + 16 * wn + 8 * ni + 2 * lc + v;
-            if (i < n && j < n && i >= j) G[i + (size_t)j * n] = g[mi][v] - acc[mi][ni][v];
-          }
-      }
-    }
-
     // Persistent form of the trailing update (opt-in, HSSMF_GRAM_SYRK=persist):
     // every CTA walks the lower 64 x 64 tiles of all tasks (stride gridDim.x)
     // and double-buffers them through shared memory, the next tile's G and L
@@ -869,7 +803,7 @@ namespace hssmf_b200 {
         while (tj + 1 < nbt && before(tj + 1) <= t) tj++;
         x.i0 = (tj + (t - before(tj))) * 64;
         x.j0 = tj * 64;
-        x.Lk = Tk.L + (size_t)k0 * x.n;
+        x.Lk = Tk.L + (size_t)(k0 + Tk.kw) * x.n;
         x.G = Tk.G;
         return x;
       };
@@ -954,6 +888,131 @@ namespace hssmf_b200 {
       cp_async_wait<0>();
     }
 
+    // ---- warm start: fixed-order panels -------------------------------------
+    // state of a warm-started task before its first fixed-order panel: the
+    // permutation the earlier ID ended with, residual norms = diag(G), the
+    // first kw positions flagged as pivoted, r11 = the largest diagonal entry
+    // (what the pivot search would have taken first), state = {kw, 0, 0}
+    __global__ void __launch_bounds__(256) gram_warm_init_kernel(const GramTask* __restrict__ tasks) {
+      const GramTask Tk = tasks[blockIdx.x];
+      if (Tk.kw <= 0) return;
+      const int n = Tk.n;
+      double mx = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double g = Tk.G[i + (size_t)i * n];
+        const int p = Tk.warm_pos[i];
+        Tk.dg[i] = g;
+        Tk.pos_of[i] = p;
+        Tk.orig_at[i] = Tk.warm_orig[i];
+        Tk.flag[i] = p < Tk.kw ? 1 : 0;
+        mx = fmax(mx, g);
+      }
+      __shared__ double sm[8];
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; w++) mx = fmax(mx, sm[w]);
+        *Tk.r11 = mx > 0.0 ? sqrt(mx) : 0.0;
+        Tk.state[0] = Tk.kw;
+        Tk.state[1] = 0;
+        Tk.state[2] = 0;
+      }
+    }
+
+    // one fixed-order panel: the NB pivots orig_at[k0 .. k0 + NB) of every task
+    // with kw > k0. Every CTA factors the panel's NB x NB diagonal block of the
+    // (updated) Gram matrix in shared memory, then each thread solves its
+    // row's NB panel entries against it: L(i, k0 + c) = (G(i, p_c) - sum_{q<c}
+    // L(i, q) Lbb(c, q)) / Lbb(c, c), downdates the row's residual norm and
+    // stores the row. No pivot search, no cluster: rows are independent once
+    // the diagonal block is known. Rows pivoted in earlier panels hold 0.
+    // A non-positive pivot (roundoff on a dependent row) stops the task with
+    // state[1] = 3: the host repeats its ID with the pivot search from step 0.
+    template <int NB>
+    __global__ void __launch_bounds__(128) gram_fixed_panel_kernel(const GramTask* __restrict__ tasks,
+                                                                   int k0) {
+      const GramTask Tk = tasks[blockIdx.y];
+      if (k0 >= Tk.kw) return;
+      const int n = Tk.n;
+      const int row0 = blockIdx.x * 128;
+      if (row0 >= n) return;
+      if (__ldcg(Tk.state + 1)) return;
+      __shared__ double Lb[NB][NB + 1];
+      __shared__ int piv[NB];
+      __shared__ int bad;
+      const int tid = threadIdx.x;
+      if (tid < NB) piv[tid] = Tk.orig_at[k0 + tid];
+      if (tid == 0) bad = 0;
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += 128) {
+        const int a = e / NB, c = e % NB;  // a >= c: lower triangle of the diagonal block
+        if (a >= c) {
+          const int pa = piv[a], pc = piv[c];
+          Lb[a][c] = pa >= pc ? Tk.G[pa + (size_t)pc * n] : Tk.G[pc + (size_t)pa * n];
+        }
+      }
+      __syncthreads();
+      // in-place Cholesky of the block (right-looking, column by column)
+      for (int c = 0; c < NB; c++) {
+        const double dcc = Lb[c][c];
+        if (!(dcc > 0.0)) {
+          if (tid == 0) bad = 1;
+        }
+        __syncthreads();
+        if (bad) break;
+        const double l = sqrt(dcc);
+        if (tid > c && tid < NB) Lb[tid][c] /= l;
+        __syncthreads();
+        if (tid == 0) Lb[c][c] = l;
+        for (int e = tid; e < (NB - c - 1) * (NB - c - 1); e += 128) {
+          const int a = c + 1 + e / (NB - c - 1), b = c + 1 + e % (NB - c - 1);
+          if (a >= b) Lb[a][b] -= Lb[a][c] * Lb[b][c];
+        }
+        __syncthreads();
+      }
+      if (bad) {
+        if (blockIdx.x == 0 && tid == 0) {
+          __stcg(Tk.state + 1, 3);
+          __stcg(Tk.state + 2, 0);
+        }
+        return;
+      }
+      const int i = row0 + tid;
+      if (i >= n) return;
+      const int pi = Tk.pos_of[i];
+      double* Li = Tk.L + i + (size_t)k0 * n;
+      if (pi < k0) {  // pivoted in an earlier panel
+#pragma unroll 4
+        for (int c = 0; c < NB; c++) Li[(size_t)c * n] = 0.0;
+        return;
+      }
+      const int own = pi < k0 + NB ? pi - k0 : NB;  // this panel's pivot rows end at their own column
+      double x[NB];
+#pragma unroll
+      for (int c = 0; c < NB; c++) {
+        const int pc = piv[c];
+        x[c] = i >= pc ? Tk.G[i + (size_t)pc * n] : Tk.G[pc + (size_t)i * n];
+      }
+      double dsum = 0.0;
+#pragma unroll
+      for (int c = 0; c < NB; c++) {
+        double v = x[c];
+#pragma unroll
+        for (int q = 0; q < c; q++) v -= x[q] * Lb[c][q];
+        v = c <= own ? v / Lb[c][c] : 0.0;
+        if (c == own) v = Lb[c][c];
+        x[c] = v;
+        dsum += v * v;
+      }
+#pragma unroll
+      for (int c = 0; c < NB; c++) Li[(size_t)c * n] = x[c];
+      if (own == NB) {
+        double dd = Tk.dg[i] - dsum;
+        Tk.dg[i] = dd > 0.0 ? dd : 0.0;
+      }
+    }
+
   }  // namespace
 
   // per-step segment cycles of the panel kernel (measurement knob): wait,
@@ -980,10 +1039,10 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemset(p, 0, sizeof(h)));
   }
 
-  void gram_cholesky_run(const std::vector<GramTask>& tasks, double eps, double abs_tol,
+  void gram_cholesky_run(const std::vector<GramTask>& tasks0, double eps, double abs_tol,
                          cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
                          double* flops, const std::function<void()>& before_sync) {
-    const int nt = (int)tasks.size();
+    const int nt = (int)tasks0.size();
     rank.assign(nt, 0);
     cert.assign(nt, 0);
     if (!nt) return;
@@ -995,9 +1054,17 @@ namespace hssmf_b200 {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemCap));
     });
     int max_n = 0, kmax = 0;
-    for (const auto& t : tasks) {
-      max_n = std::max(max_n, t.n);
-      kmax = std::max(kmax, t.kmax);
+    for (const auto& t : tasks0) max_n = std::max(max_n, t.n);
+    // warm starts need the one-row-per-thread panels (n <= 8192) and whole
+    // panels of fixed pivots
+    std::vector<GramTask> tasks(tasks0);
+    int max_kw = 0;
+    for (auto& t : tasks) {
+      if (max_n > 16 * 512 || getenv("HSSMF_GRAM_V1") || !t.warm_orig || !t.warm_pos) t.kw = 0;
+      t.kw = std::min(t.kw, t.kmax) / kGramPanel * kGramPanel;
+      if (!t.kw) t.warm_orig = t.warm_pos = nullptr;
+      max_kw = std::max(max_kw, t.kw);
+      kmax = std::max(kmax, t.kmax - t.kw);  // steps of the pivot search
     }
     int CL = 1;
     // cluster size: one row per thread up to 16 CTAs (HSSMF_GRAM_MAXCL caps it;
@@ -1048,10 +1115,7 @@ namespace hssmf_b200 {
         HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_persist_kernel<NB2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kSyrkPersistSmem));
-        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_rmw_kernel<NB2, 3>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
-        HSSMF_CUDA(cudaFuncSetAttribute(gram_syrk_rmw_kernel<NB2, 4>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB2 * 68 * 8));
+
       });
       while (CL2 * RPC_MAX < max_n) CL2 *= 2;
       T2 = std::max(32, ((max_n + CL2 - 1) / CL2 + 31) / 32 * 32);
@@ -1065,8 +1129,29 @@ namespace hssmf_b200 {
     // slower on c5: 1.92 TB/s against 2.51 for one tile per CTA, 2 CTAs per SM,
     // profiles/r02/README.md)
     const bool syrk_persist = esy && !strcmp(esy, "persist");
-    const bool syrk_rmw4 = esy && !strcmp(esy, "rmw4");
-    const bool syrk_rmw = esy && (!strcmp(esy, "rmw") || syrk_rmw4);
+    // (a variant that reads and writes the G tile after the products, 64-80
+    // registers and 3-4 CTAs per SM, measured slower: 6.7-8.4 us per step at
+    // n = 7400 against 6.1, tools/gram_bench.py)
+    // warm-started tasks: their first kw pivots as fixed-order panels (one
+    // grid over the rows per panel, no pivot search), each followed by the
+    // trailing update
+    if (v2 && max_kw > 0) {
+      gram_warm_init_kernel<<<nt, 256, 0, s>>>((const GramTask*)d);
+      HSSMF_LAUNCH_CHECK();
+      const int nbt = (max_n + 63) / 64;
+      for (int k0 = 0; k0 < max_kw; k0 += NB2) {
+        gram_fixed_panel_kernel<NB2><<<dim3((max_n + 127) / 128, nt), 128, 0, s>>>((const GramTask*)d, k0);
+        HSSMF_LAUNCH_CHECK();
+        ProbeScope prs(PROBE_GRAM_SYRK, s, 0.0, 0.0);
+        unsigned long long* pb = probe_enabled() ? probe_device_bytes() : nullptr;
+        gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
+            (const GramTask*)d, k0, pb, 1);
+        HSSMF_LAUNCH_CHECK();
+        if (flops)
+          for (const auto& T : tasks)
+            if (k0 < T.kw) *flops += (double)T.n * T.n * NB2;
+      }
+    }
     // all panels are queued without host round trips: a finished task's
     // panel kernel returns at once and its trailing GEMM is skipped on device
     for (int k0 = 0; k0 <= kmax; k0 += nb) {
@@ -1108,23 +1193,17 @@ namespace hssmf_b200 {
             const int grid = std::max(1, std::min(sp.pre[nt], 148));
             gram_syrk_persist_kernel<NB2><<<grid, 256, kSyrkPersistSmem, s>>>(
                 (const GramTask*)d, k0, sp, pb);
-          } else if (syrk_rmw4)
-            gram_syrk_rmw_kernel<NB2, 4><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
-                (const GramTask*)d, k0, pb);
-          else if (syrk_rmw)
-            gram_syrk_rmw_kernel<NB2, 3><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
-                (const GramTask*)d, k0, pb);
-          else if (syrk_cuda_cores)
+          } else if (syrk_cuda_cores)
             gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
                 (const GramTask*)d, k0, pb);
           else
             gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
-                (const GramTask*)d, k0, pb);
+                (const GramTask*)d, k0, pb, 0);
           HSSMF_LAUNCH_CHECK();
         }
         if (flops)
           for (const auto& T : tasks)
-            if (k0 <= T.kmax) *flops += (double)T.n * T.n * NB2;
+            if (k0 + T.kw <= T.kmax) *flops += (double)T.n * T.n * NB2;
         continue;
       }
       cudaLaunchConfig_t cfg = {};
@@ -1170,6 +1249,9 @@ namespace hssmf_b200 {
     for (int t = 0; t < nt; t++) {
       rank[t] = hst[3 * t];
       cert[t] = hst[3 * t + 2];
+      // a fixed-order panel met a non-positive pivot: the caller repeats the
+      // ID without the warm start
+      if (hst[3 * t + 1] == 3) rank[t] = -1;
     }
     if (owned) HSSMF_CUDA(cudaFreeAsync(d, s));
   }

@@ -38,9 +38,22 @@ namespace hssmf_b200 {
     int* state;      // [k, stopped, certified]
     double* r11;     // first pivot norm
     int n, kmax_dim, kmax, kcap;
+    // warm start (v2 panels, n <= 8192): the first kw (a multiple of the panel
+    // width) pivots are taken, in order, from an earlier ID of the same node
+    // (its final orig_at / pos_of arrays) and eliminated as blocked fixed-order
+    // steps; the pivot search resumes at step kw
+    const int* warm_orig = nullptr;
+    const int* warm_pos = nullptr;
+    int kw = 0;
+    // optional: [pivot norm examined at the stop, r11] (how far from the
+    // threshold an ID that hit its cap ended)
+    double* pvlast = nullptr;
   };
+  constexpr int kGramPanel = 48;  // panel width of the one-row-per-thread kernels
 
-  // runs the factorization of all tasks; returns per task (rank, certified)
+  // runs the factorization of all tasks; returns per task (rank, certified);
+  // rank -1: a warm-started task whose fixed-order part broke down (repeat it
+  // with kw = 0)
   // after ONE host sync; before_sync may enqueue more device->host reads
   // that the same sync then covers
   // HSSMF_GRAM_TPROBE=1: per-step segment cycles of the panel kernel

@@ -32,7 +32,7 @@ def run(env_extra):
     env = {k: v for k, v in os.environ.items()
            if k not in ("HSSMF_SPEC_FOLD", "HSSMF_NO_SPEC_SAMPLING", "HSSMF_NO_SYM",
                         "HSSMF_SPEC_ID", "HSSMF_SPEC_ID_ROWS", "HSSMF_SPEC_PEERS",
-                        "HSSMF_LEVEL_PASS")}
+                        "HSSMF_LEVEL_PASS", "HSSMF_WARM_IDS")}
     env.update(env_extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT], capture_output=True, text=True,
                          env=env, timeout=600)
@@ -79,3 +79,16 @@ def test_wavefront_batches_match_level_batches():
     assert level["hss"] > 0
     assert level["rank"] == wave["rank"]
     assert level["x"] == wave["x"]
+
+
+def test_warm_started_id_filter_matches_full_search():
+    # opt-in (HSSMF_WARM_IDS=filter): retries of a failed node run warm first
+    # (the failed ID's pivots in their old order as blocked fixed-order panels,
+    # then the pivot search for the rest); only failures that end at least 25%
+    # above the threshold are taken from the warm ID, everything else is
+    # decided by the full pivot search: ranks and solution are the full search's
+    cold = run({})
+    warm = run({"HSSMF_WARM_IDS": "filter"})
+    assert cold["hss"] > 0 and cold["hss"] == warm["hss"]
+    assert cold["rank"] == warm["rank"]
+    assert cold["x"] == warm["x"]
