@@ -322,8 +322,17 @@ namespace hssmf_b200 {
         return st;
       }
     }
+    // worker streams (the fronts' latency-bound chains of small launches) run
+    // at the highest stream priority, their side streams (speculative sampling
+    // products: full-device TMA GEMMs) at the default, lowest one: a chain's
+    // next small kernel takes the SMs the moment CTAs of another front's
+    // sampling product retire instead of queueing behind its whole grid
+    // (HSSMF_NO_PRIO=1: all streams at the default priority)
     cudaStream_t st;
-    HSSMF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int least = 0, greatest = 0;
+    HSSMF_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    static const bool no_prio = getenv("HSSMF_NO_PRIO") != nullptr;
+    HSSMF_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, no_prio ? least : greatest));
     return st;
   }
   void worker_stream_give(int device, cudaStream_t st) {

@@ -5,6 +5,7 @@
 // launch covers all problems of a batch: blockIdx.x enumerates tiles, the
 // owning problem is found by binary search over the tile prefix.
 #include "gemm.cuh"
+#include "staging.cuh"
 
 #include <cstdlib>
 #include <cstring>
@@ -354,8 +355,11 @@ namespace hssmf_b200 {
         pr.tiles = tiles;
         pr.kmax = km;
         pr.nprob = b.nprob;
-        if (small) gemm_param_kernel<SM_BM, SM_BN><<<tiles, THREADS, SMEM_SMALL, s>>>(b);
-        else gemm_param_kernel<BM, BN><<<tiles, THREADS, SMEM, s>>>(b);
+        // (full-device launches of a worker stream go through its
+        // low-priority lane, staging.cuh)
+        BigLaunch bl(s, !small && tiles >= 2 * 148);
+        if (small) gemm_param_kernel<SM_BM, SM_BN><<<tiles, THREADS, SMEM_SMALL, bl.stream()>>>(b);
+        else gemm_param_kernel<BM, BN><<<tiles, THREADS, SMEM, bl.stream()>>>(b);
         HSSMF_LAUNCH_CHECK();
       }
       b.nprob = 0;

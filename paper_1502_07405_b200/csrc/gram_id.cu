@@ -1144,8 +1144,11 @@ namespace hssmf_b200 {
         HSSMF_LAUNCH_CHECK();
         ProbeScope prs(PROBE_GRAM_SYRK, s, 0.0, 0.0);
         unsigned long long* pb = probe_enabled() ? probe_device_bytes() : nullptr;
-        gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
-            (const GramTask*)d, k0, pb, 1);
+        {
+          BigLaunch bl(s, (long long)nbt * (nbt + 1) / 2 * nt >= 2 * 148);
+          gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, bl.stream()>>>(
+              (const GramTask*)d, k0, pb, 1);
+        }
         HSSMF_LAUNCH_CHECK();
         if (flops)
           for (const auto& T : tasks)
@@ -1196,9 +1199,11 @@ namespace hssmf_b200 {
           } else if (syrk_cuda_cores)
             gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
                 (const GramTask*)d, k0, pb);
-          else
-            gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, s>>>(
+          else {
+            BigLaunch bl(s, (long long)nbt * (nbt + 1) / 2 * nt >= 2 * 148);
+            gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, bl.stream()>>>(
                 (const GramTask*)d, k0, pb, 0);
+          }
           HSSMF_LAUNCH_CHECK();
         }
         if (flops)

@@ -64,6 +64,34 @@ namespace hssmf_b200 {
   // threads' CUDA calls; a pinned one does not)
   void d2h(void* dst, const void* src, size_t n, cudaStream_t s);
 
+  // Low-priority lane of a high-priority worker stream. The fronts of one tree
+  // level run concurrently, each a chain of small, latency-bound launches
+  // (pivot panels, index copies, small GEMMs) interleaved with full-device
+  // kernels (big GEMMs, Gram trailing updates). At equal priority a small
+  // kernel queues behind every CTA the other fronts' big grids still have to
+  // dispatch. Worker streams therefore run at the highest priority and send
+  // their big kernels through a lowest-priority lane: BigLaunch orders the
+  // lane after everything enqueued on the worker stream (fork event) and the
+  // worker stream after the kernel (join event), so the stream's order of
+  // operations is unchanged; only the CTA dispatch priority differs.
+  // The priorities alone are the default; the lanes are opt-in (HSSMF_LANES=1,
+  // measured slower, see low_lane_for). HSSMF_NO_PRIO=1: every stream at the
+  // default priority.
+  struct LowLane {
+    cudaStream_t lo = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+  };
+  LowLane* low_lane_for(cudaStream_t s);  // nullptr unless s is a high-priority stream
+  struct BigLaunch {
+    cudaStream_t s;
+    LowLane* lane;
+    BigLaunch(cudaStream_t st, bool big);
+    ~BigLaunch();
+    cudaStream_t stream() const { return lane ? lane->lo : s; }
+    BigLaunch(const BigLaunch&) = delete;
+    BigLaunch& operator=(const BigLaunch&) = delete;
+  };
+
   // process-wide ring per stream (created on first use)
   Staging* staging_for(cudaStream_t s);
   // thread-local current staging ring
