@@ -36,6 +36,78 @@ namespace hssmf_b200 {
   namespace {
     constexpr int NB = 32;  // LU panel width (reference lu_recursive base, lu.hpp:51)
 
+    // Device blocks of a destroyed engine wait on a per-device list for the
+    // next engine: a user who factors one matrix after another (the end-to-end
+    // bench step) allocates the same sizes again, and cudaMalloc / cudaFree of
+    // ~100 GB cost tenths of a second per engine (cudaFree also synchronizes the
+    // device). Only blocks of >= 1 MB are kept, sizes are rounded to 2 MB, the
+    // list is emptied when an allocation fails, when it would hold more than
+    // half of the device memory, and at the end of every analyze() (so that
+    // only blocks the next engine actually reuses outlive it).
+    struct DevBlockCache {
+      std::mutex mu;
+      std::multimap<size_t, void*> blocks;
+      size_t bytes = 0;
+    };
+    DevBlockCache& dev_cache() {
+      static DevBlockCache* c = new DevBlockCache[64];  // never destroyed
+      int dev = 0;
+      cudaGetDevice(&dev);
+      return c[dev & 63];
+    }
+    size_t dev_round(size_t b) { return b >= (1u << 20) ? (b + (2u << 20) - 1) / (2u << 20) * (2u << 20) : b; }
+    void dev_cache_purge() {
+      DevBlockCache& c = dev_cache();
+      std::lock_guard<std::mutex> lk(c.mu);
+      for (auto& kv : c.blocks) cudaFree(kv.second);
+      c.blocks.clear();
+      c.bytes = 0;
+    }
+    void* dev_block_take(size_t b) {
+      static const bool off = getenv("HSSMF_NO_DEV_CACHE") != nullptr;
+      const size_t r = dev_round(b);
+      if (!off && r >= (1u << 20)) {
+        DevBlockCache& c = dev_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.blocks.find(r);
+        if (it != c.blocks.end()) {
+          void* p = it->second;
+          c.blocks.erase(it);
+          c.bytes -= r;
+          return p;
+        }
+      }
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, r);
+      if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        dev_cache_purge();
+        e = cudaMalloc(&p, r);
+      }
+      HSSMF_CUDA(e);
+      return p;
+    }
+    void dev_block_give(void* p, size_t b) {
+      static const bool off = getenv("HSSMF_NO_DEV_CACHE") != nullptr;
+      const size_t r = dev_round(b);
+      if (off || r < (1u << 20)) {
+        cudaFree(p);
+        return;
+      }
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      DevBlockCache& c = dev_cache();
+      bool purge = false;
+      {
+        std::lock_guard<std::mutex> lk(c.mu);
+        purge = c.bytes + r > tot / 2;
+      }
+      if (purge) dev_cache_purge();
+      std::lock_guard<std::mutex> lk(c.mu);
+      c.blocks.emplace(r, p);
+      c.bytes += r;
+    }
+
     struct DevMem {
       void* p = nullptr;
       size_t bytes = 0;
@@ -54,11 +126,11 @@ namespace hssmf_b200 {
       }
       void alloc(size_t b) {
         free();
-        if (b) HSSMF_CUDA(cudaMalloc(&p, b));
+        if (b) p = dev_block_take(b);
         bytes = b;
       }
       void free() {
-        if (p) cudaFree(p);
+        if (p) dev_block_give(p, bytes);
         p = nullptr;
         bytes = 0;
       }
@@ -344,6 +416,10 @@ namespace hssmf_b200 {
   Engine::~Engine() {
     cudaSetDevice(device_);
     auto hs = d_->hstreams;
+    // (freed blocks go to the device block list without cudaFree's implicit
+    // synchronization: nothing of this engine may still run)
+    for (auto st : hs) cudaStreamSynchronize(st);
+    if (stream_) cudaStreamSynchronize(stream_);
     d_.reset();
     for (auto st : hs) worker_stream_give(device_, st);
     if (stream_) worker_stream_give(device_, stream_);
@@ -351,6 +427,8 @@ namespace hssmf_b200 {
 
   void Engine::analyze(const Csr& a, const Etree& t, const Options& o, const char* owned) {
     HSSMF_CUDA(cudaSetDevice(device_));
+    const double t_an0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    auto devmem_bytes_public = [&] { return (double)d_->devmem_bytes(); };
     auto& D = *d_;
     if (a.n != t.n) throw SolverFailure(1, -1, -1, "mf factor: matrix and tree sizes differ");
     D.a = a;
@@ -391,18 +469,24 @@ namespace hssmf_b200 {
       upd_off[i] = upd_all.size();
       upd_all.insert(upd_all.end(), D.t.nodes[i].upd.begin(), D.t.nodes[i].upd.end());
     }
-    auto local = [&](const FrontNode& f, int g) {
-      if (g < f.sep_end) return g - f.sep_begin;
-      auto it = std::lower_bound(f.upd.begin(), f.upd.end(), g);
-      return f.ns() + (int)(it - f.upd.begin());
-    };
     for (int i = 0; i < nn; i++) {
       const auto& f = D.t.nodes[i];
       for (int slot = 0; slot < 2; slot++) {
         const int c = slot ? f.child1 : f.child0;
         if (c < 0) continue;
         (slot ? pos_off1 : pos_off0)[i] = pos_all.size();
-        for (int g : D.t.nodes[c].upd) pos_all.push_back(local(f, g));
+        // both index lists ascend: one merge instead of a search per entry
+        // (10 M entries on c5)
+        size_t it = 0;
+        const int ns_f = f.ns();
+        for (int g : D.t.nodes[c].upd) {
+          if (g < f.sep_end) {
+            pos_all.push_back(g - f.sep_begin);
+            continue;
+          }
+          while (it < f.upd.size() && f.upd[it] < g) it++;
+          pos_all.push_back(ns_f + (int)it);
+        }
       }
     }
     upload(D.d_upd, upd_all);
@@ -649,6 +733,13 @@ namespace hssmf_b200 {
       st.rank = 0;
       st.type = 0;
       st.flops = dense_front_flops(f.ns(), f.nu());
+    }
+    // blocks of an earlier engine that this one did not take are released now
+    dev_cache_purge();
+    if (getenv("HSSMF_DEBUG_AN")) {
+      const double t1 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      fprintf(stderr, "[hssmf] analyze (maps, plans, device storage %.1f GB): %.3f s\n",
+              devmem_bytes_public() / 1e9, t1 - t_an0);
     }
   }
 
