@@ -719,13 +719,27 @@ def main():
                      frac=ach / peaks["hbm_gbs"], peak_src=peaks["hbm_src"],
                      algorithmic="16 B per lower-triangle Gram element per panel (read + write)")
         else:
-            # a panel launch runs at most 32 dependent pivot steps
-            e.update(bound="latency", us_per_pivot_step=round(e["avg_launch_us"] / 32, 3),
+            # a panel launch runs at most 48 dependent pivot steps
+            e.update(bound="latency", us_per_pivot_step=round(e["avg_launch_us"] / 48, 3),
                      note="pivot chain: one cluster-wide argmax per elimination step; "
-                          "us_per_pivot_step = avg launch / 32 steps (an upper bound when "
+                          "us_per_pivot_step = avg launch / 48 steps (an upper bound when "
                           "tasks stop inside a panel)")
         e["traffic"] = TRAFFIC.get(name)
         roofs.append(e)
+    # the assembly kernels (north_star (1)): bracketed per level by CUDA events on
+    # the engine stream, algorithmic bytes from the analysis (extend-add:
+    # 24 B per child update entry + 4 B per child row)
+    for k in ks:
+        if k["name"] in ("extend_add", "assemble_sparse") and k["ms"] > 0 and k["bytes"] > 0:
+            ach = k["bytes"] / (k["ms"] * 1e-3) / 1e9
+            roofs.append({"kernel": k["name"], "launches": k["launches"], "ms": round(k["ms"], 2),
+                          "avg_launch_us": round(1e3 * k["ms"] / k["launches"], 2),
+                          "share_of_step": k["ms"] / tot_ms, "bound": "hbm", "achieved": ach,
+                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                          "peak_src": peaks["hbm_src"],
+                          "algorithmic": "extend-add: 24 B per child update entry + 4 B per child row; "
+                                         "sparse assembly: 28 B per owned entry + the zeroing of the level",
+                          "traffic": TRAFFIC.get(k["name"])})
     roofs.sort(key=lambda e: -e["ms"])
     dom = [e for e in roofs if e.get("bound") in ("tensor", "hbm")]
     roof = dict(dom[0]) if dom else {"kernel": None}

@@ -1039,6 +1039,14 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemset(p, 0, sizeof(h)));
   }
 
+  namespace {
+    // HSSMF_LANES=1: GEMMs only; HSSMF_LANES=all: the Gram trailing updates too
+    bool lanes_for_syrk() {
+      static const bool v = getenv("HSSMF_LANES") && !strcmp(getenv("HSSMF_LANES"), "all");
+      return v;
+    }
+  }  // namespace
+
   void gram_cholesky_run(const std::vector<GramTask>& tasks0, double eps, double abs_tol,
                          cudaStream_t s, std::vector<int>& rank, std::vector<int>& cert,
                          double* flops, const std::function<void()>& before_sync) {
@@ -1145,7 +1153,7 @@ namespace hssmf_b200 {
         ProbeScope prs(PROBE_GRAM_SYRK, s, 0.0, 0.0);
         unsigned long long* pb = probe_enabled() ? probe_device_bytes() : nullptr;
         {
-          BigLaunch bl(s, (long long)nbt * (nbt + 1) / 2 * nt >= 2 * 148);
+          BigLaunch bl(s, lanes_for_syrk() && (long long)nbt * (nbt + 1) / 2 * nt >= 2 * 148);
           gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, bl.stream()>>>(
               (const GramTask*)d, k0, pb, 1);
         }
@@ -1200,7 +1208,7 @@ namespace hssmf_b200 {
             gram_syrk_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 64 * 8, s>>>(
                 (const GramTask*)d, k0, pb);
           else {
-            BigLaunch bl(s, (long long)nbt * (nbt + 1) / 2 * nt >= 2 * 148);
+            BigLaunch bl(s, lanes_for_syrk() && (long long)nbt * (nbt + 1) / 2 * nt >= 2 * 148);
             gram_syrk_dmma_kernel<NB2><<<dim3(nbt * (nbt + 1) / 2, nt), 256, 2 * NB2 * 68 * 8, bl.stream()>>>(
                 (const GramTask*)d, k0, pb, 0);
           }

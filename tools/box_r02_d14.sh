@@ -8,3 +8,5 @@ d=json.loads(open('gpurun_out/d14_bench_$tag.json').read().strip().splitlines()[
 run cache HSSMF_DEBUG_AN=1
 run nocache HSSMF_NO_DEV_CACHE=1
 run cache2 A=1
+run lanes_gemm HSSMF_LANES=1
+run lanes_all HSSMF_LANES=all
