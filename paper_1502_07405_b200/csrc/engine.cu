@@ -36,78 +36,6 @@ namespace hssmf_b200 {
   namespace {
     constexpr int NB = 32;  // LU panel width (reference lu_recursive base, lu.hpp:51)
 
-    // Device blocks of a destroyed engine wait on a per-device list for the
-    // next engine: a user who factors one matrix after another (the end-to-end
-    // bench step) allocates the same sizes again, and cudaMalloc / cudaFree of
-    // ~100 GB cost tenths of a second per engine (cudaFree also synchronizes the
-    // device). Only blocks of >= 1 MB are kept, sizes are rounded to 2 MB, the
-    // list is emptied when an allocation fails, when it would hold more than
-    // half of the device memory, and at the end of every analyze() (so that
-    // only blocks the next engine actually reuses outlive it).
-    struct DevBlockCache {
-      std::mutex mu;
-      std::multimap<size_t, void*> blocks;
-      size_t bytes = 0;
-    };
-    DevBlockCache& dev_cache() {
-      static DevBlockCache* c = new DevBlockCache[64];  // never destroyed
-      int dev = 0;
-      cudaGetDevice(&dev);
-      return c[dev & 63];
-    }
-    size_t dev_round(size_t b) { return b >= (1u << 20) ? (b + (2u << 20) - 1) / (2u << 20) * (2u << 20) : b; }
-    void dev_cache_purge() {
-      DevBlockCache& c = dev_cache();
-      std::lock_guard<std::mutex> lk(c.mu);
-      for (auto& kv : c.blocks) cudaFree(kv.second);
-      c.blocks.clear();
-      c.bytes = 0;
-    }
-    void* dev_block_take(size_t b) {
-      static const bool off = getenv("HSSMF_NO_DEV_CACHE") != nullptr;
-      const size_t r = dev_round(b);
-      if (!off && r >= (1u << 20)) {
-        DevBlockCache& c = dev_cache();
-        std::lock_guard<std::mutex> lk(c.mu);
-        auto it = c.blocks.find(r);
-        if (it != c.blocks.end()) {
-          void* p = it->second;
-          c.blocks.erase(it);
-          c.bytes -= r;
-          return p;
-        }
-      }
-      void* p = nullptr;
-      cudaError_t e = cudaMalloc(&p, r);
-      if (e == cudaErrorMemoryAllocation) {
-        cudaGetLastError();
-        dev_cache_purge();
-        e = cudaMalloc(&p, r);
-      }
-      HSSMF_CUDA(e);
-      return p;
-    }
-    void dev_block_give(void* p, size_t b) {
-      static const bool off = getenv("HSSMF_NO_DEV_CACHE") != nullptr;
-      const size_t r = dev_round(b);
-      if (off || r < (1u << 20)) {
-        cudaFree(p);
-        return;
-      }
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      DevBlockCache& c = dev_cache();
-      bool purge = false;
-      {
-        std::lock_guard<std::mutex> lk(c.mu);
-        purge = c.bytes + r > tot / 2;
-      }
-      if (purge) dev_cache_purge();
-      std::lock_guard<std::mutex> lk(c.mu);
-      c.blocks.emplace(r, p);
-      c.bytes += r;
-    }
-
     struct DevMem {
       void* p = nullptr;
       size_t bytes = 0;
@@ -126,11 +54,11 @@ namespace hssmf_b200 {
       }
       void alloc(size_t b) {
         free();
-        if (b) p = dev_block_take(b);
+        if (b) HSSMF_CUDA(cudaMalloc(&p, b));
         bytes = b;
       }
       void free() {
-        if (p) dev_block_give(p, bytes);
+        if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
       }
@@ -416,10 +344,6 @@ namespace hssmf_b200 {
   Engine::~Engine() {
     cudaSetDevice(device_);
     auto hs = d_->hstreams;
-    // (freed blocks go to the device block list without cudaFree's implicit
-    // synchronization: nothing of this engine may still run)
-    for (auto st : hs) cudaStreamSynchronize(st);
-    if (stream_) cudaStreamSynchronize(stream_);
     d_.reset();
     for (auto st : hs) worker_stream_give(device_, st);
     if (stream_) worker_stream_give(device_, stream_);
@@ -429,6 +353,8 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaSetDevice(device_));
     const double t_an0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     auto devmem_bytes_public = [&] { return (double)d_->devmem_bytes(); };
+    auto now_s = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t_an[6] = {t_an0, 0, 0, 0, 0, 0};
     auto& D = *d_;
     if (a.n != t.n) throw SolverFailure(1, -1, -1, "mf factor: matrix and tree sizes differ");
     D.a = a;
@@ -465,6 +391,10 @@ namespace hssmf_b200 {
     // multifrontal.hpp:67-94)
     std::vector<int> upd_all, pos_all;
     std::vector<long long> upd_off(nn), pos_off0(nn, -1), pos_off1(nn, -1);
+    size_t upd_total = 0;
+    for (int i = 0; i < nn; i++) upd_total += D.t.nodes[i].upd.size();
+    upd_all.reserve(upd_total);
+    pos_all.reserve(upd_total);
     for (int i = 0; i < nn; i++) {
       upd_off[i] = upd_all.size();
       upd_all.insert(upd_all.end(), D.t.nodes[i].upd.begin(), D.t.nodes[i].upd.end());
@@ -491,6 +421,7 @@ namespace hssmf_b200 {
     }
     upload(D.d_upd, upd_all);
     upload(D.d_pos, pos_all);
+    t_an[1] = now_s();
 
     // HSS selection (multifrontal.hpp:410-412)
     D.want_hss.assign(nn, 0);
@@ -571,6 +502,7 @@ namespace hssmf_b200 {
       boff += D.t.nodes[c].nu();
     }
     D.bupd_total = boff;
+    t_an[2] = now_s();
     D.persist.alloc(std::max<size_t>(poff, 256));
     D.ipersist.alloc(std::max<size_t>(ipoff * sizeof(int), 256));
     D.trans[0].alloc(std::max<size_t>(cmax[0], 256));
@@ -627,6 +559,7 @@ namespace hssmf_b200 {
       gpre.insert(gpre.end(), pre.begin(), pre.end());
       return b;
     };
+    t_an[3] = now_s();
     for (int L = nlev - 1; L >= 0; L--) {
       auto& P = D.levels[L];
       std::vector<int> dl;
@@ -706,6 +639,7 @@ namespace hssmf_b200 {
       P.flops_schur = gemm_flops(probs);
       P.schur = add_batch(probs);
     }
+    t_an[4] = now_s();
     upload(D.d_colpre, colpre);
     upload(D.d_gemm, gp);
     upload(D.d_gpre, gpre);
@@ -734,12 +668,12 @@ namespace hssmf_b200 {
       st.type = 0;
       st.flops = dense_front_flops(f.ns(), f.nu());
     }
-    // blocks of an earlier engine that this one did not take are released now
-    dev_cache_purge();
     if (getenv("HSSMF_DEBUG_AN")) {
       const double t1 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-      fprintf(stderr, "[hssmf] analyze (maps, plans, device storage %.1f GB): %.3f s\n",
-              devmem_bytes_public() / 1e9, t1 - t_an0);
+      fprintf(stderr, "[hssmf] analyze (device storage %.1f GB): %.3f s = copies + maps %.3f, layout %.3f, "
+                      "allocation %.3f, level plans %.3f, uploads + stats %.3f\n",
+              devmem_bytes_public() / 1e9, t1 - t_an0, t_an[1] - t_an[0], t_an[2] - t_an[1],
+              t_an[3] - t_an[2], t_an[4] - t_an[3], t1 - t_an[4]);
     }
   }
 

@@ -32,6 +32,41 @@ def test_gemm_matches_fp64(ta, tb, m, n, k):
     assert np.abs(got - want).max() <= tol
 
 
+def test_transposed_operands_on_the_tma_kernel():
+    # transposed operands run on the 64 x 64 kernel by default;
+    # HSSMF_TMA_TRANS=1 sends them to the TMA kernel, whose T/N, N/T and T/T
+    # variants stay covered here (values and bitwise repeatability)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_1502_07405_b200.api as A
+rng = np.random.default_rng(3)
+for (ta, tb, m, n, k) in [("T", "N", 640, 128, 4096), ("N", "T", 258, 130, 2302), ("T", "T", 384, 256, 2048)]:
+    a = rng.standard_normal((m, k) if ta == "N" else (k, m))
+    b = rng.standard_normal((k, n) if tb == "N" else (n, k))
+    c = rng.standard_normal((m, n))
+    got = A.dev_gemm(ta, tb, -0.5, a, b, 2.0, c)
+    again = A.dev_gemm(ta, tb, -0.5, a, b, 2.0, c)
+    oa = a if ta == "N" else a.T
+    ob = b if tb == "N" else b.T
+    want = -0.5 * oa @ ob + 2.0 * c
+    tol = 8 * k * np.finfo(float).eps * (np.abs(oa) @ np.abs(ob) + np.abs(c)).max()
+    assert np.abs(got - want).max() <= tol, (ta, tb, m, n, k)
+    assert np.array_equal(got, again), (ta, tb, m, n, k)
+print("ok")
+''' % root
+    env = dict(os.environ, HSSMF_TMA_TRANS="1")
+    env.pop("HSSMF_NO_TMA", None)
+    out = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, env=env,
+                         timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
 def test_gemm_beta_zero_ignores_nan():
     a = np.ones((9, 4))
     b = np.ones((4, 6))
