@@ -440,9 +440,15 @@ namespace hssmf_b200 {
       const char* e = getenv("HSSMF_REGION");
       return e && e[0] == '1';
     }();
-    if (use_region && !partial)
+    // HSSMF_REGION_LEVEL=k: only tree levels <= k run dependency-driven (the
+    // few top fronts, where a parent can start while its cousins still run);
+    // deeper levels keep their level barriers
+    static const int region_top = getenv("HSSMF_REGION_LEVEL") ? atoi(getenv("HSSMF_REGION_LEVEL")) : -1;
+    if ((use_region || region_top >= 0) && !partial) {
       for (int i = 0; i < nn; i++)
         if (D.want_hss[i]) D.region_level = std::max(D.region_level, D.t.nodes[i].level);
+      if (region_top >= 0 && D.region_level >= 0) D.region_level = std::min(D.region_level, region_top);
+    }
     D.lv.assign(nlev, {});
     auto& lv = D.lv;
     for (int i = 0; i < nn; i++)
