@@ -113,7 +113,8 @@ namespace hssmf_b200 {
   };
 
   struct Engine::Impl {
-    Csr a;
+    Csr a;           // sizes only (analyze)
+    size_t nnz = 0;  // entries of the matrix on the device
     Etree t;
     Options opt;
     std::vector<FrontDev> hf, hf0;  // live descriptors, analysis-time descriptors
@@ -357,7 +358,11 @@ namespace hssmf_b200 {
     double t_an[6] = {t_an0, 0, 0, 0, 0, 0};
     auto& D = *d_;
     if (a.n != t.n) throw SolverFailure(1, -1, -1, "mf factor: matrix and tree sizes differ");
-    D.a = a;
+    // (only the sizes of the matrix are kept on the host: its arrays go to the
+    // device below, and a 128^3 copy is 180 MB per call)
+    D.a = Csr();
+    D.a.n = a.n;
+    D.nnz = a.val.size();
     D.t = t;
     D.t.compute_levels();
     D.opt = o;
@@ -685,7 +690,7 @@ namespace hssmf_b200 {
 
   void Engine::set_values(const double* val, bool on_device) {
     auto& D = *d_;
-    HSSMF_CUDA(cudaMemcpyAsync(D.d_val.p, val, D.a.val.size() * sizeof(double),
+    HSSMF_CUDA(cudaMemcpyAsync(D.d_val.p, val, D.nnz * sizeof(double),
                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                stream_));
     factored_ = false;
