@@ -298,6 +298,8 @@ namespace hssmf_b200 {
     HSSMF_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
     int nw = 8;
     if (const char* e = getenv("HSSMF_HSS_STREAMS")) nw = std::max(1, atoi(e));
+    // HSSMF_HSS_STREAMS_SMALL=n: width of the levels whose fronts are all < 9000 rows
+    if (const char* e = getenv("HSSMF_HSS_STREAMS_SMALL")) nw = std::max(nw, atoi(e));
     for (int w = 0; w < nw; w++) d_->hstreams.push_back(worker_stream_take(device));
   }
 
@@ -895,7 +897,9 @@ namespace hssmf_b200 {
     // (measured on c5: 4 -> 9.01 s, 6 -> 8.81 s, 8 -> 8.84 s per step)
     int mmax = 0;
     for (int i : lst) mmax = std::max(mmax, t.nodes[i].m());
-    size_t width = mmax >= 9000 ? std::min<size_t>(6, hstreams.size()) : hstreams.size();
+    static const int small_w = getenv("HSSMF_HSS_STREAMS_SMALL") ? atoi(getenv("HSSMF_HSS_STREAMS_SMALL")) : 8;
+    size_t width = mmax >= 9000 ? std::min<size_t>(6, hstreams.size())
+                                : std::min<size_t>(std::max(1, small_w), hstreams.size());
     if (const char* e = getenv("HSSMF_HSS_STREAMS")) width = std::max(1, atoi(e));
     const int nw = (int)std::min<size_t>(lst.size(), std::min(width, hstreams.size()));
     std::vector<HssResult> res(lst.size());
