@@ -278,7 +278,12 @@ namespace hssmf_b200 {
     GemmProblem pt = p0;
     gemm_set_op(pt, ta, tb, alpha, beta);
     const bool tma = gemm_tma_aligned(pt) && p0.k >= 2048;
-    const int S = gemm_splitk_factor(p0.m, p0.n, p0.k, tma);
+    int S = gemm_splitk_factor(p0.m, p0.n, p0.k, tma);
+    // HSSMF_SPLITK_KSLICE=k: slices of at most k (>= 512) of K on the TMA
+    // kernel: its CTAs hold a whole SM each (164 KB of shared memory), so
+    // shorter CTAs return SMs to the other fronts' latency-bound chains sooner
+    static const int kslice = getenv("HSSMF_SPLITK_KSLICE") ? std::max(512, atoi(getenv("HSSMF_SPLITK_KSLICE"))) : 0;
+    if (tma && kslice > 0) S = std::max(S, std::min(ceil_div(p0.k, kslice), 64));
     if (S <= 1) {
       gemm_run_host({p0}, ta, tb, alpha, beta, s);
       return;
