@@ -898,7 +898,8 @@ namespace hssmf_b200 {
     int mmax = 0;
     for (int i : lst) mmax = std::max(mmax, t.nodes[i].m());
     static const int small_w = getenv("HSSMF_HSS_STREAMS_SMALL") ? atoi(getenv("HSSMF_HSS_STREAMS_SMALL")) : 8;
-    size_t width = mmax >= 9000 ? std::min<size_t>(6, hstreams.size())
+    static const int big_w = getenv("HSSMF_HSS_STREAMS_BIG") ? atoi(getenv("HSSMF_HSS_STREAMS_BIG")) : 6;
+    size_t width = mmax >= 9000 ? std::min<size_t>(std::max(1, big_w), hstreams.size())
                                 : std::min<size_t>(std::max(1, small_w), hstreams.size());
     if (const char* e = getenv("HSSMF_HSS_STREAMS")) width = std::max(1, atoi(e));
     const int nw = (int)std::min<size_t>(lst.size(), std::min(width, hstreams.size()));
